@@ -1,0 +1,114 @@
+"""ctypes wrapper for oracle/papg_oracle.c -- TEST INFRASTRUCTURE ONLY (see oracle/__init__.py)."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "papg_oracle.c")
+_SO = os.path.join(_HERE, "libpapg_oracle.so")
+_lib = None
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile the fp64 oracle: gcc -O2 -fopenmp (no -ffast-math, no intrinsics)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               _SRC, "-o", _SO, "-lm"])
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        L = C.CDLL(_SO)
+        i64, i32, d = C.c_int64, C.c_int, C.c_double
+        dpn = C.c_void_p  # nullable double*
+        L.oracle_papg.argtypes = [i64, i32, _dp, _dp, d, d, i64, _dp, _dp, C.POINTER(d), dpn, dpn, i32]
+        L.oracle_eta.argtypes = [i64, i32, _dp, _dp, d, _dp, _dp, _dp, i32]
+        L.oracle_stats.argtypes = [i64, i32, _dp, _dp, d, dpn, _dp, _dp, _dp, i32]
+        L.oracle_project_rows.argtypes = [i64, i32, _dp, _dp, _dp, d, _ip, i64, _dp, _dp, i32]
+        for f in (L.oracle_papg, L.oracle_eta, L.oracle_stats, L.oracle_project_rows):
+            f.restype = C.c_int
+        L.oracle_max_threads.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def momentum_next(t: float) -> float:
+    """Step 3 of Fig. 2: t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2."""
+    return (1.0 + math.sqrt(1.0 + 4.0 * t * t)) / 2.0
+
+
+def papg(X, ybar, gamma, L, K, Tprev=None, Tt=None, t=1.0, nthreads=0):
+    """Run K P-APG iterations (Fig. 2) from state (theta^{k-1}, theta~^k, t_k).
+
+    Defaults are the paper's start: theta^0 = 0, theta~^1 = theta^0, t_1 = 1.
+    Returns dict(Tprev=theta^{last}, Tt=theta~^{last+1}, t=t_{last+1}, y, xi) where
+    (y, xi) = eta of the last iteration's Step 1.
+    """
+    X = _c64(X)
+    ybar = _c64(ybar)
+    N, n = X.shape
+    Tprev = np.zeros((N, N)) if Tprev is None else _c64(Tprev).copy()
+    Tt = Tprev.copy() if Tt is None else _c64(Tt).copy()
+    y = np.zeros(N)
+    xi = np.zeros((N, n))
+    tt = C.c_double(float(t))
+    rc = lib().oracle_papg(N, n, X, ybar, float(gamma), float(L), int(K), Tprev, Tt, C.byref(tt),
+                           y.ctypes.data, xi.ctypes.data, int(nthreads))
+    if rc:
+        raise MemoryError("oracle_papg allocation failed")
+    return dict(Tprev=Tprev, Tt=Tt, t=tt.value, y=y, xi=xi)
+
+
+def eta(X, ybar, gamma, T, nthreads=0):
+    """eta(Theta) = Step-1 minimizer at Theta (Theorem 1); returns (y, xi)."""
+    X = _c64(X)
+    N, n = X.shape
+    y = np.zeros(N)
+    xi = np.zeros((N, n))
+    rc = lib().oracle_eta(N, n, X, _c64(ybar), float(gamma), _c64(T), y, xi, int(nthreads))
+    if rc:
+        raise MemoryError("oracle_eta allocation failed")
+    return y, xi
+
+
+def stats(X, ybar, gamma, T, y, xi, nthreads=0):
+    """dict(r_gamma, g, gap, max_violation, infeas_norm) -- see papg_oracle.c oracle_stats."""
+    X = _c64(X)
+    N, n = X.shape
+    out = np.zeros(5)
+    Tp = None if T is None else _c64(T)
+    rc = lib().oracle_stats(N, n, X, _c64(ybar), float(gamma), None if Tp is None else Tp.ctypes.data,
+                            _c64(y), _c64(xi).reshape(N, n), out, int(nthreads))
+    if rc:
+        raise MemoryError("oracle_stats allocation failed")
+    return dict(r_gamma=out[0], g=out[1], gap=out[2], max_violation=out[3], infeas_norm=out[4])
+
+
+def project_rows(X, y, xi, L, rows, Tt_rows, nthreads=0):
+    """Step 2 for selected rows given eta^k and the rows of theta~^k."""
+    X = _c64(X)
+    N, n = X.shape
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros((len(rows), N))
+    lib().oracle_project_rows(N, n, X, _c64(y), _c64(xi).reshape(N, n), float(L), rows, len(rows),
+                              _c64(Tt_rows).reshape(len(rows), N), out, int(nthreads))
+    return out

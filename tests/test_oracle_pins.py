@@ -1,0 +1,344 @@
+"""Pins for the fp64 oracle (oracle/) against what the paper and mathematics fix.
+
+Each test names the pin of SURVEY.md §8(c) / DESIGN.md §Oracle it implements.
+None of these tests touch the GPU path.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import crdata
+import oracle
+from oracle import ref
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _tiny(N, n, seed=0, noise=0.3):
+    return crdata.random_problem(N, n, seed=seed, noise_sd=noise)
+
+
+# ---------------------------------------------------------------- P2 operators
+def test_spec_worked_operator_values():
+    """SPEC.md S:51, S:61, S:69 worked values for the dense Def. A1A2 construction."""
+    g = _gold("spec_operator_examples.json")
+    A1 = ref.dense_A1(2)
+    np.testing.assert_array_equal(A1 @ np.array(g["A1_y"]["y"]), g["A1_y"]["expect"])
+    np.testing.assert_array_equal(A1.T @ np.array(g["A1T_z"]["z"]), g["A1T_z"]["expect"])
+    A2 = ref.dense_A2(np.array(g["A2_xi"]["X"]))
+    np.testing.assert_array_equal(A2 @ np.array(g["A2_xi"]["xi"]), g["A2_xi"]["expect"])
+
+
+@pytest.mark.parametrize("N,n", [(3, 1), (5, 2), (7, 3)])
+def test_dense_rows_are_pair_constraints(N, n):
+    """Row (l1,l2) of A1 y + A2 xi equals y_l2 - y_l1 + xi_l1^T (x_l1 - x_l2) (Eq. (original))."""
+    X, _ = _tiny(N, n, seed=N)
+    rng = np.random.default_rng(1)
+    y, xi = rng.standard_normal(N), rng.standard_normal((N, n))
+    z = ref.dense_A1(N) @ y + ref.dense_A2(X) @ xi.reshape(-1)
+    for i in range(N):
+        for j in range(N):
+            if i != j:
+                want = y[j] - y[i] + xi[i] @ (X[i] - X[j])
+                assert abs(z[ref.pair_index(i, j, N)] - want) < 1e-12
+
+
+@pytest.mark.parametrize("N,n,seed", [(4, 1, 0), (6, 2, 1), (8, 3, 2)])
+def test_oracle_eta_equals_dense_stationary_point(N, n, seed):
+    """Step 1 closed form in the C oracle == dense G^{-1} C^T theta + (ybar, 0)."""
+    X, ybar = _tiny(N, n, seed)
+    T = crdata.random_theta(N, seed=seed + 10)
+    gamma = 0.05
+    y, xi = oracle.eta(X, ybar, gamma, T)
+    yd, xid = ref.eta_dense(ref.theta_vec(T), X, ybar, gamma)
+    np.testing.assert_allclose(y, yd, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(xi, xid, rtol=0, atol=1e-11)
+    # and it really is the minimizer: gradient of the Lagrangian vanishes
+    th = ref.theta_vec(T)
+    base = ref.lagrangian_dense(y, xi, th, X, ybar, gamma)
+    rng = np.random.default_rng(seed)
+    for _ in range(5):
+        dy, dxi = rng.standard_normal(N) * 1e-3, rng.standard_normal((N, n)) * 1e-3
+        assert ref.lagrangian_dense(y + dy, xi + dxi, th, X, ybar, gamma) >= base - 1e-14
+
+
+@pytest.mark.parametrize("N,n,seed", [(4, 1, 3), (6, 2, 4), (8, 3, 5)])
+def test_oracle_step_equals_dense_fig2_step(N, n, seed):
+    """One Fig. 2 iteration from a random mid-run state vs dense Steps 1-4."""
+    X, ybar = _tiny(N, n, seed)
+    gamma, L = 0.02, 37.0
+    Tprev = crdata.random_theta(N, seed=seed, scale=0.1)
+    Tt = crdata.random_theta(N, seed=seed + 1, scale=0.1)
+    t = 2.7
+    out = oracle.papg(X, ybar, gamma, L, 1, Tprev=Tprev, Tt=Tt, t=t)
+    # dense reference
+    th_t = ref.theta_vec(Tt)
+    y, xi = ref.eta_dense(th_t, X, ybar, gamma)
+    Ceta = ref.dense_C(X) @ np.concatenate([y, xi.reshape(-1)])
+    th_k = np.maximum(0.0, th_t - Ceta / L)
+    tn = (1 + math.sqrt(1 + 4 * t * t)) / 2
+    th_next = th_k + (t - 1) / tn * (th_k - ref.theta_vec(Tprev))
+    np.testing.assert_allclose(ref.theta_vec(out["Tprev"]), th_k, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(ref.theta_vec(out["Tt"]), th_next, rtol=0, atol=1e-13)
+    assert np.all(np.diag(out["Tprev"]) == 0) and np.all(np.diag(out["Tt"]) == 0)
+    assert out["t"] == tn
+    np.testing.assert_allclose(out["y"], y, atol=1e-12)
+    np.testing.assert_allclose(out["xi"], xi, atol=1e-11)
+
+
+# ---------------------------------------------------------------- P1 step from zero
+def test_first_step_from_zero_closed_form():
+    """P1: theta^0 = 0 => eta(0) = (ybar, 0), R_ij = ybar_j - ybar_i, Theta^1_ij = (ybar_i - ybar_j)_+ / L."""
+    X, ybar = _tiny(9, 2, seed=7)
+    L = 123.0
+    out = oracle.papg(X, ybar, 1e-3, L, 1)
+    want = np.maximum(0.0, ybar[:, None] - ybar[None, :]) / L
+    np.fill_diagonal(want, 0.0)
+    np.testing.assert_allclose(out["Tprev"], want, rtol=1e-15, atol=0)
+    np.testing.assert_allclose(out["Tt"], want, rtol=1e-15, atol=0)  # beta_1 = (t_1-1)/t_2 = 0
+    np.testing.assert_array_equal(out["y"], ybar)
+    np.testing.assert_array_equal(out["xi"], 0.0)
+
+
+# ---------------------------------------------------------------- P11 constant ybar
+def test_constant_ybar_is_a_fixed_point():
+    """P11: ybar constant => C eta(0) = 0 => Theta stays 0, y = ybar, xi = 0 for every k."""
+    X, _ = _tiny(12, 3, seed=2)
+    ybar = np.full(12, 2.5)
+    out = oracle.papg(X, ybar, 1e-3, 50.0, 25)
+    assert np.all(out["Tprev"] == 0) and np.all(out["Tt"] == 0)
+    np.testing.assert_array_equal(out["y"], ybar)
+    np.testing.assert_array_equal(out["xi"], 0.0)
+
+
+# ---------------------------------------------------------------- P4 N=2 worked example
+@pytest.mark.parametrize("case", [0, 1])
+def test_n2_closed_form(case):
+    """P4: N=2 closed form (tests/golden/n2_closed_form.json) -- NNLS and the oracle APG both reach it."""
+    g = _gold("n2_closed_form.json")
+    c = g["cases"][case]
+    X, ybar, gamma = np.array(g["X"]), np.array(g["ybar"]), c["gamma"]
+    opt = ref.regularized_optimum(X, ybar, gamma)
+    np.testing.assert_allclose(opt["y"], c["y"], atol=1e-12)
+    np.testing.assert_allclose(opt["xi"][:, 0], c["xi"], atol=1e-12)
+    np.testing.assert_allclose(opt["theta"], [c["theta12"], c["theta21"]], atol=1e-12)
+    L = ref.lipschitz(X, gamma)
+    out = oracle.papg(X, ybar, gamma, L, 4000)
+    y, xi = oracle.eta(X, ybar, gamma, out["Tprev"])
+    np.testing.assert_allclose(y, c["y"], atol=1e-7)
+    np.testing.assert_allclose(out["Tprev"][0, 1], c["theta12"], rtol=1e-6)
+    assert out["Tprev"][1, 0] == 0.0
+
+
+# ---------------------------------------------------------------- P3 / P5 / P6 / P7 / P13
+@pytest.fixture(scope="module")
+def small_run():
+    N, n, gamma = 7, 2, 0.05
+    X, ybar = _tiny(N, n, seed=11)
+    L = ref.lipschitz(X, gamma)
+    opt = ref.regularized_optimum(X, ybar, gamma)
+    return dict(N=N, n=n, gamma=gamma, X=X, ybar=ybar, L=L, opt=opt)
+
+
+def test_apg_reaches_nnls_optimum(small_run):
+    """P3: oracle APG -> exact regularized optimum (Lawson-Hanson NNLS of the dual)."""
+    s = small_run
+    out = oracle.papg(s["X"], s["ybar"], s["gamma"], s["L"], 20000)
+    y, xi = oracle.eta(s["X"], s["ybar"], s["gamma"], out["Tprev"])
+    np.testing.assert_allclose(y, s["opt"]["y"], atol=1e-9)
+    np.testing.assert_allclose(xi, s["opt"]["xi"], atol=1e-8)
+    st = oracle.stats(s["X"], s["ybar"], s["gamma"], out["Tprev"], y, xi)
+    # P7 KKT: primal objective equals p*, complementarity gap -> 0, violation -> 0
+    assert abs(st["r_gamma"] - s["opt"]["p"]) <= 1e-10 * s["opt"]["p"]
+    assert abs(st["gap"]) < 1e-9
+    assert st["max_violation"] < 1e-8
+
+
+def test_theorem1_envelope_and_apg_rate(small_run):
+    """P5 Theorem 1 and P6 APG rate at every iterate; P13 invariants."""
+    s = small_run
+    X, ybar, gamma, L = s["X"], s["ybar"], s["gamma"], s["L"]
+    p, ys, xis = s["opt"]["p"], s["opt"]["y"], s["opt"]["xi"]
+    th_star = s["opt"]["theta"]
+    R0 = float(th_star @ th_star)                      # ||theta^0 - theta*||^2 with theta^0 = 0
+    N = s["N"]
+    Tprev, Tt, t = np.zeros((N, N)), np.zeros((N, N)), 1.0
+    for k in range(1, 301):
+        out = oracle.papg(X, ybar, gamma, L, 1, Tprev=Tprev, Tt=Tt, t=t)
+        Tprev, Tt, t_next = out["Tprev"], out["Tt"], out["t"]
+        assert np.all(Tprev >= 0) and np.all(np.diag(Tprev) == 0)          # P13
+        assert t_next >= (k + 2) / 2 - 1e-12                                 # t_{k+1} >= (k+2)/2
+        g = ref.dual_value_dense(ref.theta_vec(Tprev), X, ybar, gamma)
+        y, xi = oracle.eta(X, ybar, gamma, Tprev)
+        lhs = np.sum((y - ys) ** 2) + gamma * np.sum((xi - xis) ** 2)
+        assert lhs <= 2 * (p - g) + 1e-10                                   # Theorem 1
+        assert p - g <= 2 * L * R0 / (k + 1) ** 2 + 1e-10                   # APG rate
+        st = oracle.stats(X, ybar, gamma, Tprev, y, xi)
+        assert abs(st["g"] - g) < 1e-10 * max(1.0, abs(g))                  # g = L(eta(theta), theta)
+        t = t_next
+
+
+def test_stats_against_dense(small_run):
+    """oracle_stats vs dense C eta for a random (theta, eta)."""
+    s = small_run
+    X, ybar, gamma, N = s["X"], s["ybar"], s["gamma"], s["N"]
+    rng = np.random.default_rng(5)
+    T = crdata.random_theta(N, seed=3)
+    y, xi = rng.standard_normal(N), rng.standard_normal((N, s["n"]))
+    st = oracle.stats(X, ybar, gamma, T, y, xi)
+    z = ref.dense_C(X) @ np.concatenate([y, xi.reshape(-1)])
+    neg = np.minimum(z, 0)
+    assert abs(st["gap"] - ref.theta_vec(T) @ z) < 1e-12
+    assert abs(st["max_violation"] - max(0.0, -z.min())) < 1e-13
+    assert abs(st["infeas_norm"] - np.linalg.norm(neg) / math.sqrt(N * N - N)) < 1e-13
+    rg = 0.5 * np.sum((y - ybar) ** 2) + 0.5 * gamma * np.sum(xi ** 2)
+    assert abs(st["r_gamma"] - rg) < 1e-12
+
+
+# ---------------------------------------------------------------- P12 gradient
+def test_gradient_is_minus_C_eta_finite_differences():
+    """P12: grad g = -C eta(theta) (Eq. (dual gradient) P:370) vs central differences of g."""
+    N, n, gamma = 5, 2, 0.1
+    X, ybar = _tiny(N, n, seed=21)
+    th = ref.theta_vec(crdata.random_theta(N, seed=22, density=1.0))
+    grad = ref.dual_grad_dense(th, X, ybar, gamma)
+    h = 1e-6
+    for r in range(0, len(th), 3):
+        e = np.zeros_like(th)
+        e[r] = h
+        fd = (ref.dual_value_dense(th + e, X, ybar, gamma) - ref.dual_value_dense(th - e, X, ybar, gamma)) / (2 * h)
+        assert abs(fd - grad[r]) <= 1e-5 * max(1.0, abs(grad[r]))
+    # the oracle's pair residual is the same C eta
+    T = ref.theta_mat(th, N)
+    y, xi = oracle.eta(X, ybar, gamma, T)
+    st = oracle.stats(X, ybar, gamma, T, y, xi)
+    assert abs(st["gap"] - th @ (-grad)) < 1e-10
+
+
+# ---------------------------------------------------------------- P9 uniqueness of y*
+def test_uniqueness_of_y_from_two_starts():
+    """P9: N >= n+1 -- APG from theta^0 = 0 and from a random theta^0 >= 0 reach the same y."""
+    N, n, gamma = 8, 2, 0.05
+    X, ybar = _tiny(N, n, seed=31)
+    L = ref.lipschitz(X, gamma)
+    a = oracle.papg(X, ybar, gamma, L, 20000)
+    T0 = crdata.random_theta(N, seed=32, scale=0.5)
+    b = oracle.papg(X, ybar, gamma, L, 20000, Tprev=T0, Tt=T0)
+    ya, _ = oracle.eta(X, ybar, gamma, a["Tprev"])
+    yb, _ = oracle.eta(X, ybar, gamma, b["Tprev"])
+    opt = ref.regularized_optimum(X, ybar, gamma)
+    np.testing.assert_allclose(ya, yb, atol=1e-8)
+    np.testing.assert_allclose(ya, opt["y"], atol=1e-8)
+
+
+# ---------------------------------------------------------------- P8 univariate / Lemma 1
+@pytest.mark.parametrize("gamma", [1e-2, 1e-4])
+def test_univariate_lemma1_against_sorted_slope_fit(gamma):
+    """P8: n=1, ||y*_gamma - y*|| <= ||xi*|| sqrt(gamma) (Lemma 1) with y* the 1-D convex LS fit.
+
+    xi* (least-norm, Eq. (tikhonov)) is the projection of 0 onto each point's
+    subdifferential interval [left slope, right slope] of the fitted interpolant.
+    """
+    N = 25
+    rng = np.random.default_rng(41)
+    x = np.sort(rng.uniform(-1, 1, N))
+    ybar = x ** 2 + 0.1 * rng.standard_normal(N)
+    ystar = ref.convex_fit_1d(x, ybar)
+    slopes = np.diff(ystar) / np.diff(x)
+    lo = np.concatenate([[-np.inf], slopes])
+    hi = np.concatenate([slopes, [np.inf]])
+    assert np.all(lo <= hi + 1e-9)                       # convex fit
+    xi_star = np.clip(0.0, lo, hi)
+    opt = ref.regularized_optimum(x[:, None], ybar, gamma)
+    dist = np.linalg.norm(opt["y"] - ystar)
+    assert dist <= np.linalg.norm(xi_star) * math.sqrt(gamma) * (1 + 1e-6) + 1e-9
+    # the oracle APG approaches the same regularized optimum
+    L = ref.lipschitz(x[:, None], gamma)
+    out = oracle.papg(x[:, None], ybar, gamma, L, 3000 if gamma > 1e-3 else 8000)
+    y, _ = oracle.eta(x[:, None], ybar, gamma, out["Tprev"])
+    p = opt["p"]
+    g = ref.dual_value_dense(ref.theta_vec(out["Tprev"]), x[:, None], ybar, gamma)
+    assert np.sum((y - opt["y"]) ** 2) <= 2 * (p - g) + 1e-10   # Theorem 1 along the way
+
+
+# ---------------------------------------------------------------- P10 L
+@pytest.mark.parametrize("N", [3, 6, 20])
+def test_lemma4_sigma_A1(N):
+    """P10: sigma_max(A1)^2 = 2N (Lemma 4): with X = 0, C^T C = diag(A1^T A1, 0)."""
+    X = np.zeros((N, 2))
+    for form in ("definition", "structured"):
+        assert abs(ref.sigma_max_sq(X, form) - 2 * N) < 1e-9 * N
+
+
+@pytest.mark.parametrize("N,n,seed", [(4, 1, 0), (6, 2, 1), (8, 3, 2)])
+def test_sigma_max_vs_dense_svd_and_bound(N, n, seed):
+    """P10: Lanczos sigma_max(C) == dense SVD (N <= 8) and <= sqrt(2N) + B_x N (Lemma 4)."""
+    X, _ = _tiny(N, n, seed)
+    s_dense = np.linalg.svd(ref.dense_C(X), compute_uv=False)[0]
+    for form in ("definition", "structured"):
+        assert abs(math.sqrt(ref.sigma_max_sq(X, form)) - s_dense) < 1e-10 * s_dense
+    Bx = np.linalg.norm(X, axis=1).max()
+    assert s_dense <= math.sqrt(2 * N) + Bx * N
+
+
+@pytest.mark.parametrize("N,n", [(9, 2), (40, 5), (130, 7)])
+def test_structured_CtC_equals_definition(N, n):
+    """The O(N n^2) C^T C product (derived) equals the pair-by-pair definition on random vectors."""
+    X, _ = _tiny(N, n, seed=N)
+    rng = np.random.default_rng(N)
+    for _ in range(3):
+        v = rng.standard_normal(N * (n + 1))
+        a, b = ref.CtC_definition(X, v, chunk=17), ref.CtC_structured(X, v)
+        np.testing.assert_allclose(b, a, rtol=0, atol=1e-10 * np.abs(a).max())
+    if N <= 9:
+        M = ref.dense_C(X)
+        v = rng.standard_normal(N * (n + 1))
+        np.testing.assert_allclose(ref.CtC_definition(X, v), M.T @ (M @ v), atol=1e-10)
+
+
+def test_lipschitz_bounds_gradient_variation():
+    """L_gamma (Eq. (lischitz), gamma <= 1) bounds ||grad g(a) - grad g(b)|| / ||a - b||."""
+    N, n, gamma = 6, 2, 0.2
+    X, ybar = _tiny(N, n, seed=51)
+    L = ref.lipschitz(X, gamma)
+    rng = np.random.default_rng(52)
+    for _ in range(10):
+        a, b = rng.exponential(size=N * (N - 1)), rng.exponential(size=N * (N - 1))
+        ga, gb = ref.dual_grad_dense(a, X, ybar, gamma), ref.dual_grad_dense(b, X, ybar, gamma)
+        assert np.linalg.norm(ga - gb) <= L * np.linalg.norm(a - b) * (1 + 1e-12)
+
+
+# ---------------------------------------------------------------- determinism / threads
+def test_oracle_independent_of_thread_count():
+    X, ybar = _tiny(300, 3, seed=61)
+    a = oracle.papg(X, ybar, 1e-3, 500.0, 3, nthreads=1)
+    b = oracle.papg(X, ybar, 1e-3, 500.0, 3, nthreads=4)
+    np.testing.assert_array_equal(a["Tt"], b["Tt"])
+    np.testing.assert_array_equal(a["xi"], b["xi"])
+
+
+def test_project_rows_matches_full_step():
+    """oracle_project_rows (sampled Step 2) == rows of a full oracle step."""
+    X, ybar = _tiny(50, 3, seed=71)
+    T = crdata.random_theta(50, seed=72, scale=1e-3)
+    out = oracle.papg(X, ybar, 1e-3, 900.0, 1, Tprev=T, Tt=T)
+    rows = np.array([0, 7, 49])
+    got = oracle.project_rows(X, out["y"], out["xi"], 900.0, rows, T[rows])
+    np.testing.assert_array_equal(got, out["Tprev"][rows])
+
+
+def test_config_generators_are_seeded_and_fp32_rounded():
+    X1, y1 = crdata.make_problem("C2", N=200)
+    X2, y2 = crdata.make_problem("C2", N=200)
+    np.testing.assert_array_equal(X1, X2)
+    assert np.all(X1.astype(np.float32).astype(np.float64) == X1)
+    Xc, yc = crdata.make_problem("C1")
+    assert Xc.shape == (50, 2) and np.abs(Xc).max() <= 1
