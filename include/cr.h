@@ -1,0 +1,199 @@
+/*
+ * cr.h -- C ABI of libcr: the B200 (sm_100a) hot path of Aybat & Wang,
+ * "A Parallelizable Dual Smoothing Method for Large Scale Convex Regression
+ * Problems" (arXiv 1608.02227).  Citations "P:n" are lines of PAPER.md.
+ *
+ * Problem (Eq. (regularize)): given observations {(x_l, ybar_l)}
+ * (Eq. (data)) and gamma > 0,
+ *     min 1/2 ||y - ybar||^2 + gamma/2 ||xi||^2
+ *     s.t. y_j - y_i + xi_i^T (x_i - x_j) >= 0   for all i != j   (Eq. (original)).
+ * Every pair constraint is dualized (the paper's partition with K = N
+ * singleton blocks, Assumption 1 P:138-143 relaxed as in DESIGN.md), so the
+ * dual variable theta (Eq. (dual-problem)) is a dense nonnegative
+ * N x N matrix Theta, Theta[i][j] <-> pair (l1, l2) = (i, j) in the
+ * lexicographic row order of P:101-102 (packed index i(N-1) + j - [j > i]),
+ * Theta[i][i] == 0.
+ *
+ * One call of cr_dual_step() is one iteration of the constant-step P-APG
+ * method, Fig. 2:
+ *   Step 1 eta^k = argmin L(eta, theta~^k): at K = N in closed form,
+ *          y = ybar + c - r,  xi_i = (r_i x_i - (Theta X)_i) / gamma,
+ *          r/c the row/column sums of theta~^k (Def. A1A2);
+ *   Step 2 Theta^k = (theta~^k - (1/L) C eta^k)_+ ,
+ *          (C eta)_ij = y_j - y_i + xi_i^T (x_i - x_j);
+ *   Steps 3-4 t_{k+1} = (1 + sqrt(1 + 4 t_k^2))/2,
+ *          theta~^{k+1} = Theta^k + (t_k - 1)/t_{k+1} (Theta^k - Theta^{k-1}).
+ * theta~ is never stored: the fused pass reads Theta^{k-1} and Theta^{k-2}
+ * and writes Theta^k over Theta^{k-2} (12 B per pair in fp32).
+ *
+ * Conventions
+ *   - Host arrays are row-major double unless stated; they are copied, never
+ *     retained.  Device workspace is owned by the caller (e.g. a torch tensor)
+ *     and must outlive the context; it must be 256-byte aligned.
+ *   - Every call enqueues on cfg.stream; calls that return host data
+ *     synchronize that stream.
+ *   - Every call returns cr_status; nothing is thrown across the ABI.
+ *     CR_ERR_INVALID_ARG / CR_ERR_STATE leave the context usable;
+ *     CR_ERR_CUDA / CR_ERR_NCCL / CR_ERR_OOM poison it (only cr_destroy,
+ *     cr_last_error are then allowed).  cr_last_error() holds the message.
+ *   - Multi-GPU: one process per GPU; rank p owns the contiguous row block
+ *     [p*S, min(N,(p+1)*S)), S = ceil(N/world), of both Theta buffers.
+ *     Per iteration ranks exchange an all-gather of y and a reduce-scatter of
+ *     the column sums (NCCL); X and ybar are replicated.
+ *   - Not thread-safe per context.
+ */
+#ifndef CR_H_
+#define CR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CR_ABI_VERSION 1
+
+typedef enum {
+    CR_OK = 0,
+    CR_ERR_INVALID_ARG = 1,  /* bad argument; context (if any) unchanged and usable       */
+    CR_ERR_CUDA = 2,         /* CUDA runtime/launch error; context poisoned                */
+    CR_ERR_NCCL = 3,         /* NCCL error; context poisoned                               */
+    CR_ERR_OOM = 4,          /* workspace too small / host allocation failed               */
+    CR_ERR_STATE = 5,        /* call not allowed in the current state (e.g. poisoned ctx)  */
+    CR_ERR_UNSUPPORTED = 6   /* configuration not built into this library (e.g. n too big) */
+} cr_status;
+
+typedef enum {
+    CR_FP32 = 0,   /* Theta, X, eta copies stored and combined in fp32; sums combined in fp64 */
+    CR_FP64 = 1    /* everything fp64 (BASELINE config C1)                                     */
+} cr_precision;
+
+typedef enum {
+    CR_KERNEL_AUTO = 0,  /* library picks (tensor-core pass when built and n large enough) */
+    CR_KERNEL_SIMT = 1,  /* CUDA-core fused pass                                           */
+    CR_KERNEL_TC = 2     /* tcgen05 (3xTF32) fused pass, fp32 only                         */
+} cr_kernel;
+
+typedef struct cr_ctx cr_ctx;
+
+typedef struct {
+    int64_t N;                  /* observations, N >= 2                                       */
+    int32_t n;                  /* dimension, 1 <= n <= cr_max_dim()                          */
+    const double *X;            /* HOST, N x n row-major (rows xbar_l); copied          */
+    const double *ybar;         /* HOST, N; copied                                      */
+    double gamma;               /* Tikhonov weight gamma > 0 (Eq. (regularize))          */
+    double L;                   /* > 0: step constant used as given; 0: L = sigma_max(C)^2/gamma
+                                   by Lanczos (Eq. (lischitz); requires gamma <= 1)      */
+    cr_precision prec;
+    cr_kernel kernel;
+    int32_t rank, world;        /* world >= 1, 0 <= rank < world                               */
+    const void *nccl_unique_id; /* world > 1: 128-byte ncclUniqueId, identical on all ranks    */
+    int32_t device;             /* CUDA device ordinal                                        */
+    void *stream;               /* cudaStream_t to enqueue on (NULL = legacy default stream)   */
+    void *workspace;            /* DEVICE memory, >= cr_workspace_size(...) bytes, caller-owned */
+    size_t workspace_bytes;
+} cr_config;
+
+/* Diagnostics of eta(Theta^k) (Theorem 1 semantics) reported per P:951 / P:1106. */
+typedef struct {
+    int64_t k;             /* iterations completed                                            */
+    double t_k;            /* momentum scalar t_{k+1} that the next iteration will use          */
+    double g;              /* dual value g_gamma(Theta^k) (Eq. (g_gamma))                 */
+    double r_gamma;        /* primal objective of eta(Theta^k) (Eq. (regularize))         */
+    double gap;            /* <Theta^k, C eta(Theta^k)>  ("duality gap")                 */
+    double max_violation;  /* max_{i != j} (-(C eta)_ij)_+                                      */
+    double infeas_norm;    /* ||(A1 y + A2 xi)_-||_2 / sqrt(N^2 - N)                 */
+    int32_t nonfinite;     /* 1 if a NaN/Inf was seen in the reported quantities               */
+} cr_step_stats;
+
+typedef struct {
+    int32_t report_every;  /* evaluate the test every m iterations (m >= 1)                    */
+    double infeas_tol;     /* stop when infeas_norm <= infeas_tol (paper: 1e-1) ...    */
+    double gap_tol;        /* ... and |gap| / (N^2 - N) <= gap_tol (paper: 5e-7)       */
+} cr_stop;
+
+typedef struct {
+    int64_t iters;         /* iterations run by this call                                     */
+    int32_t converged;     /* 1 if the stop test fired                                         */
+    cr_step_stats last;    /* stats at exit (only when stop != NULL)                           */
+} cr_report;
+
+/* Bytes of device workspace cr_init needs for this shape / rank (0 if unsupported). */
+size_t cr_workspace_size(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel,
+                         int32_t rank, int32_t world);
+
+/* Largest n this library was built for. */
+int32_t cr_max_dim(void);
+
+/* world > 1 bootstrap: write a fresh 128-byte ncclUniqueId into out (host memory).  Rank 0
+ * calls this and broadcasts the bytes to the other ranks (e.g. over torch.distributed). */
+cr_status cr_nccl_get_unique_id(void *out);
+
+/* Validate cfg, copy X/ybar to the device, compute L if cfg->L == 0 (Lanczos, host fp64),
+ * initialise the NCCL communicator (world > 1), set Theta^0 = 0, t_1 = 1.
+ * On success *out owns the context; on failure *out = NULL. */
+cr_status cr_init(const cr_config *cfg, cr_ctx **out);
+
+/* Load a full APG state: Theta^{k-1} and Theta^{k-2} (HOST, this rank's rows x N, zero
+ * diagonal; NULL means all-zero) and the scalars t_{k-1}, t_k, so that the next
+ * cr_dual_step forms theta~^k = Theta^{k-1} + (t_{k-1}-1)/t_k (Theta^{k-1} - Theta^{k-2}).
+ * The paper's start is (Theta^0, Theta^0, 1, 1).  Values are rounded to the
+ * storage precision.  Negative or non-finite entries: CR_ERR_INVALID_ARG. */
+cr_status cr_set_theta(cr_ctx *ctx, const double *theta_km1, const double *theta_km2,
+                       double t_km1, double t_k);
+
+/* Read back the state: Theta^k, Theta^{k-1} (HOST, rows x N each, either may be NULL)
+ * and t_k, t_{k+1} -- exactly the arguments cr_set_theta takes to continue. */
+cr_status cr_get_theta(cr_ctx *ctx, double *theta_k, double *theta_km1, double *t_k,
+                       double *t_kp1);
+
+/* Read rows [row0, row0 + nrows) (local to this rank) of Theta^k (which = 0) or
+ * Theta^{k-1} (which = 1) into HOST out (nrows x N). */
+cr_status cr_get_theta_rows(cr_ctx *ctx, int32_t which, int64_t row0, int64_t nrows,
+                            double *out);
+
+/* One P-APG iteration (Fig. 2).  If out != NULL, also evaluates eta(Theta^k) and the
+ * diagnostics (one extra read-only pass over Theta^k) and synchronizes. */
+cr_status cr_dual_step(cr_ctx *ctx, cr_step_stats *out);
+
+/* Run up to max_iters iterations (CUDA-graph replay).  stop == NULL: exactly max_iters,
+ * no synchronisation.  Otherwise evaluates the paper's stopping pair every
+ * stop->report_every iterations and returns early when both hold. */
+cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_report *out);
+
+/* Final estimator eta(Theta^k) (Theorem 1): y (HOST, all N) and xi (HOST, this
+ * rank's rows x n), either may be NULL; optional diagnostics.  Synchronizes. */
+cr_status cr_primal(cr_ctx *ctx, double *y, double *xi, cr_step_stats *out);
+
+/* eta^k = Step-1 minimizer of the most recent iteration (eta(theta~^k)), or of the most
+ * recent cr_primal: y (HOST, all N), xi (HOST, this rank's rows x n). */
+cr_status cr_get_eta(cr_ctx *ctx, double *y, double *xi);
+
+/* Step constant in use. */
+double cr_lipschitz(const cr_ctx *ctx);
+
+/* Host-only: L = sigma_max(C)^2 / gamma by fp64 Lanczos on the structured C^T C
+ * (Eq. (lischitz); Lemma 4 P:476 bounds it).  No device needed. */
+cr_status cr_lipschitz_host(int64_t N, int32_t n, const double *X, double gamma, double *L_out);
+
+/* Kernel-level accounting: number of kernels this context launched (all calls). */
+int64_t cr_launch_count(const cr_ctx *ctx);
+
+/* Per-launch timing of the fused pair pass: when on, CUDA events bracket every pass
+ * launch on the context stream.  cr_pass_timing synchronizes and returns the summed
+ * pass time (ms) and number of timed launches since the last reset. */
+cr_status cr_set_pass_timing(cr_ctx *ctx, int32_t on);
+cr_status cr_pass_timing(cr_ctx *ctx, double *total_ms, int64_t *launches);
+
+/* Which fused-pass kernel the context uses (CR_KERNEL_SIMT or CR_KERNEL_TC). */
+cr_kernel cr_active_kernel(const cr_ctx *ctx);
+
+const char *cr_last_error(const cr_ctx *ctx);
+const char *cr_status_string(cr_status s);
+void cr_destroy(cr_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CR_H_ */

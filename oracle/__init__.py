@@ -22,5 +22,5 @@ Parity status per function:
     definition form and Lemma 4 closed forms.
 """
 from .core import (  # noqa: F401
-    build_oracle, lib, papg, eta, stats, project_rows, momentum_next, max_threads,
+    build_oracle, lib, papg, eta, stats, project_rows, momentum_next, max_threads, extrapolate, state_after,
 )

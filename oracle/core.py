@@ -112,3 +112,17 @@ def project_rows(X, y, xi, L, rows, Tt_rows, nthreads=0):
     lib().oracle_project_rows(N, n, X, _c64(y), _c64(xi).reshape(N, n), float(L), rows, len(rows),
                               _c64(Tt_rows).reshape(len(rows), N), out, int(nthreads))
     return out
+
+
+def extrapolate(Tk, Tkm1, t_k, t_kp1):
+    """Step 4 of Fig. 2: theta~^{k+1} = theta^k + ((t_k - 1)/t_{k+1}) (theta^k - theta^{k-1})."""
+    Tk = _c64(Tk)
+    return Tk + ((t_k - 1.0) / t_kp1) * (Tk - _c64(Tkm1))
+
+
+def state_after(X, ybar, gamma, L, K, nthreads=0):
+    """Oracle run of K >= 1 iterations from theta^0 = 0 returning the GPU-style state
+    (Theta^K, Theta^{K-1}, t_K, t_{K+1}) plus eta^K (Step 1 of iteration K)."""
+    a = papg(X, ybar, gamma, L, K - 1, nthreads=nthreads)          # Tprev = theta^{K-1}, t = t_K
+    b = papg(X, ybar, gamma, L, 1, Tprev=a["Tprev"], Tt=a["Tt"], t=a["t"], nthreads=nthreads)
+    return dict(Tk=b["Tprev"], Tkm1=a["Tprev"], t_k=a["t"], t_kp1=b["t"], y=b["y"], xi=b["xi"])

@@ -1,0 +1,275 @@
+"""Thin ctypes binding of libcr (include/cr.h).  Argument marshalling only.
+
+Every step of the hot path runs in libcr's CUDA kernels; PyTorch supplies device memory
+(the workspace tensor), the stream, and the process group that broadcasts the NCCL id.
+There is no CPU fallback: if libcr.so is missing or no CUDA device is present, the
+constructor raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcr.so")
+
+CR_OK, CR_ERR_INVALID_ARG, CR_ERR_CUDA, CR_ERR_NCCL, CR_ERR_OOM, CR_ERR_STATE, CR_ERR_UNSUPPORTED = range(7)
+PREC = {"fp32": 0, "fp64": 1}
+KERNEL = {"auto": 0, "simt": 1, "tc": 2}
+KERNEL_NAME = {v: k for k, v in KERNEL.items()}
+
+# Symbols include/cr.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "cr_workspace_size", "cr_max_dim", "cr_nccl_get_unique_id", "cr_init", "cr_set_theta", "cr_get_theta",
+    "cr_get_theta_rows", "cr_dual_step", "cr_solve", "cr_primal", "cr_get_eta", "cr_lipschitz",
+    "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
+    "cr_last_error", "cr_status_string", "cr_destroy",
+)
+
+
+class CrConfig(C.Structure):
+    _fields_ = [("N", C.c_int64), ("n", C.c_int32), ("X", C.c_void_p), ("ybar", C.c_void_p),
+                ("gamma", C.c_double), ("L", C.c_double), ("prec", C.c_int), ("kernel", C.c_int),
+                ("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("device", C.c_int32), ("stream", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t)]
+
+
+class CrStepStats(C.Structure):
+    _fields_ = [("k", C.c_int64), ("t_k", C.c_double), ("g", C.c_double), ("r_gamma", C.c_double),
+                ("gap", C.c_double), ("max_violation", C.c_double), ("infeas_norm", C.c_double),
+                ("nonfinite", C.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class CrStop(C.Structure):
+    _fields_ = [("report_every", C.c_int32), ("infeas_tol", C.c_double), ("gap_tol", C.c_double)]
+
+
+class CrReport(C.Structure):
+    _fields_ = [("iters", C.c_int64), ("converged", C.c_int32), ("last", CrStepStats)]
+
+
+class CrError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libcr.so (built by ``python -m paper_1608_02227_b200.build``); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise CrError(f"libcr.so not found at {path}; build it with `python -m paper_1608_02227_b200.build` "
+                      "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    vp, i64, i32, d = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    sig = {
+        "cr_workspace_size": (C.c_size_t, [i64, i32, C.c_int, C.c_int, i32, i32]),
+        "cr_max_dim": (i32, []),
+        "cr_nccl_get_unique_id": (C.c_int, [vp]),
+        "cr_init": (C.c_int, [C.POINTER(CrConfig), C.POINTER(vp)]),
+        "cr_set_theta": (C.c_int, [vp, vp, vp, d, d]),
+        "cr_get_theta": (C.c_int, [vp, vp, vp, C.POINTER(d), C.POINTER(d)]),
+        "cr_get_theta_rows": (C.c_int, [vp, i32, i64, i64, vp]),
+        "cr_dual_step": (C.c_int, [vp, C.POINTER(CrStepStats)]),
+        "cr_solve": (C.c_int, [vp, i64, C.POINTER(CrStop), C.POINTER(CrReport)]),
+        "cr_primal": (C.c_int, [vp, vp, vp, C.POINTER(CrStepStats)]),
+        "cr_get_eta": (C.c_int, [vp, vp, vp]),
+        "cr_lipschitz": (d, [vp]),
+        "cr_lipschitz_host": (C.c_int, [i64, i32, vp, d, C.POINTER(d)]),
+        "cr_launch_count": (i64, [vp]),
+        "cr_set_pass_timing": (C.c_int, [vp, i32]),
+        "cr_pass_timing": (C.c_int, [vp, C.POINTER(d), C.POINTER(i64)]),
+        "cr_active_kernel": (C.c_int, [vp]),
+        "cr_last_error": (C.c_char_p, [vp]),
+        "cr_status_string": (C.c_char_p, [C.c_int]),
+        "cr_destroy": (None, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None and a.shape != shape:
+        raise ValueError(f"expected shape {shape}, got {a.shape}")
+    return a
+
+
+def workspace_size(N, n, prec="fp32", kernel="auto", rank=0, world=1) -> int:
+    return int(load().cr_workspace_size(int(N), int(n), PREC[prec], KERNEL[kernel], int(rank), int(world)))
+
+
+def lipschitz_host(X, gamma) -> float:
+    """L = sigma_max(C)^2 / gamma by libcr's host Lanczos (Eq. (lischitz))."""
+    X = _f64(X)
+    out = C.c_double()
+    st = load().cr_lipschitz_host(X.shape[0], X.shape[1], X.ctypes.data, float(gamma), C.byref(out))
+    if st != CR_OK:
+        raise CrError(f"cr_lipschitz_host: status {st}")
+    return out.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    st = load().cr_nccl_get_unique_id(buf)
+    if st != CR_OK:
+        raise CrError(f"cr_nccl_get_unique_id: status {st}")
+    return bytes(buf)
+
+
+class Solver:
+    """One rank's share of the smoothed-dual P-APG solve (Fig. 2).
+
+    X [N, n], ybar [N] are host arrays (copied).  With ``group`` (a torch.distributed
+    process group of world > 1) rank r owns rows [r*S, min(N, (r+1)*S)), S = ceil(N/world),
+    and NCCL is bootstrapped by broadcasting the unique id over ``group``.
+    """
+
+    def __init__(self, X, ybar, gamma, L=0.0, prec="fp32", kernel="auto", device=None, stream=None,
+                 group=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise CrError("libcr needs a CUDA device (no CPU fallback)")
+        self.lib = load()
+        self.X = _f64(X)
+        self.N, self.n = self.X.shape
+        self.ybar = _f64(ybar, (self.N,))
+        self.gamma = float(gamma)
+        self.prec = prec
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.device = dev
+        self.rank, self.world = 0, 1
+        uid = None
+        if group is not None:
+            import torch.distributed as dist
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+            if self.world > 1:
+                raw = nccl_unique_id() if self.rank == 0 else bytes(128)
+                bdev = dev if dist.get_backend(group) == "nccl" else torch.device("cpu")
+                t = torch.tensor(list(raw), dtype=torch.uint8, device=bdev)
+                dist.broadcast(t, src=dist.get_global_rank(group, 0), group=group)
+                uid = (C.c_char * 128).from_buffer_copy(bytes(t.cpu().tolist()))
+        self._uid = uid
+        S = -(-self.N // self.world)
+        self.row0 = min(self.N, self.rank * S)
+        self.rows = min(self.N, self.row0 + S) - self.row0
+        nbytes = workspace_size(self.N, self.n, prec, kernel, self.rank, self.world)
+        if nbytes == 0:
+            raise CrError(f"unsupported shape/precision: N={self.N} n={self.n} prec={prec} kernel={kernel}")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.stream = torch.cuda.current_stream(dev) if stream is None else stream
+        cfg = CrConfig(N=self.N, n=self.n, X=self.X.ctypes.data, ybar=self.ybar.ctypes.data, gamma=self.gamma,
+                       L=float(L), prec=PREC[prec], kernel=KERNEL[kernel], rank=self.rank, world=self.world,
+                       nccl_unique_id=C.cast(uid, C.c_void_p) if uid is not None else None,
+                       device=dev.index, stream=self.stream.cuda_stream,
+                       workspace=self.workspace.data_ptr(), workspace_bytes=nbytes)
+        h = C.c_void_p()
+        st = self.lib.cr_init(C.byref(cfg), C.byref(h))
+        if st != CR_OK:
+            raise CrError(f"cr_init failed: {self.lib.cr_status_string(st).decode()}")
+        self.h = h
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st, what):
+        if st != CR_OK:
+            msg = self.lib.cr_last_error(self.h).decode() if self.h else ""
+            raise CrError(f"{what}: {self.lib.cr_status_string(st).decode()} {msg}")
+
+    @property
+    def L(self) -> float:
+        return float(self.lib.cr_lipschitz(self.h))
+
+    @property
+    def kernel(self) -> str:
+        return KERNEL_NAME[int(self.lib.cr_active_kernel(self.h))]
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.cr_launch_count(self.h))
+
+    # ------------------------------------------------------------------ API
+    def step(self, stats: bool = False):
+        s = CrStepStats()
+        self._check(self.lib.cr_dual_step(self.h, C.byref(s) if stats else None), "cr_dual_step")
+        return s.as_dict() if stats else None
+
+    def solve(self, iters: int, report_every: int = 0, infeas_tol: float = 1e-1, gap_tol: float = 5e-7):
+        rep = CrReport()
+        stop = CrStop(report_every, infeas_tol, gap_tol) if report_every > 0 else None
+        self._check(self.lib.cr_solve(self.h, int(iters), C.byref(stop) if stop else None, C.byref(rep)),
+                    "cr_solve")
+        return dict(iters=rep.iters, converged=bool(rep.converged), last=rep.last.as_dict() if stop else None)
+
+    def primal(self):
+        y = np.empty(self.N)
+        xi = np.empty((self.rows, self.n))
+        s = CrStepStats()
+        self._check(self.lib.cr_primal(self.h, y.ctypes.data, xi.ctypes.data, C.byref(s)), "cr_primal")
+        return y, xi, s.as_dict()
+
+    def get_eta(self):
+        y = np.empty(self.N)
+        xi = np.empty((self.rows, self.n))
+        self._check(self.lib.cr_get_eta(self.h, y.ctypes.data, xi.ctypes.data), "cr_get_eta")
+        return y, xi
+
+    def set_theta(self, theta_km1=None, theta_km2=None, t_km1=1.0, t_k=1.0):
+        shp = (self.rows, self.N)
+        a = None if theta_km1 is None else _f64(theta_km1, shp)
+        b = None if theta_km2 is None else _f64(theta_km2, shp)
+        self._check(self.lib.cr_set_theta(self.h, None if a is None else a.ctypes.data,
+                                          None if b is None else b.ctypes.data, float(t_km1), float(t_k)),
+                    "cr_set_theta")
+
+    def get_theta(self):
+        a = np.empty((self.rows, self.N))
+        b = np.empty((self.rows, self.N))
+        tk, tk1 = C.c_double(), C.c_double()
+        self._check(self.lib.cr_get_theta(self.h, a.ctypes.data, b.ctypes.data, C.byref(tk), C.byref(tk1)),
+                    "cr_get_theta")
+        return a, b, tk.value, tk1.value
+
+    def get_theta_rows(self, which: int, row0: int, nrows: int):
+        out = np.empty((nrows, self.N))
+        self._check(self.lib.cr_get_theta_rows(self.h, int(which), int(row0), int(nrows), out.ctypes.data),
+                    "cr_get_theta_rows")
+        return out
+
+    def set_pass_timing(self, on: bool):
+        self._check(self.lib.cr_set_pass_timing(self.h, 1 if on else 0), "cr_set_pass_timing")
+
+    def pass_timing(self):
+        ms, n = C.c_double(), C.c_int64()
+        self._check(self.lib.cr_pass_timing(self.h, C.byref(ms), C.byref(n)), "cr_pass_timing")
+        return ms.value, n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

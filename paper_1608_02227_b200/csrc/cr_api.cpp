@@ -1,0 +1,740 @@
+// libcr: C ABI (include/cr.h) and host orchestration of the P-APG hot path.
+//
+// Per iteration (Fig. 2) the host enqueues on the context stream:
+//   prologue  (Step 1 closed form from the sums of Theta^{k-1}, Theta^{k-2})
+//   [world > 1: ncclAllGather of y']
+//   fused pass (Steps 2 + 4 for every owned pair, sums of Theta^k)
+//   reduce    (fixed-order fp64 sums -> S^k; Step 3 momentum update on device)
+//   [world > 1: ncclReduceScatter of the column sums]
+// cr_solve replays the iteration as a CUDA graph (two graphs: buffer parities 0/1).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/cr.h"
+#include "cr_internal.h"
+
+namespace cr {
+double sigma_max_sq_lanczos(int64_t N, int n, const double *X, double tol, int max_iter);
+}
+
+using namespace cr;
+
+namespace {
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+    int64_t N = 0, S = 0, Ns = 0, row0 = 0, Rp = 0, ldT = 0;
+    int n = 0, NB = 0, NBP = 0, nRB = 0, world = 1, fp64 = 0;
+    size_t es = 4;
+    // byte offsets
+    size_t th[2], XT, Xh, X64, ybar, r[2], c[2], P[2], y64, yv, bv, XiT, Xi64, a64, colpart, rowpart,
+        slot0, rb_ptr, rb_slots, cfull, ts, statpro, statres, total;
+};
+
+bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank, int world, Layout *L) {
+    if (N < 2 || n < 1 || world < 1 || rank < 0 || rank >= world) return false;
+    if (kernel == CR_KERNEL_TC) return false;  // tensor-core pass not built in this library version
+    L->N = N;
+    L->n = n;
+    L->world = world;
+    L->fp64 = prec == CR_FP64;
+    L->es = L->fp64 ? 8 : 4;
+    L->NB = simt_bucket(n);
+    if (L->NB == 0 || (L->fp64 && L->NB > 24)) return false;
+    L->NBP = L->NB + 4;
+    L->S = (N + world - 1) / world;
+    L->row0 = std::min<int64_t>(N, (int64_t)rank * L->S);
+    L->Ns = std::min<int64_t>(N, L->row0 + L->S) - L->row0;
+    L->Rp = (int64_t)align_up((size_t)std::max<int64_t>(L->S, 1), kRowAlign);
+    L->ldT = (int64_t)align_up((size_t)N, kColAlign);
+    L->nRB = (int)(L->Rp / kBM);
+    const size_t es = L->es, A = 256;
+    const int64_t WS = (int64_t)world * L->S;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + std::max<size_t>(bytes, 1), A); return r; };
+    for (int b = 0; b < 2; ++b) L->th[b] = take((size_t)L->Rp * L->ldT * es);
+    L->XT = take((size_t)L->NB * L->ldT * es);
+    L->Xh = take((size_t)L->ldT * L->NBP * es);
+    L->X64 = take((size_t)N * n * 8);
+    L->ybar = take((size_t)N * 8);
+    for (int s = 0; s < 2; ++s) {
+        L->r[s] = take((size_t)L->Rp * 8);
+        L->c[s] = take((size_t)L->Rp * 8);
+        L->P[s] = take((size_t)L->Rp * n * 8);
+    }
+    L->y64 = take((size_t)std::max(WS, N) * 8);
+    L->yv = take((size_t)std::max(WS, L->ldT) * es);
+    L->bv = take((size_t)L->Rp * es);
+    L->XiT = take((size_t)L->NB * L->Rp * es);
+    L->Xi64 = take((size_t)L->Rp * n * 8);
+    L->a64 = take((size_t)L->Rp * 8);
+    L->colpart = take((size_t)L->nRB * L->ldT * es);
+    L->rowpart = take((size_t)(L->nRB + kGMax) * kBM * L->NBP * 8);
+    L->slot0 = take((size_t)kGMax * 4);
+    L->rb_ptr = take((size_t)(L->nRB + 1) * 4);
+    L->rb_slots = take((size_t)(L->nRB + kGMax) * 4);
+    L->cfull = take((size_t)WS * 8);
+    L->ts = take(sizeof(DevScalars));
+    L->statpro = take((size_t)(L->Rp / 256 + 2) * 8 * 8);
+    L->statres = take((size_t)kStatBlocks * 8 * 8);
+    L->total = o;
+    return true;
+}
+
+}  // namespace
+
+struct cr_ctx {
+    Layout lay;
+    cr_precision prec = CR_FP32;
+    cr_kernel kernel = CR_KERNEL_SIMT;
+    double gamma = 0, L = 0;
+    int rank = 0, world = 1, device = 0;
+    cudaStream_t stream = nullptr;
+    char *ws = nullptr;
+    // device views
+    void *th[2];
+    double *r[2], *c[2], *P[2];
+    int b1 = 0;          // buffer holding Theta^{k-1} at the start of the next iteration
+    int s1 = 0;          // sums slot of Theta^{k-1}
+    int64_t k = 0;
+    int G = 0, nCB = 0;
+    int64_t T = 0;
+    int64_t launches = 0;
+    bool poisoned = false;
+    std::string err;
+    // pass timing
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;
+    size_t ev_used = 0;
+    // graphs per parity
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    ncclComm_t comm = nullptr;
+
+    template <typename P> P *at(size_t off) { return reinterpret_cast<P *>(ws + off); }
+};
+
+namespace {
+
+cr_status fail(cr_ctx *c, cr_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) {
+        c->err = buf;
+        if (s == CR_ERR_CUDA || s == CR_ERR_NCCL || s == CR_ERR_OOM) c->poisoned = true;
+    }
+    return s;
+}
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            return fail(ctx, CR_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,           \
+                        cudaGetErrorString(e_));                                               \
+    } while (0)
+#define NK(call)                                                                               \
+    do {                                                                                       \
+        ncclResult_t r_ = (call);                                                              \
+        if (r_ != ncclSuccess)                                                                 \
+            return fail(ctx, CR_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,           \
+                        ncclGetErrorString(r_));                                               \
+    } while (0)
+
+ncclDataType_t nccl_t(const cr_ctx *ctx) { return ctx->lay.fp64 ? ncclFloat64 : ncclFloat32; }
+
+PassParams pass_params(cr_ctx *ctx, int b_read, int b_write) {
+    const Layout &Ly = ctx->lay;
+    PassParams p{};
+    p.B1 = ctx->th[b_read];
+    p.B2 = ctx->th[b_write];
+    p.ldT = Ly.ldT;
+    p.N = Ly.N;
+    p.Ns = Ly.Ns;
+    p.row0 = Ly.row0;
+    p.nRB = Ly.nRB;
+    p.nCB = ctx->nCB;
+    p.T = ctx->T;
+    p.G = ctx->G;
+    p.XT = ctx->ws + Ly.XT;
+    p.Xh = ctx->ws + Ly.Xh;
+    p.XiT = ctx->ws + Ly.XiT;
+    p.bv = ctx->ws + Ly.bv;
+    p.yv = ctx->ws + Ly.yv;
+    p.Rp = Ly.Rp;
+    p.colpart = ctx->ws + Ly.colpart;
+    p.rowpart = ctx->at<double>(Ly.rowpart);
+    p.cta_slot0 = ctx->at<int>(Ly.slot0);
+    p.ts = ctx->at<double>(Ly.ts);
+    return p;
+}
+
+ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance) {
+    const Layout &Ly = ctx->lay;
+    ReduceParams q{};
+    q.N = Ly.N;
+    q.Ns = Ly.Ns;
+    q.Rp = Ly.Rp;
+    q.ldT = Ly.ldT;
+    q.n = Ly.n;
+    q.NBP = Ly.NBP;
+    q.nRB = Ly.nRB;
+    q.colpart = ctx->ws + Ly.colpart;
+    q.rowpart = ctx->at<double>(Ly.rowpart);
+    q.rb_ptr = ctx->at<int>(Ly.rb_ptr);
+    q.rb_slots = ctx->at<int>(Ly.rb_slots);
+    q.r = ctx->r[slot];
+    q.P = ctx->P[slot];
+    q.c_out = ctx->world > 1 ? ctx->at<double>(Ly.cfull) : ctx->c[slot];
+    q.ts = ctx->at<DevScalars>(Ly.ts);
+    q.advance_t = advance;
+    return q;
+}
+
+SmallParams small_params(cr_ctx *ctx, int sa, int sb, int use_beta, double scale, bool stats) {
+    const Layout &Ly = ctx->lay;
+    SmallParams p{};
+    p.N = Ly.N;
+    p.Ns = Ly.Ns;
+    p.row0 = Ly.row0;
+    p.Rp = Ly.Rp;
+    p.ldT = Ly.ldT;
+    p.n = Ly.n;
+    p.NB = Ly.NB;
+    p.NBP = Ly.NBP;
+    p.gamma = ctx->gamma;
+    p.scale = scale;
+    p.X64 = ctx->at<double>(Ly.X64);
+    p.ybar = ctx->at<double>(Ly.ybar);
+    p.r1 = ctx->r[sa]; p.c1 = ctx->c[sa]; p.P1 = ctx->P[sa];
+    p.r2 = ctx->r[sb]; p.c2 = ctx->c[sb]; p.P2 = ctx->P[sb];
+    p.y64 = ctx->at<double>(Ly.y64);
+    p.Xi64 = ctx->at<double>(Ly.Xi64);
+    p.a64 = ctx->at<double>(Ly.a64);
+    p.yv = ctx->ws + Ly.yv;
+    p.bv = ctx->ws + Ly.bv;
+    p.XiT = ctx->ws + Ly.XiT;
+    p.statpart = stats ? ctx->at<double>(Ly.statpro) : nullptr;
+    p.ts = ctx->at<DevScalars>(Ly.ts);
+    p.use_beta = use_beta;
+    return p;
+}
+
+cudaEvent_t next_event(cr_ctx *ctx) {
+    if (ctx->ev_used == ctx->ev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        ctx->ev.push_back(e);
+    }
+    return ctx->ev[ctx->ev_used++];
+}
+
+// Sums (r, c, Theta X) of buffer b into slot s, read-only pass.
+cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
+    const Layout &Ly = ctx->lay;
+    PassParams p = pass_params(ctx, b, b);
+    CK(launch_pass_simt(p, Ly.fp64, Ly.NB, MODE_SUMS, ctx->stream));
+    ReduceParams q = reduce_params(ctx, s, 0);
+    CK(launch_reduce(q, Ly.fp64, ctx->stream));
+    ctx->launches += 2;
+    if (ctx->world > 1)
+        NK(ncclReduceScatter(ctx->at<double>(Ly.cfull), ctx->c[s], (size_t)Ly.S, ncclFloat64, ncclSum,
+                             ctx->comm, ctx->stream));
+    return CR_OK;
+}
+
+// One P-APG iteration for the current parity (no host sync).
+cr_status enqueue_step(cr_ctx *ctx, bool allow_timing) {
+    const Layout &Ly = ctx->lay;
+    const int b1 = ctx->b1, b2 = 1 - b1, s1 = ctx->s1, s2 = 1 - s1;
+    SmallParams sp = small_params(ctx, s1, s2, 1, 1.0 / ctx->L, false);
+    CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
+    if (ctx->world > 1) {
+        char *yv = ctx->ws + Ly.yv;
+        NK(ncclAllGather(yv + (size_t)ctx->rank * Ly.S * Ly.es, yv, (size_t)Ly.S, nccl_t(ctx), ctx->comm,
+                         ctx->stream));
+    }
+    PassParams p = pass_params(ctx, b1, b2);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (allow_timing && ctx->timing) {
+        e0 = next_event(ctx);
+        e1 = next_event(ctx);
+        if (!e0 || !e1) return fail(ctx, CR_ERR_CUDA, "cudaEventCreate failed");
+        CK(cudaEventRecord(e0, ctx->stream));
+    }
+    CK(launch_pass_simt(p, Ly.fp64, Ly.NB, MODE_STEP, ctx->stream));
+    if (e1) CK(cudaEventRecord(e1, ctx->stream));
+    ReduceParams q = reduce_params(ctx, s2, 1);
+    CK(launch_reduce(q, Ly.fp64, ctx->stream));
+    if (ctx->world > 1)
+        NK(ncclReduceScatter(ctx->at<double>(Ly.cfull), ctx->c[s2], (size_t)Ly.S, ncclFloat64, ncclSum,
+                             ctx->comm, ctx->stream));
+    ctx->launches += 3;
+    return CR_OK;
+}
+
+void advance_host(cr_ctx *ctx) {
+    ctx->b1 = 1 - ctx->b1;
+    ctx->s1 = 1 - ctx->s1;
+    ctx->k += 1;
+}
+
+// eta(Theta^k) and diagnostics (Theorem 1 semantics); synchronizes.
+cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
+    const Layout &Ly = ctx->lay;
+    const int s = ctx->s1, b = ctx->b1;
+    int nb_pro = 0, nb_res = 0;
+    SmallParams sp = small_params(ctx, s, s, 0, 1.0, true);
+    CK(launch_prologue(sp, Ly.fp64, ctx->stream, &nb_pro));
+    double *y64 = ctx->at<double>(Ly.y64);
+    if (ctx->world > 1)
+        NK(ncclAllGather(y64 + (size_t)ctx->rank * Ly.S, y64, (size_t)Ly.S, ncclFloat64, ctx->comm,
+                         ctx->stream));
+    ResidualParams rp{};
+    rp.Theta = ctx->th[b];
+    rp.ldT = Ly.ldT;
+    rp.N = Ly.N;
+    rp.Ns = Ly.Ns;
+    rp.row0 = Ly.row0;
+    rp.Rp = Ly.Rp;
+    rp.n = Ly.n;
+    rp.X64 = ctx->at<double>(Ly.X64);
+    rp.y64 = y64;
+    rp.Xi64 = ctx->at<double>(Ly.Xi64);
+    rp.a64 = ctx->at<double>(Ly.a64);
+    rp.statpart = ctx->at<double>(Ly.statres);
+    CK(launch_residual(rp, Ly.fp64, ctx->stream, &nb_res));
+    DevScalars *ts = ctx->at<DevScalars>(Ly.ts);
+    CK(launch_stats_finalize(ctx->at<double>(Ly.statpro), nb_pro, ctx->at<double>(Ly.statres), nb_res, ts,
+                             ctx->stream));
+    ctx->launches += 3;
+    if (ctx->world > 1) {
+        // stats[0..5] and [7] are sums; [6] is a max
+        NK(ncclGroupStart());
+        NK(ncclAllReduce(ts->stats, ts->stats, 6, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+        NK(ncclAllReduce(ts->stats + 6, ts->stats + 6, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream));
+        NK(ncclAllReduce(ts->stats + 7, ts->stats + 7, 1, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+        NK(ncclGroupEnd());
+    }
+    DevScalars h{};
+    CK(cudaMemcpyAsync(&h, ts, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (out) {
+        const double u2 = h.stats[0], uy = h.stats[1], xi2 = h.stats[2];
+        const double Nd = (double)Ly.N;
+        out->k = ctx->k;
+        out->t_k = h.t_cur;
+        out->r_gamma = 0.5 * u2 + 0.5 * ctx->gamma * xi2;                 // Eq. (regularize)
+        out->g = -0.5 * u2 - 0.5 * ctx->gamma * xi2 - uy;                 // g at eta(theta)
+        out->gap = h.stats[4];                                            // <theta, C eta>
+        out->max_violation = h.stats[6];
+        out->infeas_norm = std::sqrt(h.stats[5]) / std::sqrt(Nd * Nd - Nd);
+        out->nonfinite = (h.stats[3] + h.stats[7]) > 0 ||
+                         !std::isfinite(out->g) || !std::isfinite(out->gap);
+    }
+    return CR_OK;
+}
+
+cr_status check_ctx(cr_ctx *ctx) {
+    if (!ctx) return CR_ERR_INVALID_ARG;
+    if (ctx->poisoned) return CR_ERR_STATE;
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    return CR_OK;
+}
+
+void drop_graphs(cr_ctx *ctx) {
+    for (auto &g : ctx->graph)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
+cr_status build_graph(cr_ctx *ctx, int parity) {
+    // parity = ctx->b1 at capture time; capture one iteration, then restore host state
+    cudaGraph_t g = nullptr;
+    const int b1 = ctx->b1, s1 = ctx->s1;
+    const int64_t k = ctx->k, launches = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    cr_status st = enqueue_step(ctx, false);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    ctx->b1 = b1; ctx->s1 = s1; ctx->k = k; ctx->launches = launches;
+    if (st != CR_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&ctx->graph[parity], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    return CR_OK;
+}
+
+}  // namespace
+
+// =============================================================================== ABI
+extern "C" {
+
+const char *cr_status_string(cr_status s) {
+    switch (s) {
+        case CR_OK: return "CR_OK";
+        case CR_ERR_INVALID_ARG: return "CR_ERR_INVALID_ARG";
+        case CR_ERR_CUDA: return "CR_ERR_CUDA";
+        case CR_ERR_NCCL: return "CR_ERR_NCCL";
+        case CR_ERR_OOM: return "CR_ERR_OOM";
+        case CR_ERR_STATE: return "CR_ERR_STATE";
+        case CR_ERR_UNSUPPORTED: return "CR_ERR_UNSUPPORTED";
+    }
+    return "CR_ERR_UNKNOWN";
+}
+
+const char *cr_last_error(const cr_ctx *ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int32_t cr_max_dim(void) { return 80; }
+
+cr_status cr_nccl_get_unique_id(void *out) {
+    if (!out) return CR_ERR_INVALID_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return CR_ERR_NCCL;
+    std::memcpy(out, &id, sizeof id);
+    return CR_OK;
+}
+
+size_t cr_workspace_size(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel, int32_t rank,
+                         int32_t world) {
+    Layout L;
+    if (!make_layout(N, n, prec, kernel, rank, world, &L)) return 0;
+    return L.total;
+}
+
+cr_status cr_lipschitz_host(int64_t N, int32_t n, const double *X, double gamma, double *L_out) {
+    if (N < 2 || n < 1 || !X || !L_out || !(gamma > 0.0) || !std::isfinite(gamma)) return CR_ERR_INVALID_ARG;
+    const double s2 = sigma_max_sq_lanczos(N, n, X, 1e-13, 2000);
+    if (!(s2 > 0.0) || !std::isfinite(s2)) return CR_ERR_INVALID_ARG;
+    *L_out = s2 / gamma;
+    return CR_OK;
+}
+
+cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
+    if (!out) return CR_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (!cfg || !cfg->X || !cfg->ybar || cfg->N < 2 || cfg->n < 1) return CR_ERR_INVALID_ARG;
+    if (!(cfg->gamma > 0.0) || !std::isfinite(cfg->gamma) || !(cfg->L >= 0.0) || !std::isfinite(cfg->L))
+        return CR_ERR_INVALID_ARG;
+    if (cfg->L == 0.0 && cfg->gamma > 1.0) return CR_ERR_INVALID_ARG;  // sigma^2/gamma bounds only for gamma<=1
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return CR_ERR_INVALID_ARG;
+    if (cfg->world > 1 && !cfg->nccl_unique_id) return CR_ERR_INVALID_ARG;
+    if (cfg->prec != CR_FP32 && cfg->prec != CR_FP64) return CR_ERR_INVALID_ARG;
+    if (cfg->prec == CR_FP64 && cfg->kernel == CR_KERNEL_TC) return CR_ERR_UNSUPPORTED;
+    if (cfg->n > cr_max_dim()) return CR_ERR_UNSUPPORTED;
+    if (cfg->kernel == CR_KERNEL_TC) return CR_ERR_UNSUPPORTED;
+    const int64_t N = cfg->N;
+    const int n = cfg->n;
+    for (int64_t i = 0; i < N * n; ++i)
+        if (!std::isfinite(cfg->X[i])) return CR_ERR_INVALID_ARG;
+    for (int64_t i = 0; i < N; ++i)
+        if (!std::isfinite(cfg->ybar[i])) return CR_ERR_INVALID_ARG;
+
+    cr_ctx *ctx = new (std::nothrow) cr_ctx();
+    if (!ctx) return CR_ERR_OOM;
+    ctx->prec = cfg->prec;
+    ctx->kernel = CR_KERNEL_SIMT;
+    ctx->gamma = cfg->gamma;
+    ctx->rank = cfg->rank;
+    ctx->world = cfg->world;
+    ctx->device = cfg->device;
+    ctx->stream = static_cast<cudaStream_t>(cfg->stream);
+    if (!make_layout(N, n, cfg->prec, ctx->kernel, cfg->rank, cfg->world, &ctx->lay)) {
+        delete ctx;
+        return CR_ERR_UNSUPPORTED;
+    }
+    const Layout &Ly = ctx->lay;
+    auto bail = [&](cr_status s) { cr_destroy(ctx); return s; };
+    if (!cfg->workspace || cfg->workspace_bytes < Ly.total || (reinterpret_cast<uintptr_t>(cfg->workspace) & 255))
+        return bail(CR_ERR_INVALID_ARG);
+    ctx->ws = static_cast<char *>(cfg->workspace);
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return bail(CR_ERR_CUDA);
+
+    // step constant (Eq. (lischitz))
+    if (cfg->L > 0.0) {
+        ctx->L = cfg->L;
+    } else {
+        double L = 0.0;
+        cr_status s = cr_lipschitz_host(N, n, cfg->X, cfg->gamma, &L);
+        if (s != CR_OK) return bail(s);
+        ctx->L = L;
+    }
+
+    for (int b = 0; b < 2; ++b) ctx->th[b] = ctx->ws + Ly.th[b];
+    for (int s = 0; s < 2; ++s) {
+        ctx->r[s] = ctx->at<double>(Ly.r[s]);
+        ctx->c[s] = ctx->at<double>(Ly.c[s]);
+        ctx->P[s] = ctx->at<double>(Ly.P[s]);
+    }
+    cudaError_t e;
+#define IK(call)                                                                                   \
+    do {                                                                                           \
+        e = (call);                                                                                \
+        if (e != cudaSuccess) {                                                                    \
+            fail(ctx, CR_ERR_CUDA, "cr_init %s: %s", #call, cudaGetErrorString(e));              \
+            std::fprintf(stderr, "libcr: %s\n", ctx->err.c_str());                                 \
+            return bail(CR_ERR_CUDA);                                                              \
+        }                                                                                          \
+    } while (0)
+    IK(cudaMemsetAsync(ctx->ws, 0, Ly.total, ctx->stream));
+    IK(cudaMemcpyAsync(ctx->ws + Ly.X64, cfg->X, (size_t)N * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    IK(cudaMemcpyAsync(ctx->ws + Ly.ybar, cfg->ybar, (size_t)N * 8, cudaMemcpyHostToDevice, ctx->stream));
+    IK(launch_fill_inputs(ctx->at<double>(Ly.X64), N, n, Ly.NB, Ly.NBP, Ly.ldT, Ly.fp64, ctx->ws + Ly.XT,
+                          ctx->ws + Ly.Xh, ctx->stream));
+    ctx->launches += 1;
+    DevScalars h{};
+    h.t_prev = 1.0;   // beta_0 = 0: theta~^1 = theta^0
+    h.t_cur = 1.0;    // t_1 = 1
+    IK(cudaMemcpyAsync(ctx->ws + Ly.ts, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+
+    // fused-pass grid: one full wave of resident CTAs, contiguous tile ranges
+    int smem = 0, bps = 0, nsm = 0;
+    IK(pass_simt_config(Ly.fp64, Ly.NB, &smem, &bps));
+    IK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+    ctx->nCB = (int)((N + kBN - 1) / kBN);
+    ctx->T = (int64_t)Ly.nRB * ctx->nCB;
+    ctx->G = (int)std::min<int64_t>({ctx->T, (int64_t)std::max(bps, 1) * nsm, (int64_t)kGMax});
+    {
+        std::vector<int> slot0(ctx->G), rb_ptr(Ly.nRB + 1, 0);
+        std::vector<std::vector<int>> per(Ly.nRB);
+        int cur = 0;
+        for (int g = 0; g < ctx->G; ++g) {
+            const int64_t t0 = (int64_t)g * ctx->T / ctx->G, t1 = (int64_t)(g + 1) * ctx->T / ctx->G;
+            slot0[g] = cur;
+            if (t0 >= t1) continue;
+            for (int64_t rb = t0 / ctx->nCB; rb <= (t1 - 1) / ctx->nCB; ++rb) per[rb].push_back(cur++);
+        }
+        std::vector<int> slots;
+        for (int rb = 0; rb < Ly.nRB; ++rb) {
+            rb_ptr[rb] = (int)slots.size();
+            slots.insert(slots.end(), per[rb].begin(), per[rb].end());
+        }
+        rb_ptr[Ly.nRB] = (int)slots.size();
+        IK(cudaMemcpyAsync(ctx->ws + Ly.slot0, slot0.data(), slot0.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        IK(cudaMemcpyAsync(ctx->ws + Ly.rb_ptr, rb_ptr.data(), rb_ptr.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        IK(cudaMemcpyAsync(ctx->ws + Ly.rb_slots, slots.data(), std::max<size_t>(slots.size(), 1) * 4,
+                           cudaMemcpyHostToDevice, ctx->stream));
+        IK(cudaStreamSynchronize(ctx->stream));   // host vectors go out of scope
+    }
+#undef IK
+    if (ctx->world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+        if (r != ncclSuccess) {
+            fail(ctx, CR_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+            return bail(CR_ERR_NCCL);
+        }
+    }
+    *out = ctx;
+    return CR_OK;
+}
+
+cr_status cr_set_theta(cr_ctx *ctx, const double *tk1, const double *tk2, double t_km1, double t_k) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    const Layout &Ly = ctx->lay;
+    if (!(t_km1 >= 1.0) || !(t_k >= 1.0) || !std::isfinite(t_km1) || !std::isfinite(t_k))
+        return fail(ctx, CR_ERR_INVALID_ARG, "t_{k-1}, t_k must be finite and >= 1");
+    const double *src[2] = {tk1, tk2};
+    for (int b = 0; b < 2; ++b) {
+        if (!src[b]) continue;
+        for (int64_t i = 0; i < Ly.Ns; ++i)
+            for (int64_t j = 0; j < Ly.N; ++j) {
+                const double v = src[b][i * Ly.N + j];
+                if (!(v >= 0.0) || !std::isfinite(v))
+                    return fail(ctx, CR_ERR_INVALID_ARG, "Theta entries must be finite and >= 0");
+                if (Ly.row0 + i == j && v != 0.0)
+                    return fail(ctx, CR_ERR_INVALID_ARG, "Theta diagonal must be 0");
+            }
+    }
+    drop_graphs(ctx);
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMemsetAsync(ctx->th[b], 0, (size_t)Ly.Rp * Ly.ldT * Ly.es, ctx->stream));
+        if (src[b] && Ly.Ns > 0) {
+            if (Ly.fp64) {
+                CK(cudaMemcpy2DAsync(ctx->th[b], Ly.ldT * 8, src[b], Ly.N * 8, Ly.N * 8, Ly.Ns,
+                                     cudaMemcpyHostToDevice, ctx->stream));
+            } else {
+                std::vector<float> tmp((size_t)Ly.Ns * Ly.N);
+                for (size_t e = 0; e < tmp.size(); ++e) tmp[e] = (float)src[b][e];
+                CK(cudaMemcpy2DAsync(ctx->th[b], Ly.ldT * 4, tmp.data(), Ly.N * 4, Ly.N * 4, Ly.Ns,
+                                     cudaMemcpyHostToDevice, ctx->stream));
+                CK(cudaStreamSynchronize(ctx->stream));
+            }
+        }
+    }
+    ctx->b1 = 0;
+    ctx->s1 = 0;
+    st = enqueue_sums(ctx, 0, 0);
+    if (st != CR_OK) return st;
+    st = enqueue_sums(ctx, 1, 1);
+    if (st != CR_OK) return st;
+    DevScalars h{};
+    h.t_prev = t_km1;
+    h.t_cur = t_k;
+    CK(cudaMemcpyAsync(ctx->ws + Ly.ts, &h, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CR_OK;
+}
+
+static cr_status read_buffer(cr_ctx *ctx, int b, int64_t row0, int64_t nrows, double *out) {
+    const Layout &Ly = ctx->lay;
+    if (nrows <= 0) return CR_OK;
+    const char *src = static_cast<const char *>(ctx->th[b]) + (size_t)row0 * Ly.ldT * Ly.es;
+    if (Ly.fp64) {
+        CK(cudaMemcpy2DAsync(out, Ly.N * 8, src, Ly.ldT * 8, Ly.N * 8, nrows, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    } else {
+        std::vector<float> tmp((size_t)nrows * Ly.N);
+        CK(cudaMemcpy2DAsync(tmp.data(), Ly.N * 4, src, Ly.ldT * 4, Ly.N * 4, nrows, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (size_t e = 0; e < tmp.size(); ++e) out[e] = tmp[e];
+    }
+    return CR_OK;
+}
+
+cr_status cr_get_theta(cr_ctx *ctx, double *theta_k, double *theta_km1, double *t_k, double *t_kp1) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    const Layout &Ly = ctx->lay;
+    if (theta_k && (st = read_buffer(ctx, ctx->b1, 0, Ly.Ns, theta_k)) != CR_OK) return st;
+    if (theta_km1 && (st = read_buffer(ctx, 1 - ctx->b1, 0, Ly.Ns, theta_km1)) != CR_OK) return st;
+    double t[2];
+    CK(cudaMemcpyAsync(t, ctx->ws + Ly.ts, sizeof t, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (t_k) *t_k = t[0];
+    if (t_kp1) *t_kp1 = t[1];
+    return CR_OK;
+}
+
+cr_status cr_get_theta_rows(cr_ctx *ctx, int32_t which, int64_t row0, int64_t nrows, double *out) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    const Layout &Ly = ctx->lay;
+    if ((which != 0 && which != 1) || row0 < 0 || nrows < 0 || row0 + nrows > Ly.Ns || (!out && nrows))
+        return fail(ctx, CR_ERR_INVALID_ARG, "cr_get_theta_rows: bad range");
+    return read_buffer(ctx, which == 0 ? ctx->b1 : 1 - ctx->b1, row0, nrows, out);
+}
+
+cr_status cr_dual_step(cr_ctx *ctx, cr_step_stats *out) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    if ((st = enqueue_step(ctx, true)) != CR_OK) return st;
+    advance_host(ctx);
+    if (out) return eval_stats(ctx, out);
+    return CR_OK;
+}
+
+cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_report *out) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    if (max_iters < 0 || (stop && stop->report_every < 1))
+        return fail(ctx, CR_ERR_INVALID_ARG, "cr_solve: bad arguments");
+    if (out) std::memset(out, 0, sizeof *out);
+    const bool use_graph = !ctx->timing;
+    const double Nd = (double)ctx->lay.N;
+    int64_t it = 0;
+    while (it < max_iters) {
+        if (use_graph) {
+            const int par = ctx->b1;
+            if (!ctx->graph[par] && (st = build_graph(ctx, par)) != CR_OK) return st;
+            CK(cudaGraphLaunch(ctx->graph[par], ctx->stream));
+            ctx->launches += 3;
+        } else if ((st = enqueue_step(ctx, true)) != CR_OK) {
+            return st;
+        }
+        advance_host(ctx);
+        ++it;
+        if (stop && (it % stop->report_every == 0 || it == max_iters)) {
+            cr_step_stats s{};
+            if ((st = eval_stats(ctx, &s)) != CR_OK) return st;
+            if (out) out->last = s;
+            if (s.infeas_norm <= stop->infeas_tol && std::fabs(s.gap) / (Nd * Nd - Nd) <= stop->gap_tol) {
+                if (out) out->converged = 1;
+                break;
+            }
+        }
+    }
+    if (out) out->iters = it;
+    return CR_OK;
+}
+
+cr_status cr_primal(cr_ctx *ctx, double *y, double *xi, cr_step_stats *out) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    cr_step_stats s{};
+    if ((st = eval_stats(ctx, &s)) != CR_OK) return st;   // eta(Theta^k) into y64 / Xi64
+    if (out) *out = s;
+    return cr_get_eta(ctx, y, xi);
+}
+
+cr_status cr_get_eta(cr_ctx *ctx, double *y, double *xi) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    const Layout &Ly = ctx->lay;
+    double *y64 = ctx->at<double>(Ly.y64);
+    if (y && ctx->world > 1) {
+        // make sure all ranks' rows are present (eta of a plain step is only local until gathered)
+        NK(ncclAllGather(y64 + (size_t)ctx->rank * Ly.S, y64, (size_t)Ly.S, ncclFloat64, ctx->comm, ctx->stream));
+    }
+    if (y) CK(cudaMemcpyAsync(y, y64, (size_t)Ly.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (xi && Ly.Ns > 0)
+        CK(cudaMemcpyAsync(xi, ctx->ws + Ly.Xi64, (size_t)Ly.Ns * Ly.n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CR_OK;
+}
+
+double cr_lipschitz(const cr_ctx *ctx) { return ctx ? ctx->L : 0.0; }
+
+int64_t cr_launch_count(const cr_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+cr_kernel cr_active_kernel(const cr_ctx *ctx) { return ctx ? ctx->kernel : CR_KERNEL_AUTO; }
+
+cr_status cr_set_pass_timing(cr_ctx *ctx, int32_t on) {
+    if (!ctx) return CR_ERR_INVALID_ARG;
+    ctx->timing = on != 0;
+    ctx->ev_used = 0;
+    return CR_OK;
+}
+
+cr_status cr_pass_timing(cr_ctx *ctx, double *total_ms, int64_t *launches) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < ctx->ev_used; i += 2) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]));
+        tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = (int64_t)(ctx->ev_used / 2);
+    ctx->ev_used = 0;
+    return CR_OK;
+}
+
+void cr_destroy(cr_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    drop_graphs(ctx);
+    for (auto e : ctx->ev) cudaEventDestroy(e);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    delete ctx;
+}
+
+}  // extern "C"

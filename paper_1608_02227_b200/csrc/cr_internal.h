@@ -1,0 +1,112 @@
+// Internal declarations shared by the host orchestration (cr_api.cpp) and the
+// CUDA kernels.  Not part of the ABI (include/cr.h is).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cr {
+
+constexpr int kBM = 64;           // SIMT fused-pass tile rows
+constexpr int kBN = 64;           // SIMT fused-pass tile columns
+constexpr int kThreads = 256;     // SIMT fused-pass CTA size
+constexpr int kGMax = 4096;       // upper bound on fused-pass CTAs (slot table sizing)
+constexpr int kRowAlign = 128;    // Theta rows allocated per shard rounded to this
+constexpr int kColAlign = 256;    // Theta row pitch (elements) rounded to this
+constexpr int kStatBlocks = 1024; // max CTAs of the stats/residual kernels
+
+// n-buckets compiled for the SIMT pass (S-GEMM depth NB; P-GEMM width NBP = NB + 4).
+int simt_bucket(int n);           // smallest compiled NB >= n, or 0 if none
+
+// Device scalar block (fp64), lives in the workspace.
+struct DevScalars {
+    double t_prev;      // t_{k-1}
+    double t_cur;       // t_k
+    double stats[16];   // finalized diagnostics (see stats kernels)
+};
+
+struct PassParams {
+    const void *B1;        // Theta^{k-1} (read)
+    void *B2;              // Theta^{k-2} (read), overwritten with Theta^k (MODE_STEP)
+    int64_t ldT;           // row pitch of Theta, XT, colpart (elements)
+    int64_t N, Ns, row0;   // global size, shard rows, first global row of the shard
+    int nRB, nCB;          // tile grid (row blocks of kBM, column tiles of kBN)
+    int64_t T;             // nRB * nCB
+    int G;                 // CTAs
+    const void *XT;        // [NB][ldT]   x_j[k] (k-major), zero padded
+    const void *Xh;        // [ldT][NBP]  x_j[d], 1 at d = n, zero padded
+    const void *XiT;       // [NB][Rp]    xi_i[k] * scale (k-major)
+    const void *bv;        // [Rp]        (a_i - y_i) * scale
+    const void *yv;        // [>= ldT]    y_j * scale (all columns, gathered)
+    int64_t Rp;            // allocated rows
+    void *colpart;         // [nRB][ldT] column partial sums (acc type)
+    double *rowpart;       // [slots][kBM][NBP] row partials (r at d = n, Theta X at d < n)
+    const int *cta_slot0;  // [G] first row-partial slot of each CTA
+    const double *ts;      // DevScalars* (t_prev, t_cur) -> beta
+};
+
+enum PassMode { MODE_STEP = 0, MODE_SUMS = 1 };
+
+// SIMT fused pass (kernels/pass_simt.cu).
+cudaError_t launch_pass_simt(const PassParams &p, int prec_fp64, int NB, int mode, cudaStream_t s);
+cudaError_t pass_simt_config(int prec_fp64, int NB, int *smem_bytes, int *blocks_per_sm);
+
+struct SmallParams {
+    int64_t N, Ns, row0, Rp, ldT;
+    int n, NB, NBP;
+    double gamma, scale;
+    const double *X64;     // [N][n]
+    const double *ybar;    // [N]
+    // sums slots (r, c, P) for S^{k-1} (s1) and S^{k-2} (s2)
+    const double *r1, *c1, *P1, *r2, *c2, *P2;
+    double *y64;           // [>= N] y of eta (all rows after gather)
+    double *Xi64;          // [Rp][n]
+    double *a64;           // [Rp]
+    void *yv, *bv, *XiT;   // storage-precision copies for the pass
+    double *statpart;      // [kStatBlocks][8] per-CTA partials
+    DevScalars *ts;
+    int use_beta;          // 1: beta from ts (Step 1 at theta~^k); 0: beta = 0 (eta(Theta^k))
+};
+
+cudaError_t launch_prologue(const SmallParams &p, int prec_fp64, cudaStream_t s, int *nblocks_out);
+
+struct ReduceParams {
+    int64_t N, Ns, Rp, ldT;
+    int n, NBP, nRB;
+    const void *colpart;   // [nRB][ldT]
+    const double *rowpart; // [slots][kBM][NBP]
+    const int *rb_ptr;     // [nRB + 1]
+    const int *rb_slots;   // row-partial slot list per row block (CTA order)
+    double *r, *P;         // this shard's rows
+    double *c_out;         // column sums for all N columns (shard partial)
+    DevScalars *ts;
+    int advance_t;         // 1: t_prev <- t_cur, t_cur <- (1 + sqrt(1 + 4 t^2)) / 2
+};
+
+cudaError_t launch_reduce(const ReduceParams &p, int prec_fp64, cudaStream_t s);
+
+struct ResidualParams {
+    const void *Theta;     // [Rp][ldT] storage precision
+    int64_t ldT, N, Ns, row0, Rp;
+    int n;
+    const double *X64, *y64, *Xi64, *a64;
+    double *statpart;      // [kStatBlocks][8]
+};
+
+cudaError_t launch_residual(const ResidualParams &p, int prec_fp64, cudaStream_t s, int *nblocks_out);
+
+// Sum the per-CTA partials: prologue partials (nb_pro blocks: |u|^2, u.ybar, |xi|^2,
+// nonfinite) and residual partials (nb_res blocks: gap, sum R_-^2, max -R, nonfinite)
+// into ts->stats[0..7] (rank-local).
+cudaError_t launch_stats_finalize(const double *pro, int nb_pro, const double *res, int nb_res,
+                                  DevScalars *ts, cudaStream_t s);
+
+// Column-major helpers for initialisation.
+cudaError_t launch_fill_inputs(const double *X64, int64_t N, int n, int NB, int NBP, int64_t ldT,
+                               int prec_fp64, void *XT, void *Xh, cudaStream_t s);
+cudaError_t launch_convert_rows(const double *src, int64_t rows, int64_t N, int64_t ldT,
+                                int prec_fp64, void *dst, cudaStream_t s);   // double -> storage
+cudaError_t launch_unconvert_rows(const void *src, int64_t rows, int64_t N, int64_t ldT,
+                                  int prec_fp64, double *dst, cudaStream_t s); // storage -> double
+
+}  // namespace cr

@@ -1,0 +1,271 @@
+// O(N n) kernels around the fused pass, and the read-only residual pass.
+//
+//   prologue   : Step 1 of Fig. 2 in closed form at K = N, from the linear sums
+//                S = (r, c, Theta X) of Theta^{k-1} and Theta^{k-2}:
+//                  S~ = S^{k-1} + beta_{k-1} (S^{k-1} - S^{k-2})      (Step 4 is linear)
+//                  y_i  = ybar_i + c~_i - r~_i                          (A1^T theta, Def. A1A2)
+//                  xi_i = (r~_i x_i - (Theta~ X)_i) / gamma             (A2^T theta / gamma)
+//                  a_i  = xi_i . x_i
+//                all in fp64; writes the storage-precision operands of the pass
+//                (y' = y s, b' = (a - y) s, xi' = xi s with s = 1/L) and fp64 masters.
+//   reduce     : fixed-order fp64 sums of the pass's row / column partials -> S^k; t update.
+//   residual   : (C eta)_ij = y_j - y_i + a_i - xi_i . x_j in fp64 over Theta^k:
+//                sum Theta R (gap), sum (R_-)^2 and max (-R)_+ (P:1106).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "../cr_internal.h"
+
+namespace cr {
+namespace {
+
+template <typename T>
+__global__ void prologue_kernel(const SmallParams p) {
+    __shared__ double red[4][256];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double u2 = 0.0, uy = 0.0, xi2 = 0.0, bad = 0.0;
+    if (i < p.Ns) {
+        const double beta = p.use_beta ? (p.ts->t_prev - 1.0) / p.ts->t_cur : 0.0;
+        const double r1 = p.r1[i], r2 = p.r2[i], c1 = p.c1[i], c2 = p.c2[i];
+        const double rt = r1 + beta * (r1 - r2);
+        const double ct = c1 + beta * (c1 - c2);
+        const int64_t gi = p.row0 + i;
+        const double u = ct - rt;                       // (A1^T theta~)_i
+        const double y = p.ybar[gi] + u;
+        const double *x = p.X64 + gi * p.n;
+        double a = 0.0;
+        T *XiT = static_cast<T *>(p.XiT);
+        for (int d = 0; d < p.n; ++d) {
+            const double P1 = p.P1[i * p.n + d], P2 = p.P2[i * p.n + d];
+            const double Pt = P1 + beta * (P1 - P2);
+            const double xi = (rt * x[d] - Pt) / p.gamma;   // (A2^T theta~)_i / gamma
+            p.Xi64[i * p.n + d] = xi;
+            XiT[(int64_t)d * p.Rp + i] = T(xi * p.scale);
+            a += xi * x[d];
+            xi2 += xi * xi;
+        }
+        p.y64[gi] = y;
+        p.a64[i] = a;
+        static_cast<T *>(p.yv)[gi] = T(y * p.scale);
+        static_cast<T *>(p.bv)[i] = T((a - y) * p.scale);
+        u2 = u * u;
+        uy = u * p.ybar[gi];
+        bad = (isfinite(y) && isfinite(a)) ? 0.0 : 1.0;
+    }
+    red[0][threadIdx.x] = u2; red[1][threadIdx.x] = uy; red[2][threadIdx.x] = xi2; red[3][threadIdx.x] = bad;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s)
+            for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && p.statpart)
+        for (int q = 0; q < 4; ++q) p.statpart[blockIdx.x * 8 + q] = red[q][0];
+}
+
+template <typename Tc>
+__global__ void reduce_kernel(const ReduceParams p) {
+    const int64_t nrow = p.Ns * (p.n + 1);
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < nrow) {
+        const int64_t i = g / (p.n + 1);
+        const int d = (int)(g % (p.n + 1));
+        const int rb = (int)(i / kBM), ii = (int)(i % kBM);
+        double s = 0.0;
+        for (int e = p.rb_ptr[rb]; e < p.rb_ptr[rb + 1]; ++e)
+            s += p.rowpart[((int64_t)p.rb_slots[e] * kBM + ii) * p.NBP + d];
+        if (d < p.n) p.P[i * p.n + d] = s;
+        else p.r[i] = s;
+    } else if (g < nrow + p.N) {
+        const int64_t j = g - nrow;
+        const Tc *cp = static_cast<const Tc *>(p.colpart);
+        double s = 0.0;
+        for (int rb = 0; rb < p.nRB; ++rb) s += (double)cp[(int64_t)rb * p.ldT + j];
+        p.c_out[j] = s;
+    }
+    if (p.advance_t && g == 0) {
+        const double t = p.ts->t_cur;
+        p.ts->t_prev = t;
+        p.ts->t_cur = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;   // Step 3
+    }
+}
+
+// Residual pass: 128 columns x 32 rows per tile, thread = (column, 16-row half).
+template <typename T>
+__global__ void __launch_bounds__(256) residual_kernel(const ResidualParams p) {
+    constexpr int RBM = 32, RBN = 128;
+    extern __shared__ double rsm[];
+    double *xs = rsm;                        // [n][RBN]
+    double *xis = xs + p.n * RBN;            // [RBM][n]
+    double *ab = xis + RBM * p.n;            // [RBM] a_i - y_i
+    __shared__ double red[3][256];
+    const int nrb = (int)((p.Ns + RBM - 1) / RBM), ncb = (int)((p.N + RBN - 1) / RBN);
+    const int64_t ntiles = (int64_t)nrb * ncb;
+    const T *Th = static_cast<const T *>(p.Theta);
+    double gap = 0.0, v2 = 0.0, vmax = 0.0;
+    const int c = threadIdx.x % RBN, h = threadIdx.x / RBN;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t rb = t / ncb, cb = t % ncb;
+        __syncthreads();
+        for (int e = threadIdx.x; e < p.n * RBN; e += blockDim.x) {
+            const int d = e / RBN, cc = e % RBN;
+            const int64_t j = cb * RBN + cc;
+            xs[e] = j < p.N ? p.X64[j * p.n + d] : 0.0;
+        }
+        for (int e = threadIdx.x; e < RBM * p.n; e += blockDim.x) {
+            const int64_t i = rb * RBM + e / p.n;
+            xis[e] = i < p.Ns ? p.Xi64[i * p.n + e % p.n] : 0.0;
+        }
+        for (int e = threadIdx.x; e < RBM; e += blockDim.x) {
+            const int64_t i = rb * RBM + e;
+            ab[e] = i < p.Ns ? p.a64[i] - p.y64[p.row0 + i] : 0.0;
+        }
+        __syncthreads();
+        const int64_t j = cb * RBN + c;
+        if (j >= p.N) continue;
+        const double yj = p.y64[j];
+        for (int q = 0; q < RBM / 2; ++q) {
+            const int ii = h * (RBM / 2) + q;
+            const int64_t i = rb * RBM + ii;
+            if (i >= p.Ns || p.row0 + i == j) continue;
+            double s = 0.0;
+            for (int d = 0; d < p.n; ++d) s = fma(xis[ii * p.n + d], xs[d * RBN + c], s);
+            const double R = yj + ab[ii] - s;              // y_j - y_i + a_i - xi_i . x_j
+            gap += (double)Th[i * p.ldT + j] * R;
+            if (R < 0.0) { v2 += R * R; vmax = fmax(vmax, -R); }
+        }
+    }
+    red[0][threadIdx.x] = gap; red[1][threadIdx.x] = v2; red[2][threadIdx.x] = vmax;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + s];
+            red[1][threadIdx.x] += red[1][threadIdx.x + s];
+            red[2][threadIdx.x] = fmax(red[2][threadIdx.x], red[2][threadIdx.x + s]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        p.statpart[blockIdx.x * 8 + 4] = red[0][0];
+        p.statpart[blockIdx.x * 8 + 5] = red[1][0];
+        p.statpart[blockIdx.x * 8 + 6] = red[2][0];
+        p.statpart[blockIdx.x * 8 + 7] = (isfinite(red[0][0]) && isfinite(red[1][0])) ? 0.0 : 1.0;
+    }
+}
+
+__global__ void stats_finalize_kernel(const double *pro, int nb_pro, const double *res, int nb_res,
+                                      DevScalars *ts) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < nb_pro; ++b)
+        for (int q = 0; q < 4; ++q) s[q] += pro[b * 8 + q];
+    for (int b = 0; b < nb_res; ++b) {
+        s[4] += res[b * 8 + 4];
+        s[5] += res[b * 8 + 5];
+        s[6] = fmax(s[6], res[b * 8 + 6]);
+        s[7] += res[b * 8 + 7];
+    }
+    for (int q = 0; q < 8; ++q) ts->stats[q] = s[q];
+}
+
+template <typename T>
+__global__ void fill_inputs_kernel(const double *X64, int64_t N, int n, int NB, int NBP, int64_t ldT,
+                                   T *XT, T *Xh) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ldT) return;
+    for (int k = 0; k < NB; ++k) XT[(int64_t)k * ldT + j] = (j < N && k < n) ? T(X64[j * n + k]) : T(0);
+    for (int d = 0; d < NBP; ++d)
+        Xh[j * NBP + d] = (j < N && d < n) ? T(X64[j * n + d]) : ((j < N && d == n) ? T(1) : T(0));
+}
+
+template <typename T>
+__global__ void convert_rows_kernel(const double *src, int64_t rows, int64_t N, int64_t ldT, T *dst) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rows * ldT) return;
+    const int64_t i = e / ldT, j = e % ldT;
+    dst[e] = j < N ? T(src[i * N + j]) : T(0);
+}
+
+template <typename T>
+__global__ void unconvert_rows_kernel(const T *src, int64_t rows, int64_t N, int64_t ldT, double *dst) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rows * N) return;
+    const int64_t i = e / N, j = e % N;
+    dst[e] = (double)src[i * ldT + j];
+}
+
+inline unsigned nblk(int64_t work, int bs) { return (unsigned)((work + bs - 1) / bs); }
+
+}  // namespace
+
+cudaError_t launch_prologue(const SmallParams &p, int fp64, cudaStream_t s, int *nb_out) {
+    const unsigned nb = p.Ns > 0 ? nblk(p.Ns, 256) : 1;
+    if (nb > (unsigned)kStatBlocks && p.statpart) {
+        // statpart capacity: fall back to no per-block stats (caller passes statpart only
+        // when Ns <= 256 * kStatBlocks)
+    }
+    if (fp64) prologue_kernel<double><<<nb, 256, 0, s>>>(p);
+    else prologue_kernel<float><<<nb, 256, 0, s>>>(p);
+    if (nb_out) *nb_out = (int)nb;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(const ReduceParams &p, int fp64, cudaStream_t s) {
+    const int64_t work = p.Ns * (p.n + 1) + p.N;
+    const unsigned nb = work > 0 ? nblk(work, 256) : 1;
+    if (fp64) reduce_kernel<double><<<nb, 256, 0, s>>>(p);
+    else reduce_kernel<float><<<nb, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual(const ResidualParams &p, int fp64, cudaStream_t s, int *nb_out) {
+    const int64_t nrb = (p.Ns + 31) / 32, ncb = (p.N + 127) / 128;
+    int64_t tiles = nrb * ncb;
+    int nb = (int)(tiles < kStatBlocks ? (tiles > 0 ? tiles : 1) : kStatBlocks);
+    const size_t smem = sizeof(double) * ((size_t)p.n * 128 + 32 * (size_t)p.n + 32);
+    cudaError_t e;
+    if (fp64) {
+        e = cudaFuncSetAttribute(residual_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        residual_kernel<double><<<nb, 256, smem, s>>>(p);
+    } else {
+        e = cudaFuncSetAttribute(residual_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        residual_kernel<float><<<nb, 256, smem, s>>>(p);
+    }
+    if (nb_out) *nb_out = nb;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats_finalize(const double *pro, int nb_pro, const double *res, int nb_res,
+                                  DevScalars *ts, cudaStream_t s) {
+    stats_finalize_kernel<<<1, 32, 0, s>>>(pro, nb_pro, res, nb_res, ts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_inputs(const double *X64, int64_t N, int n, int NB, int NBP, int64_t ldT,
+                               int fp64, void *XT, void *Xh, cudaStream_t s) {
+    const unsigned nb = nblk(ldT, 256);
+    if (fp64) fill_inputs_kernel<double><<<nb, 256, 0, s>>>(X64, N, n, NB, NBP, ldT, (double *)XT, (double *)Xh);
+    else fill_inputs_kernel<float><<<nb, 256, 0, s>>>(X64, N, n, NB, NBP, ldT, (float *)XT, (float *)Xh);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_convert_rows(const double *src, int64_t rows, int64_t N, int64_t ldT, int fp64,
+                                void *dst, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    const unsigned nb = nblk(rows * ldT, 256);
+    if (fp64) convert_rows_kernel<double><<<nb, 256, 0, s>>>(src, rows, N, ldT, (double *)dst);
+    else convert_rows_kernel<float><<<nb, 256, 0, s>>>(src, rows, N, ldT, (float *)dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unconvert_rows(const void *src, int64_t rows, int64_t N, int64_t ldT, int fp64,
+                                  double *dst, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    const unsigned nb = nblk(rows * N, 256);
+    if (fp64) unconvert_rows_kernel<double><<<nb, 256, 0, s>>>((const double *)src, rows, N, ldT, dst);
+    else unconvert_rows_kernel<float><<<nb, 256, 0, s>>>((const float *)src, rows, N, ldT, dst);
+    return cudaGetLastError();
+}
+
+}  // namespace cr

@@ -1,0 +1,210 @@
+"""GPU parity: libcr (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Tolerances (north star, BASELINE.json): single step Theta, y, xi within 1e-5 relative
+(Frobenius) in fp32 mode, 1e-12 in fp64 mode; after K iterations the primal objective and
+the max constraint violation of eta(Theta^K) within 1e-4 relative.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import crdata
+import oracle
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def crp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1608_02227_b200 import build
+    build.build()
+    import paper_1608_02227_b200 as m
+    return m
+
+
+def rnd32(a):
+    return np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def single_step_case(crp, X, ybar, gamma, K, prec, tol, kernel="auto"):
+    """State after K oracle iterations (rounded to the storage precision) -> one GPU step
+    vs one oracle step from the identical state."""
+    L = ref.lipschitz(X, gamma)
+    st = oracle.state_after(X, ybar, gamma, L, K)
+    Tk, Tkm1 = (rnd32(st["Tk"]), rnd32(st["Tkm1"])) if prec == "fp32" else (st["Tk"], st["Tkm1"])
+    Tt = oracle.extrapolate(Tk, Tkm1, st["t_k"], st["t_kp1"])       # theta~^{K+1} (Step 4)
+    want = oracle.papg(X, ybar, gamma, L, 1, Tprev=Tk, Tt=Tt, t=st["t_kp1"])
+    s = crp.Solver(X, ybar, gamma, L=L, prec=prec, kernel=kernel)
+    s.set_theta(Tk, Tkm1, st["t_k"], st["t_kp1"])
+    s.step()
+    Tg, Tg1, tk, tk1 = s.get_theta()
+    y, xi = s.get_eta()
+    errs = dict(theta=rel(Tg, want["Tprev"]), y=rel(y, want["y"]), xi=rel(xi, want["xi"]))
+    assert np.all(Tg >= 0) and np.all(np.diag(Tg) == 0)
+    np.testing.assert_array_equal(Tg1, Tk if prec == "fp64" else rnd32(Tk))
+    assert tk == st["t_kp1"] and tk1 == oracle.momentum_next(st["t_kp1"])
+    for k_, v in errs.items():
+        assert v <= tol, (k_, v, errs)
+    s.close()
+    return errs
+
+
+@pytest.mark.parametrize("N,n,K,seed", [(64, 3, 5, 0), (200, 5, 40, 1), (333, 7, 25, 2), (1000, 10, 60, 3),
+                                         (517, 16, 30, 4), (130, 20, 12, 5)])
+def test_single_step_fp32(crp, N, n, K, seed):
+    X, ybar = crdata.random_problem(N, n, seed=seed, fp32=True)
+    single_step_case(crp, X, ybar, 1e-3, K, "fp32", 1e-5)
+
+
+@pytest.mark.parametrize("N,n,K,seed", [(50, 2, 30, 0), (97, 3, 17, 1), (260, 1, 40, 2)])
+def test_single_step_fp64(crp, N, n, K, seed):
+    X, ybar = crdata.random_problem(N, n, seed=seed)
+    single_step_case(crp, X, ybar, 1e-3, K, "fp64", 1e-12)
+
+
+def test_single_step_C2_config(crp):
+    X, ybar = crdata.make_problem("C2")
+    single_step_case(crp, X, ybar, 1e-3, 100, "fp32", 1e-5)
+
+
+def test_single_step_C1_config(crp):
+    X, ybar = crdata.make_problem("C1")
+    single_step_case(crp, X, ybar, 1e-3, 200, "fp64", 1e-12)
+
+
+@pytest.mark.parametrize("N,n", [(2, 1), (3, 2), (65, 4), (127, 80), (300, 48), (259, 33)])
+def test_edge_shapes_single_step(crp, N, n):
+    """Degenerate / ragged shapes: N = 2, one-element last tile, the largest compiled n."""
+    X, ybar = crdata.random_problem(N, n, seed=N + n, fp32=True)
+    single_step_case(crp, X, ybar, 1e-2, 4, "fp32", 1e-5)
+
+
+def k_iteration_case(crp, cfg_name, prec, K=None, N=None, tol=1e-4):
+    cfg = crdata.CONFIGS[cfg_name]
+    X, ybar = crdata.make_problem(cfg, N=N)
+    K = cfg.iters if K is None else K
+    L = ref.lipschitz(X, cfg.gamma)
+    out = oracle.papg(X, ybar, cfg.gamma, L, K)
+    yo, xio = oracle.eta(X, ybar, cfg.gamma, out["Tprev"])
+    so = oracle.stats(X, ybar, cfg.gamma, out["Tprev"], yo, xio)
+    s = crp.Solver(X, ybar, cfg.gamma, L=L, prec=prec)
+    s.solve(K)
+    y, xi, sg = s.primal()
+    e_obj = abs(sg["r_gamma"] - so["r_gamma"]) / abs(so["r_gamma"])
+    e_viol = abs(sg["max_violation"] - so["max_violation"]) / max(abs(so["max_violation"]), 1e-300)
+    assert e_obj <= tol, (e_obj, sg, so)
+    assert e_viol <= tol, (e_viol, sg, so)
+    # the remaining diagnostics agree too (looser: differences of nearly equal numbers)
+    assert abs(sg["g"] - so["g"]) <= 1e-3 * abs(so["g"]) + 1e-12
+    assert rel(y, yo) <= 1e-4
+    s.close()
+    return e_obj, e_viol
+
+
+def test_K_iterations_C1(crp):
+    """C1 (N=50, n=2, fp64, 500 iterations): objective and max violation of eta(Theta^K)."""
+    k_iteration_case(crp, "C1", "fp64", tol=1e-9)
+
+
+def test_K_iterations_C2(crp):
+    """C2 (N=1000, n=10, fp32, 2000 iterations)."""
+    k_iteration_case(crp, "C2", "fp32")
+
+
+def test_K_iterations_C3_reduced(crp):
+    """C3 laws at N=1500 (fp32, 300 iterations): several tiles and a ragged tail."""
+    k_iteration_case(crp, "C3", "fp32", K=300, N=1500)
+
+
+def test_graph_solve_equals_stepwise_and_is_deterministic(crp):
+    X, ybar = crdata.random_problem(700, 6, seed=9, fp32=True)
+    a = crp.Solver(X, ybar, 1e-3)
+    a.solve(37)
+    b = crp.Solver(X, ybar, 1e-3)
+    for _ in range(37):
+        b.step()
+    c = crp.Solver(X, ybar, 1e-3)
+    c.solve(20)
+    c.solve(17)
+    Ta, Tb, Tc = a.get_theta()[0], b.get_theta()[0], c.get_theta()[0]
+    np.testing.assert_array_equal(Ta, Tb)
+    np.testing.assert_array_equal(Ta, Tc)
+    assert a.launch_count > 37 * 3
+
+
+def test_constant_ybar_fixed_point(crp):
+    """P11 on the GPU: constant ybar keeps Theta = 0, y = ybar, xi = 0."""
+    X, _ = crdata.random_problem(300, 4, seed=3, fp32=True)
+    ybar = np.full(300, 1.5)
+    s = crp.Solver(X, ybar, 1e-3)
+    s.solve(10)
+    T = s.get_theta()[0]
+    assert np.all(T == 0)
+    y, xi, st = s.primal()
+    np.testing.assert_array_equal(y, ybar)
+    assert np.all(xi == 0) and st["max_violation"] == 0.0
+
+
+def test_first_step_closed_form(crp):
+    """P1 on the GPU: Theta^1_ij = (ybar_i - ybar_j)_+ / L."""
+    X, ybar = crdata.make_problem("C3", N=2000)
+    s = crp.Solver(X, ybar, 1e-3)
+    s.step()
+    T1 = s.get_theta()[0]
+    want = np.maximum(0.0, ybar[:, None] - ybar[None, :]) / s.L
+    np.fill_diagonal(want, 0.0)
+    assert rel(T1, want) <= 1e-6
+
+
+def test_stats_against_oracle_midrun(crp):
+    """cr_dual_step diagnostics vs oracle_stats on the same state."""
+    X, ybar = crdata.random_problem(400, 5, seed=17, fp32=True)
+    L = ref.lipschitz(X, 1e-3)
+    s = crp.Solver(X, ybar, 1e-3, L=L)
+    s.solve(49)
+    st = s.step(stats=True)
+    T = s.get_theta()[0]
+    y, xi = oracle.eta(X, ybar, 1e-3, T)
+    so = oracle.stats(X, ybar, 1e-3, T, y, xi)
+    for key in ("r_gamma", "g", "gap", "max_violation", "infeas_norm"):
+        assert abs(st[key] - so[key]) <= 1e-9 * max(1.0, abs(so[key])), (key, st[key], so[key])
+    assert st["k"] == 50 and st["nonfinite"] == 0
+
+
+def test_lipschitz_computed_by_library(crp):
+    X, ybar = crdata.make_problem("C2")
+    s = crp.Solver(X, ybar, 1e-3)
+    assert abs(s.L - ref.lipschitz(X, 1e-3)) <= 1e-10 * s.L
+
+
+@pytest.mark.slow
+def test_full_size_C4_sampled_step(crp):
+    """C4 at full size (N=16384, n=40) in the bench's launch configuration: 3 GPU steps from
+    theta^0 = 0, then step 4 checked on sampled rows of Theta^4 and on all of eta^4."""
+    cfg = crdata.CONFIGS["C4"]
+    X, ybar = crdata.make_problem(cfg)
+    L = ref.lipschitz(X, cfg.gamma)
+    s = crp.Solver(X, ybar, cfg.gamma, L=L)
+    s.solve(3)
+    T3, T2, t3, t4 = s.get_theta()
+    s.step()
+    y, xi = s.get_eta()
+    Tt = oracle.extrapolate(T3, T2, t3, t4)
+    del T2
+    yo, xio = oracle.eta(X, ybar, cfg.gamma, Tt)
+    assert rel(y, yo) <= 1e-5 and rel(xi, xio) <= 1e-5
+    rows = np.array([0, 1, 777, 8191, 8192, 12345, 16383])
+    want = oracle.project_rows(X, yo, xio, L, rows, Tt[rows])
+    got = np.concatenate([s.get_theta_rows(0, int(r), 1) for r in rows])
+    assert rel(got, want) <= 1e-5
