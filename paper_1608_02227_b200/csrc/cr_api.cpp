@@ -118,6 +118,7 @@ struct cr_ctx {
     size_t ev_used = 0;
     // graphs per parity
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    cudaStream_t cap_stream = nullptr;   // private stream used only to record graphs
     ncclComm_t comm = nullptr;
 
     template <typename P> P *at(size_t off) { return reinterpret_cast<P *>(ws + off); }
@@ -365,9 +366,19 @@ cr_status build_graph(cr_ctx *ctx, int parity) {
     cudaGraph_t g = nullptr;
     const int b1 = ctx->b1, s1 = ctx->s1;
     const int64_t k = ctx->k, launches = ctx->launches;
-    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    // The caller's stream may be the legacy default stream, which cannot be captured: record
+    // on a private stream, replay on the caller's stream (cudaGraphLaunch(..., ctx->stream)).
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->cap_stream;
+    cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        ctx->stream = user;
+        return fail(ctx, CR_ERR_CUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(e));
+    }
     cr_status st = enqueue_step(ctx, false);
-    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    e = cudaStreamEndCapture(ctx->stream, &g);
+    ctx->stream = user;
     ctx->b1 = b1; ctx->s1 = s1; ctx->k = k; ctx->launches = launches;
     if (st != CR_OK) { if (g) cudaGraphDestroy(g); return st; }
     if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
@@ -732,6 +743,7 @@ void cr_destroy(cr_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     drop_graphs(ctx);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     for (auto e : ctx->ev) cudaEventDestroy(e);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     delete ctx;

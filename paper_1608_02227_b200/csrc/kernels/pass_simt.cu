@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
     T *colpart = static_cast<T *>(p.colpart);
     const int64_t ldT = p.ldT;
 
-    T beta = T(0);
-    if (MODE == MODE_STEP) beta = T((p.ts[0] - 1.0) / p.ts[1]);   // beta_{k-1} = (t_{k-1}-1)/t_k
+    double beta64 = 0.0;
+    if (MODE == MODE_STEP) beta64 = (p.ts[0] - 1.0) / p.ts[1];   // beta_{k-1} = (t_{k-1}-1)/t_k
 
     // X-tile loader (cp.async): X^T tile [NB][BN], [X|1] tile [BN][NBP], y' tile [BN]
     auto load_xtile = [&](int64_t cb, int buf) {
@@ -242,14 +242,11 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
             T yj[4], bi[4];
             lds4(ys + tx * 4, yj);
             lds4(bS + ty * 4, bi);
-            T acc[4][4];
+            T acc[4][4];                                     // -> -(C eta)_ij / L
 #pragma unroll
             for (int r = 0; r < 4; ++r)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    T tt = cb1[r][c] + beta * (cb1[r][c] - cb2[r][c]);   // theta~ (Step 4)
-                    acc[r][c] = tt - (yj[c] + bi[r]);
-                }
+                for (int c = 0; c < 4; ++c) acc[r][c] = -(yj[c] + bi[r]);
 #pragma unroll 4
             for (int k = 0; k < NB; ++k) {
                 T xv[4], xj[4];
@@ -267,7 +264,11 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
                 for (int c = 0; c < 4; ++c) {
                     const int64_t gj = gj0 + c;
                     const bool ok = (lr < p.Ns) && (gj < p.N) && (gj != gr);
-                    th[r][c] = ok ? fmax0(acc[r][c]) : T(0);         // ( . )_+  (Step 2)
+                    // theta~ (Step 4 of the previous iteration) - (C eta)/L, combined in fp64 so
+                    // the stored value carries one rounding
+                    const double b1 = (double)cb1[r][c];
+                    const double v = fma(beta64, b1 - (double)cb2[r][c], b1) + (double)acc[r][c];
+                    th[r][c] = ok ? T(fmax(v, 0.0)) : T(0);           // ( . )_+  (Step 2)
                 }
                 st4cs(B2 + lr * ldT + gj0, th[r]);
             }
