@@ -36,14 +36,28 @@ struct Layout {
     int64_t N = 0, S = 0, Ns = 0, row0 = 0, Rp = 0, ldT = 0;
     int n = 0, NB = 0, NBP = 0, nRB = 0, world = 1, fp64 = 0;
     size_t es = 4;
+    // tensor-core pass
+    bool tc = false;
+    int NK = 0, NP2 = 0, NPAN = 0, nCBtc = 0, nRBtc = 0;
     // byte offsets
     size_t th[2], XT, Xh, X64, ybar, r[2], c[2], P[2], y64, yv, bv, XiT, Xi64, a64, colpart, rowpart,
-        slot0, rb_ptr, rb_slots, cfull, ts, statpro, statres, total;
+        slot0, rb_ptr, rb_slots, cfull, ts, statpro, statres, xhi, xlo, XiR, slot0_tc, rb_ptr_tc, rb_slots_tc,
+        total;
 };
+
+// Kernel the library uses for this shape: the tcgen05 pass for fp32 with n >= 16 (where the
+// two rank-n contractions make the CUDA-core pass FFMA-bound), else the SIMT pass.
+bool use_tc(int n, cr_precision prec, cr_kernel kernel) {
+    if (prec != CR_FP32) return false;
+    if (kernel == CR_KERNEL_TC) return true;
+    if (kernel == CR_KERNEL_SIMT) return false;
+    return n >= 16;
+}
 
 bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank, int world, Layout *L) {
     if (N < 2 || n < 1 || world < 1 || rank < 0 || rank >= world) return false;
-    if (kernel == CR_KERNEL_TC) return false;  // tensor-core pass not built in this library version
+    if (kernel == CR_KERNEL_TC && prec != CR_FP32) return false;
+    L->tc = use_tc(n, prec, kernel);
     L->N = N;
     L->n = n;
     L->world = world;
@@ -79,7 +93,17 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     L->Xi64 = take((size_t)L->Rp * n * 8);
     L->a64 = take((size_t)L->Rp * 8);
     L->colpart = take((size_t)L->nRB * L->ldT * es);
-    L->rowpart = take((size_t)(L->nRB + kGMax) * kBM * L->NBP * 8);
+    size_t rp_simt = (size_t)(L->nRB + kGMax) * kBM * L->NBP * 8;
+    if (L->tc) {
+        L->NK = (n + 7) / 8 * 8;
+        L->NP2 = (n + 1 + 15) / 16 * 16;
+        L->NPAN = (L->NP2 + 31) / 32;
+        L->nCBtc = (int)((N + kTcBN - 1) / kTcBN);
+        L->nRBtc = (int)(L->Rp / kTcBM);
+        if (192 + L->NP2 + 2 * L->NK > 512) return false;     // TMEM columns
+        rp_simt = std::max(rp_simt, (size_t)(L->nRBtc + kGMax) * kTcBM * L->NP2 * 8);
+    }
+    L->rowpart = take(rp_simt);
     L->slot0 = take((size_t)kGMax * 4);
     L->rb_ptr = take((size_t)(L->nRB + 1) * 4);
     L->rb_slots = take((size_t)(L->nRB + kGMax) * 4);
@@ -87,8 +111,66 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     L->ts = take(sizeof(DevScalars));
     L->statpro = take((size_t)(L->Rp / 256 + 2) * 8 * 8);
     L->statres = take((size_t)kStatBlocks * 8 * 8);
+    if (L->tc) {
+        const size_t img = (size_t)L->nCBtc * L->NPAN * kTcBN * 128;
+        L->xhi = take(img);
+        L->xlo = take(img);
+        L->XiR = take((size_t)L->Rp * L->NK * 4);
+        L->slot0_tc = take((size_t)kGMax * 4);
+        L->rb_ptr_tc = take((size_t)(L->nRBtc + 1) * 4);
+        L->rb_slots_tc = take((size_t)(L->nRBtc + kGMax) * 4);
+    }
     L->total = o;
     return true;
+}
+
+// Slot tables for a persistent pass with G CTAs over T = nRB x nCB tiles (row-major),
+// CTA g owning [g T / G, (g+1) T / G): slot0[g] = first row-partial slot of g; per row
+// block, the slots of the CTA runs that cover it, in CTA order.
+void slot_tables(int G, int64_t T, int nRB, int nCB, std::vector<int> &slot0, std::vector<int> &rb_ptr,
+                 std::vector<int> &slots) {
+    slot0.assign(G, 0);
+    rb_ptr.assign(nRB + 1, 0);
+    std::vector<std::vector<int>> per(nRB);
+    int cur = 0;
+    for (int g = 0; g < G; ++g) {
+        const int64_t t0 = (int64_t)g * T / G, t1 = (int64_t)(g + 1) * T / G;
+        slot0[g] = cur;
+        if (t0 >= t1) continue;
+        for (int64_t rb = t0 / nCB; rb <= (t1 - 1) / nCB; ++rb) per[rb].push_back(cur++);
+    }
+    slots.clear();
+    for (int rb = 0; rb < nRB; ++rb) {
+        rb_ptr[rb] = (int)slots.size();
+        slots.insert(slots.end(), per[rb].begin(), per[rb].end());
+    }
+    rb_ptr[nRB] = (int)slots.size();
+    if (slots.empty()) slots.push_back(0);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D tensor map over one Theta buffer (Rp rows x ldT fp32 columns), 128-B swizzled boxes of
+// 32 columns x 128 rows (the tensor-core pass tile).
+bool make_theta_tmap(CUtensorMap *m, void *base, int64_t rows, int64_t ldT) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            return false;
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)ldT, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldT * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)kTcBN, (cuuint32_t)kTcBM};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -119,6 +201,11 @@ struct cr_ctx {
     // graphs per parity
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     cudaStream_t cap_stream = nullptr;   // private stream used only to record graphs
+    // tensor-core pass
+    CUtensorMap tm[2];
+    int G_tc = 0, stages = 0, window = 64, smem_tc = 0;
+    uint32_t stage_bytes = 0;
+    int64_t T_tc = 0;
     ncclComm_t comm = nullptr;
 
     template <typename P> P *at(size_t off) { return reinterpret_cast<P *>(ws + off); }
@@ -182,7 +269,7 @@ PassParams pass_params(cr_ctx *ctx, int b_read, int b_write) {
     return p;
 }
 
-ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance) {
+ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance, bool tc = false) {
     const Layout &Ly = ctx->lay;
     ReduceParams q{};
     q.N = Ly.N;
@@ -190,12 +277,13 @@ ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance) {
     q.Rp = Ly.Rp;
     q.ldT = Ly.ldT;
     q.n = Ly.n;
-    q.NBP = Ly.NBP;
-    q.nRB = Ly.nRB;
+    q.NBP = tc ? Ly.NP2 : Ly.NBP;
+    q.nRB = tc ? Ly.nRBtc : Ly.nRB;
+    q.rbm = tc ? kTcBM : kBM;
     q.colpart = ctx->ws + Ly.colpart;
     q.rowpart = ctx->at<double>(Ly.rowpart);
-    q.rb_ptr = ctx->at<int>(Ly.rb_ptr);
-    q.rb_slots = ctx->at<int>(Ly.rb_slots);
+    q.rb_ptr = ctx->at<int>(tc ? Ly.rb_ptr_tc : Ly.rb_ptr);
+    q.rb_slots = ctx->at<int>(tc ? Ly.rb_slots_tc : Ly.rb_slots);
     q.r = ctx->r[slot];
     q.P = ctx->P[slot];
     q.c_out = ctx->world > 1 ? ctx->at<double>(Ly.cfull) : ctx->c[slot];
@@ -230,6 +318,37 @@ SmallParams small_params(cr_ctx *ctx, int sa, int sb, int use_beta, double scale
     p.statpart = stats ? ctx->at<double>(Ly.statpro) : nullptr;
     p.ts = ctx->at<DevScalars>(Ly.ts);
     p.use_beta = use_beta;
+    p.XiR = Ly.tc ? ctx->at<float>(Ly.XiR) : nullptr;
+    p.NK = Ly.NK;
+    return p;
+}
+
+TcParams tc_params(cr_ctx *ctx) {
+    const Layout &Ly = ctx->lay;
+    TcParams p{};
+    p.N = Ly.N;
+    p.Ns = Ly.Ns;
+    p.row0 = Ly.row0;
+    p.ldT = Ly.ldT;
+    p.T = ctx->T_tc;
+    p.G = ctx->G_tc;
+    p.nCB = Ly.nCBtc;
+    p.NK = Ly.NK;
+    p.NP2 = Ly.NP2;
+    p.NPAN = Ly.NPAN;
+    p.stages = ctx->stages;
+    p.window = ctx->window;
+    p.stage_bytes = ctx->stage_bytes;
+    p.smem_bytes = ctx->smem_tc;
+    p.xhi_img = ctx->at<float>(Ly.xhi);
+    p.xlo_img = ctx->at<float>(Ly.xlo);
+    p.yv = ctx->at<float>(Ly.yv);
+    p.XiR = ctx->at<float>(Ly.XiR);
+    p.bv = ctx->at<float>(Ly.bv);
+    p.colpart = ctx->at<float>(Ly.colpart);
+    p.rowpart = ctx->at<double>(Ly.rowpart);
+    p.cta_slot0 = ctx->at<int>(Ly.slot0_tc);
+    p.ts = ctx->at<double>(Ly.ts);
     return p;
 }
 
@@ -267,7 +386,6 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing) {
         NK(ncclAllGather(yv + (size_t)ctx->rank * Ly.S * Ly.es, yv, (size_t)Ly.S, nccl_t(ctx), ctx->comm,
                          ctx->stream));
     }
-    PassParams p = pass_params(ctx, b1, b2);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (allow_timing && ctx->timing) {
         e0 = next_event(ctx);
@@ -275,9 +393,15 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing) {
         if (!e0 || !e1) return fail(ctx, CR_ERR_CUDA, "cudaEventCreate failed");
         CK(cudaEventRecord(e0, ctx->stream));
     }
-    CK(launch_pass_simt(p, Ly.fp64, Ly.NB, MODE_STEP, ctx->stream));
+    if (Ly.tc) {
+        TcParams tp = tc_params(ctx);
+        CK(launch_pass_tc(ctx->tm[b1], ctx->tm[b2], tp, ctx->stream));
+    } else {
+        PassParams p = pass_params(ctx, b1, b2);
+        CK(launch_pass_simt(p, Ly.fp64, Ly.NB, MODE_STEP, ctx->stream));
+    }
     if (e1) CK(cudaEventRecord(e1, ctx->stream));
-    ReduceParams q = reduce_params(ctx, s2, 1);
+    ReduceParams q = reduce_params(ctx, s2, 1, Ly.tc);
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
     if (ctx->world > 1)
         NK(ncclReduceScatter(ctx->at<double>(Ly.cfull), ctx->c[s2], (size_t)Ly.S, ncclFloat64, ncclSum,
@@ -445,7 +569,6 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     if (cfg->prec != CR_FP32 && cfg->prec != CR_FP64) return CR_ERR_INVALID_ARG;
     if (cfg->prec == CR_FP64 && cfg->kernel == CR_KERNEL_TC) return CR_ERR_UNSUPPORTED;
     if (cfg->n > cr_max_dim()) return CR_ERR_UNSUPPORTED;
-    if (cfg->kernel == CR_KERNEL_TC) return CR_ERR_UNSUPPORTED;
     const int64_t N = cfg->N;
     const int n = cfg->n;
     for (int64_t i = 0; i < N * n; ++i)
@@ -456,13 +579,13 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     cr_ctx *ctx = new (std::nothrow) cr_ctx();
     if (!ctx) return CR_ERR_OOM;
     ctx->prec = cfg->prec;
-    ctx->kernel = CR_KERNEL_SIMT;
+    ctx->kernel = use_tc(cfg->n, cfg->prec, cfg->kernel) ? CR_KERNEL_TC : CR_KERNEL_SIMT;
     ctx->gamma = cfg->gamma;
     ctx->rank = cfg->rank;
     ctx->world = cfg->world;
     ctx->device = cfg->device;
     ctx->stream = static_cast<cudaStream_t>(cfg->stream);
-    if (!make_layout(N, n, cfg->prec, ctx->kernel, cfg->rank, cfg->world, &ctx->lay)) {
+    if (!make_layout(N, n, cfg->prec, cfg->kernel, cfg->rank, cfg->world, &ctx->lay)) {
         delete ctx;
         return CR_ERR_UNSUPPORTED;
     }
@@ -510,35 +633,46 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     h.t_cur = 1.0;    // t_1 = 1
     IK(cudaMemcpyAsync(ctx->ws + Ly.ts, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
 
-    // fused-pass grid: one full wave of resident CTAs, contiguous tile ranges
+    // SIMT fused-pass grid (also used for the read-only sums pass of cr_set_theta): one full
+    // wave of resident CTAs, contiguous tile ranges
     int smem = 0, bps = 0, nsm = 0;
     IK(pass_simt_config(Ly.fp64, Ly.NB, &smem, &bps));
     IK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
     ctx->nCB = (int)((N + kBN - 1) / kBN);
     ctx->T = (int64_t)Ly.nRB * ctx->nCB;
     ctx->G = (int)std::min<int64_t>({ctx->T, (int64_t)std::max(bps, 1) * nsm, (int64_t)kGMax});
-    {
-        std::vector<int> slot0(ctx->G), rb_ptr(Ly.nRB + 1, 0);
-        std::vector<std::vector<int>> per(Ly.nRB);
-        int cur = 0;
-        for (int g = 0; g < ctx->G; ++g) {
-            const int64_t t0 = (int64_t)g * ctx->T / ctx->G, t1 = (int64_t)(g + 1) * ctx->T / ctx->G;
-            slot0[g] = cur;
-            if (t0 >= t1) continue;
-            for (int64_t rb = t0 / ctx->nCB; rb <= (t1 - 1) / ctx->nCB; ++rb) per[rb].push_back(cur++);
-        }
-        std::vector<int> slots;
-        for (int rb = 0; rb < Ly.nRB; ++rb) {
-            rb_ptr[rb] = (int)slots.size();
-            slots.insert(slots.end(), per[rb].begin(), per[rb].end());
-        }
-        rb_ptr[Ly.nRB] = (int)slots.size();
-        IK(cudaMemcpyAsync(ctx->ws + Ly.slot0, slot0.data(), slot0.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-        IK(cudaMemcpyAsync(ctx->ws + Ly.rb_ptr, rb_ptr.data(), rb_ptr.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-        IK(cudaMemcpyAsync(ctx->ws + Ly.rb_slots, slots.data(), std::max<size_t>(slots.size(), 1) * 4,
-                           cudaMemcpyHostToDevice, ctx->stream));
-        IK(cudaStreamSynchronize(ctx->stream));   // host vectors go out of scope
+    std::vector<int> slot0, rb_ptr, slots, slot0t, rb_ptrt, slotst;
+    slot_tables(ctx->G, ctx->T, Ly.nRB, ctx->nCB, slot0, rb_ptr, slots);
+    IK(cudaMemcpyAsync(ctx->ws + Ly.slot0, slot0.data(), slot0.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    IK(cudaMemcpyAsync(ctx->ws + Ly.rb_ptr, rb_ptr.data(), rb_ptr.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    IK(cudaMemcpyAsync(ctx->ws + Ly.rb_slots, slots.data(), slots.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (Ly.tc) {
+        // tcgen05 pass: one persistent CTA per SM (512 TMEM columns, ~200 KB smem each)
+        ctx->T_tc = (int64_t)Ly.nRBtc * Ly.nCBtc;
+        ctx->G_tc = (int)std::min<int64_t>({ctx->T_tc, (int64_t)nsm, (int64_t)kGMax});
+        ctx->stage_bytes = (uint32_t)((2 * kTcBM * kTcBN * 4 + 2 * Ly.NPAN * kTcBN * 128 + kTcBN * 4 + 1023) / 1024 * 1024);
+        const size_t fixed = tc_barrier_bytes() + 1024 + 64;
+        const size_t budget = 227 * 1024;
+        ctx->stages = (int)std::min<size_t>(kTcMaxStages, (budget - fixed) / ctx->stage_bytes);
+        if (ctx->stages < 2) { fail(ctx, CR_ERR_UNSUPPORTED, "tc pass: smem"); return bail(CR_ERR_UNSUPPORTED); }
+        ctx->smem_tc = (int)(ctx->stages * (size_t)ctx->stage_bytes + fixed);
+        IK(pass_tc_prepare(ctx->smem_tc));
+        slot_tables(ctx->G_tc, ctx->T_tc, Ly.nRBtc, Ly.nCBtc, slot0t, rb_ptrt, slotst);
+        IK(cudaMemcpyAsync(ctx->ws + Ly.slot0_tc, slot0t.data(), slot0t.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        IK(cudaMemcpyAsync(ctx->ws + Ly.rb_ptr_tc, rb_ptrt.data(), rb_ptrt.size() * 4, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        IK(cudaMemcpyAsync(ctx->ws + Ly.rb_slots_tc, slotst.data(), slotst.size() * 4, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        IK(launch_tc_xhat(ctx->at<double>(Ly.X64), N, n, Ly.NPAN, Ly.nCBtc, ctx->at<float>(Ly.xhi),
+                          ctx->at<float>(Ly.xlo), ctx->stream));
+        ctx->launches += 1;
+        for (int b = 0; b < 2; ++b)
+            if (!make_theta_tmap(&ctx->tm[b], ctx->th[b], Ly.Rp, Ly.ldT)) {
+                fail(ctx, CR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                return bail(CR_ERR_CUDA);
+            }
     }
+    IK(cudaStreamSynchronize(ctx->stream));   // host vectors go out of scope
 #undef IK
     if (ctx->world > 1) {
         ncclUniqueId id;

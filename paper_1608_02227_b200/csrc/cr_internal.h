@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace cr {
@@ -14,6 +15,9 @@ constexpr int kGMax = 4096;       // upper bound on fused-pass CTAs (slot table 
 constexpr int kRowAlign = 128;    // Theta rows allocated per shard rounded to this
 constexpr int kColAlign = 256;    // Theta row pitch (elements) rounded to this
 constexpr int kStatBlocks = 1024; // max CTAs of the stats/residual kernels
+constexpr int kTcBM = 128;        // tensor-core pass tile rows (TMEM lanes)
+constexpr int kTcBN = 32;         // tensor-core pass tile columns
+constexpr int kTcMaxStages = 6;
 
 // n-buckets compiled for the SIMT pass (S-GEMM depth NB; P-GEMM width NBP = NB + 4).
 int simt_bucket(int n);           // smallest compiled NB >= n, or 0 if none
@@ -66,13 +70,15 @@ struct SmallParams {
     double *statpart;      // [kStatBlocks][8] per-CTA partials
     DevScalars *ts;
     int use_beta;          // 1: beta from ts (Step 1 at theta~^k); 0: beta = 0 (eta(Theta^k))
+    float *XiR;            // optional [Rp][NK] row-major xi * scale (tensor-core pass operand)
+    int NK;
 };
 
 cudaError_t launch_prologue(const SmallParams &p, int prec_fp64, cudaStream_t s, int *nblocks_out);
 
 struct ReduceParams {
     int64_t N, Ns, Rp, ldT;
-    int n, NBP, nRB;
+    int n, NBP, nRB, rbm;  // rbm: rows per row block of the pass that wrote the partials
     const void *colpart;   // [nRB][ldT]
     const double *rowpart; // [slots][kBM][NBP]
     const int *rb_ptr;     // [nRB + 1]
@@ -100,6 +106,28 @@ cudaError_t launch_residual(const ResidualParams &p, int prec_fp64, cudaStream_t
 // into ts->stats[0..7] (rank-local).
 cudaError_t launch_stats_finalize(const double *pro, int nb_pro, const double *res, int nb_res,
                                   DevScalars *ts, cudaStream_t s);
+
+struct TcParams {
+    int64_t N, Ns, row0, ldT, T;
+    int G, nCB, NK, NP2, NPAN, stages, window;
+    uint32_t stage_bytes;
+    int smem_bytes;
+    const float *xhi_img, *xlo_img;  // [nCB][NPAN][32 x 128 B] swizzled X-hat tiles
+    const float *yv;                 // y * scale, gathered
+    const float *XiR;                // [Rp][NK] xi * scale
+    const float *bv;                 // [Rp] (a - y) * scale
+    float *colpart;                  // [nRB128][ldT]
+    double *rowpart;                 // [slots][128][NP2]
+    const int *cta_slot0;
+    const double *ts;
+};
+
+// tcgen05 fused pass (kernels/pass_tc.cu).
+cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const TcParams &p, cudaStream_t s);
+cudaError_t pass_tc_prepare(int smem_bytes);
+size_t tc_barrier_bytes();
+cudaError_t launch_tc_xhat(const double *X64, int64_t N, int n, int NPAN, int nCB, float *hi, float *lo,
+                           cudaStream_t s);
 
 // Column-major helpers for initialisation.
 cudaError_t launch_fill_inputs(const double *X64, int64_t N, int n, int NB, int NBP, int64_t ldT,

@@ -40,6 +40,7 @@ __global__ void prologue_kernel(const SmallParams p) {
             const double xi = (rt * x[d] - Pt) / p.gamma;   // (A2^T theta~)_i / gamma
             p.Xi64[i * p.n + d] = xi;
             XiT[(int64_t)d * p.Rp + i] = T(xi * p.scale);
+            if (p.XiR) p.XiR[i * p.NK + d] = (float)(xi * p.scale);
             a += xi * x[d];
             xi2 += xi * xi;
         }
@@ -69,10 +70,10 @@ __global__ void reduce_kernel(const ReduceParams p) {
     if (g < nrow) {
         const int64_t i = g / (p.n + 1);
         const int d = (int)(g % (p.n + 1));
-        const int rb = (int)(i / kBM), ii = (int)(i % kBM);
+        const int rb = (int)(i / p.rbm), ii = (int)(i % p.rbm);
         double s = 0.0;
         for (int e = p.rb_ptr[rb]; e < p.rb_ptr[rb + 1]; ++e)
-            s += p.rowpart[((int64_t)p.rb_slots[e] * kBM + ii) * p.NBP + d];
+            s += p.rowpart[((int64_t)p.rb_slots[e] * p.rbm + ii) * p.NBP + d];
         if (d < p.n) p.P[i * p.n + d] = s;
         else p.r[i] = s;
     } else if (g < nrow + p.N) {

@@ -67,6 +67,21 @@ def test_single_step_fp32(crp, N, n, K, seed):
     single_step_case(crp, X, ybar, 1e-3, K, "fp32", 1e-5)
 
 
+@pytest.mark.parametrize("N,n,K,seed", [(130, 16, 6, 0), (300, 20, 30, 1), (517, 33, 25, 2), (1000, 40, 40, 3),
+                                         (129, 80, 8, 4), (2100, 24, 20, 5), (33, 17, 3, 6)])
+def test_single_step_fp32_tensor_core(crp, N, n, K, seed):
+    """The tcgen05 (3xTF32) fused pass: several 128x32 tiles, ragged row and column tails."""
+    X, ybar = crdata.random_problem(N, n, seed=seed, fp32=True)
+    single_step_case(crp, X, ybar, 1e-3, K, "fp32", 1e-5, kernel="tc")
+
+
+@pytest.mark.parametrize("N,n,K,seed", [(300, 20, 30, 1), (1000, 40, 40, 3), (129, 80, 8, 4)])
+def test_single_step_fp32_simt_large_n(crp, N, n, K, seed):
+    """The CUDA-core pass on shapes the library would route to the tensor cores."""
+    X, ybar = crdata.random_problem(N, n, seed=seed, fp32=True)
+    single_step_case(crp, X, ybar, 1e-3, K, "fp32", 1e-5, kernel="simt")
+
+
 @pytest.mark.parametrize("N,n,K,seed", [(50, 2, 30, 0), (97, 3, 17, 1), (260, 1, 40, 2)])
 def test_single_step_fp64(crp, N, n, K, seed):
     X, ybar = crdata.random_problem(N, n, seed=seed)
