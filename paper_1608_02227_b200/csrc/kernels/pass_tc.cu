@@ -28,18 +28,30 @@ using namespace sm100;
 
 constexpr int TBM = kTcBM;      // 128 rows per tile (TMEM lanes)
 constexpr int TBN = kTcBN;      // 32 columns per tile
-constexpr int NTHR = 192;       // 6 warps
+constexpr int NTHR = 384;       // 12 warps: producer, MMA, storer, spare, 2 x 4 epilogue
 constexpr uint32_t TILE_BYTES = TBM * TBN * 4;     // 16 KB
 constexpr uint32_t PANEL_BYTES = TBN * 128;        // 4 KB: 32 rows j x 32 fp32 (128 B)
 
 struct __align__(8) TcBarriers {
     uint64_t full[kTcMaxStages], empty[kTcMaxStages];
-    uint64_t d1_full[2], d1_empty[2], at_full[2], at_empty[2];
+    uint64_t d1_full[2], d1_empty[2], at_full[2], at_empty[2], st_full[2];
     uint64_t d2_full, d2_empty, xi_full;
     uint32_t tmem_base;
 };
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// butterfly step: lane keeps the half of v selected by its bit, adds the partner's other half
+template <int H>
+__device__ __forceinline__ void bfly(const float *v, float *o, int lane) {
+    const bool up = (lane & H) != 0;
+#pragma unroll
+    for (int c = 0; c < H; ++c) {
+        const float send = up ? v[c] : v[c + H];
+        const float keep = up ? v[c + H] : v[c];
+        o[c] = keep + __shfl_xor_sync(0xffffffffu, send, H);
+    }
+}
 
 __global__ void __launch_bounds__(NTHR, 1)
 pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2, const TcParams p) {
@@ -48,11 +60,12 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     const int S = p.stages;
     const uint32_t stage_bytes = p.stage_bytes;
     TcBarriers *bar = reinterpret_cast<TcBarriers *>(smem + (size_t)S * stage_bytes);
-    float *colS = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + sizeof(TcBarriers) + 8);  // [2][4][32]
+    float *colS = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + sizeof(TcBarriers) + 8);  // [2 wg][2][4][32]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t0 = (int64_t)blockIdx.x * p.T / p.G, t1 = (int64_t)(blockIdx.x + 1) * p.T / p.G;
     if (t0 >= t1) return;
+    const int64_t U = t1 - t0;
     const int nCB = p.nCB;
     const int NK = p.NK, NP2 = p.NP2, NPAN = p.NPAN;
     const uint32_t xpan_bytes = (uint32_t)NPAN * PANEL_BYTES;
@@ -60,8 +73,9 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     auto stage_ptr = [&](int s) { return smem + (size_t)s * stage_bytes; };
     // stage image: [B1 16K][B2 16K][Xhi NPAN*4K][Xlo NPAN*4K][y' 128B]
     auto run_start = [&](int64_t t) { return t == t0 || (t % nCB) == 0; };
+    auto run_end = [&](int64_t t) { return t + 1 == t1 || ((t + 1) % nCB) == 0; };
     auto flush_after = [&](int64_t t) {
-        if (t + 1 == t1 || ((t + 1) % nCB) == 0) return true;
+        if (run_end(t)) return true;
         const int64_t rs = (t / nCB) * nCB > t0 ? (t / nCB) * nCB : t0;
         return ((t - rs + 1) % p.window) == 0;
     };
@@ -71,6 +85,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         for (int b = 0; b < 2; ++b) {
             mbar_init(&bar->d1_full[b], 1); mbar_init(&bar->d1_empty[b], 4);
             mbar_init(&bar->at_full[b], 4); mbar_init(&bar->at_empty[b], 1);
+            mbar_init(&bar->st_full[b], 4);
         }
         mbar_init(&bar->d2_full, 1);
         mbar_init(&bar->d2_empty, 4);
@@ -83,15 +98,15 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bar->tmem_base;
-    // TMEM column map
+    // TMEM column map: D1[2] 0..63, Theta^k A operand [2] x (hi 32, lo 32) 64..191, D2, Xi' (hi, lo)
     const uint32_t c_d1 = 0, c_at = 64, c_d2 = 192, c_xi = 192 + (uint32_t)NP2;
 
     if (warp == 0) {
         // ============================================================ TMA producer
         if (lane == 0) {
             const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-            for (int64_t t = t0; t < t1; ++t) {
-                const int64_t u = t - t0;
+            for (int64_t u = 0; u < U; ++u) {
+                const int64_t t = t0 + u;
                 const int s = (int)(u % S);
                 mbar_wait(&bar->empty[s], (uint32_t)(((u / S) & 1) ^ 1));
                 const int64_t rb = t / nCB, cb = t % nCB;
@@ -112,8 +127,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             const uint32_t id2 = idesc_tf32(TBM, NP2, 0, 1);   // A K-major (TMEM), B MN-major (X tile, d inner)
             int64_t run = 0, flushes = 0;
             bool window_start = true;
-            auto gemm1 = [&](int64_t t) {
-                const int64_t u = t - t0;
+            auto gemm1 = [&](int64_t u) {
                 const int s = (int)(u % S), b = (int)(u & 1);
                 mbar_wait(&bar->full[s], (uint32_t)((u / S) & 1));
                 mbar_wait(&bar->d1_empty[b], (uint32_t)(((u >> 1) & 1) ^ 1));
@@ -135,11 +149,11 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             };
             mbar_wait(&bar->xi_full, 0);
             tc_fence_after();
-            gemm1(t0);
-            for (int64_t t = t0; t < t1; ++t) {
-                const int64_t u = t - t0;
-                const bool next_same_run = (t + 1 < t1) && !run_start(t + 1);
-                if (next_same_run) gemm1(t + 1);
+            gemm1(0);
+            for (int64_t u = 0; u < U; ++u) {
+                const int64_t t = t0 + u;
+                const bool next_same_run = (u + 1 < U) && !run_start(t + 1);
+                if (next_same_run) gemm1(u + 1);
                 const int s = (int)(u % S), a = (int)(u & 1);
                 mbar_wait(&bar->at_full[a], (uint32_t)((u >> 1) & 1));
                 if (window_start && flushes > 0) mbar_wait(&bar->d2_empty, (uint32_t)((flushes - 1) & 1));
@@ -165,34 +179,46 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     ++flushes;
                     window_start = true;
                 }
-                if (t + 1 < t1 && !next_same_run) {
+                if (u + 1 < U && !next_same_run) {
                     ++run;
                     mbar_wait(&bar->xi_full, (uint32_t)(run & 1));
                     tc_fence_after();
-                    gemm1(t + 1);
+                    gemm1(u + 1);
                 }
             }
         }
-    } else {
-        // ============================================================ epilogue (4 warps)
+    } else if (warp == 2) {
+        // ============================================================ TMA storer
+        if (lane == 0) {
+            const uint64_t pol_stream = policy_evict_first();
+            for (int64_t u = 0; u < U; ++u) {
+                const int64_t t = t0 + u;
+                const int s = (int)(u % S), w = (int)(u & 1);
+                mbar_wait(&bar->st_full[w], (uint32_t)((u >> 1) & 1));
+                tma_store_2d(&tmB2, (int)((t % nCB) * TBN), (int)((t / nCB) * TBM), stage_ptr(s) + TILE_BYTES,
+                             pol_stream);
+                bulk_commit();
+                bulk_wait_read<0>();                      // slot read by the store engine
+                mbar_arrive(&bar->empty[s]);
+            }
+            bulk_wait<0>();
+        }
+    } else if (warp >= 4) {
+        // ============================================================ epilogue: 2 warpgroups, ping-pong tiles
+        const int wg = (warp - 4) >> 2;               // warpgroup: tiles u with u % 2 == wg
         const int q = warp & 3;                       // TMEM lane quarter
         const int r = q * 32 + lane;                  // row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const float beta = (float)((p.ts[0] - 1.0) / p.ts[1]);   // beta_{k-1} = (t_{k-1}-1)/t_k
-        const double beta64 = (p.ts[0] - 1.0) / p.ts[1];
-        (void)beta64;
-        const bool store_thread = (threadIdx.x == 64);
+        int64_t flushes = 0;
+        int flush_in_run = 0;
         int slot = p.cta_slot0[blockIdx.x];
-        bool first_flush = true;
-        int64_t flushes = 0, run = 0;
         float bi = 0.f;
-        int64_t prev_s = -1;
+        float *my_colS = colS + wg * 2 * 4 * 32;
 
         auto load_xi = [&](int64_t rb) {
-            // Xi' row r of row block rb into TMEM (hi and lo columns), b'_i into a register
-            const int64_t lr = rb * TBM + r;
-            const float *src = p.XiR + lr * NK;
-            bi = p.bv[lr];
+            // Xi' row r of row block rb into TMEM (hi and lo columns)
+            const float *src = p.XiR + (rb * TBM + r) * NK;
             for (int k0 = 0; k0 < NK; k0 += 8) {
                 uint32_t hi[8], lo[8];
 #pragma unroll
@@ -210,168 +236,140 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->xi_full);
         };
-
-        load_xi(t0 / nCB);
-        for (int64_t t = t0; t < t1; ++t) {
-            const int64_t u = t - t0;
-            const int s = (int)(u % S), b = (int)(u & 1);
-            const int64_t rb = t / nCB, cb = t % nCB;
-            if (t != t0 && run_start(t)) { ++run; load_xi(rb); }
-
-            // ---- S' = Xi' X^T from TMEM
-            mbar_wait(&bar->d1_full[b], (uint32_t)((u >> 1) & 1));
+        // flush of the row accumulator after tile tf (done by warpgroup 0 only, in tile order,
+        // so every slot sees its window partials added in a fixed order)
+        auto flush = [&](int64_t tf) {
+            mbar_wait(&bar->d2_full, (uint32_t)(flushes & 1));
             tc_fence_after();
-            uint32_t sv[32];
-            {
-                uint32_t a0[16], a1[16];
-                tmem_ld16(tmem + lane_off + c_d1 + (uint32_t)b * TBN, a0);
-                tmem_ld16(tmem + lane_off + c_d1 + (uint32_t)b * TBN + 16, a1);
+            double *dst = p.rowpart + ((int64_t)slot * TBM + r) * NP2;
+            for (int d0 = 0; d0 < NP2; d0 += 16) {
+                uint32_t a[16];
+                tmem_ld16(tmem + lane_off + c_d2 + (uint32_t)d0, a);
                 tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 16; ++e) { sv[e] = a0[e]; sv[16 + e] = a1[e]; }
+                for (int e = 0; e < 16; ++e) {
+                    const double v = (double)__uint_as_float(a[e]);
+                    if (flush_in_run == 0) dst[d0 + e] = v;
+                    else dst[d0 + e] += v;                 // same thread, in order: deterministic
+                }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar->d1_empty[b]);
+            if (lane == 0) mbar_arrive(&bar->d2_empty);
+            ++flushes;
+            ++flush_in_run;
+            if (run_end(tf)) { ++slot; flush_in_run = 0; }
+        };
 
-            // ---- Theta tiles landed?
+        if (wg == 0) load_xi(t0 / nCB);
+        for (int64_t u = wg; u < U; u += 2) {
+            const int64_t t = t0 + u;
+            const int s = (int)(u % S), b = (int)(u & 1);
+            const int64_t rb = t / nCB, cb = t % nCB;
+            if (u > 0 && run_start(t)) {
+                // new run: all GEMM1 of the previous run are complete once D1 of tile u-1 is
+                mbar_wait(&bar->d1_full[b ^ 1], (uint32_t)(((u - 1) >> 1) & 1));
+                load_xi(rb);
+            }
+            const int64_t lr = rb * TBM + r, gr = p.row0 + lr;
+            bi = p.bv[lr];
+            // ---- Theta tiles landed? (B1, B2, y' of this tile)
             mbar_wait(&bar->full[s], (uint32_t)((u / S) & 1));
             uint8_t *st = stage_ptr(s);
             const float *yt = reinterpret_cast<const float *>(st + 2 * TILE_BYTES + 2 * xpan_bytes);
             uint8_t *rowB1 = st + r * 128, *rowB2 = st + TILE_BYTES + r * 128;
-            const int64_t lr = rb * TBM + r, gr = p.row0 + lr;
+            // ---- S' = Xi' X^T from TMEM
+            mbar_wait(&bar->d1_full[b], (uint32_t)((u >> 1) & 1));
+            tc_fence_after();
+            const bool clean = (gr < cb * TBN || gr >= cb * TBN + TBN) && (cb * TBN + TBN <= p.N) && (lr < p.Ns);
             float th[32];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int off = ((k ^ (r & 7)) << 4);
-                const float4 v1 = *reinterpret_cast<const float4 *>(rowB1 + off);
-                const float4 v2 = *reinterpret_cast<const float4 *>(rowB2 + off);
-                const float4 yv4 = *reinterpret_cast<const float4 *>(yt + 4 * k);
-                const float b1[4] = {v1.x, v1.y, v1.z, v1.w}, b2[4] = {v2.x, v2.y, v2.z, v2.w};
-                const float yj[4] = {yv4.x, yv4.y, yv4.z, yv4.w};
+            for (int half = 0; half < 2; ++half) {
+                uint32_t sv[16];
+                tmem_ld16(tmem + lane_off + c_d1 + (uint32_t)b * TBN + 16 * half, sv);
+                tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int c = 4 * k + e;
-                    const int64_t j = cb * TBN + c;
-                    const float acc = __uint_as_float(sv[c]) - (yj[e] + bi);   // -(C eta)_ij / L
-                    // theta~ + acc with one rounding of (b1 + acc) recovered exactly (TwoSum)
-                    const float dd = b1[e] - b2[e];
-                    const float sm = b1[e] + acc;
-                    const float bb = sm - b1[e];
-                    const float er = (b1[e] - (sm - bb)) + (acc - bb);
-                    const float v = fmaf(beta, dd, sm) + er;
-                    const bool ok = (lr < p.Ns) && (j < p.N) && (j != gr);
-                    th[c] = (ok && v > 0.f) ? v : 0.f;              // ( . )_+ (Step 2), mask
+                for (int k4 = 0; k4 < 4; ++k4) {
+                    const int k = 4 * half + k4;
+                    const int off = ((k ^ (r & 7)) << 4);
+                    const float4 v1 = *reinterpret_cast<const float4 *>(rowB1 + off);
+                    const float4 v2 = *reinterpret_cast<const float4 *>(rowB2 + off);
+                    const float4 yv4 = *reinterpret_cast<const float4 *>(yt + 4 * k);
+                    const float b1[4] = {v1.x, v1.y, v1.z, v1.w}, b2[4] = {v2.x, v2.y, v2.z, v2.w};
+                    const float yj[4] = {yv4.x, yv4.y, yv4.z, yv4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int c = 4 * k + e;
+                        const float acc = __uint_as_float(sv[4 * k4 + e]) - (yj[e] + bi);   // -(C eta)_ij / L
+                        // theta~ + acc: b1 + acc formed exactly (TwoSum), one final rounding
+                        const float dd = b1[e] - b2[e];
+                        const float sm = b1[e] + acc;
+                        const float bb = sm - b1[e];
+                        const float er = (b1[e] - (sm - bb)) + (acc - bb);
+                        const float v = fmaf(beta, dd, sm) + er;
+                        float o = fmaxf(v, 0.f);                                            // ( . )_+
+                        if (!clean) {
+                            const int64_t j = cb * TBN + c;
+                            if (!(lr < p.Ns && j < p.N && j != gr)) o = 0.f;                // diag / tails
+                        }
+                        th[c] = o;
+                    }
                 }
             }
-            // ---- Theta^k (hi = raw, lo = remainder) into TMEM as GEMM2's A operand
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar->d1_empty[b]);
+            // ---- Theta^k (hi = tf32 truncation, lo = remainder) into TMEM as GEMM2's A operand
             mbar_wait(&bar->at_empty[b], (uint32_t)(((u >> 1) & 1) ^ 1));
             tc_fence_after();
-            {
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
                 uint32_t h[16], l[16];
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const float x = th[16 * half + e];
-                        h[e] = __float_as_uint(x);
-                        l[e] = __float_as_uint(x - tf32_hi(x));
-                    }
-                    tmem_st16(tmem + lane_off + c_at + (uint32_t)b * 64 + 16 * half, h);
-                    tmem_st16(tmem + lane_off + c_at + (uint32_t)b * 64 + 32 + 16 * half, l);
+                for (int e = 0; e < 16; ++e) {
+                    const float x = th[16 * half + e];
+                    const float hx = tf32_hi(x);
+                    h[e] = __float_as_uint(hx);
+                    l[e] = __float_as_uint(x - hx);
                 }
+                tmem_st16(tmem + lane_off + c_at + (uint32_t)b * 64 + 16 * half, h);
+                tmem_st16(tmem + lane_off + c_at + (uint32_t)b * 64 + 32 + 16 * half, l);
             }
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->at_full[b]);
-
             // ---- Theta^k into the B2 slot (in place) for the TMA store
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int off = ((k ^ (r & 7)) << 4);
                 *reinterpret_cast<float4 *>(rowB2 + off) = make_float4(th[4 * k], th[4 * k + 1], th[4 * k + 2], th[4 * k + 3]);
             }
-            // ---- column sums over this warp's 32 rows (butterfly transpose-reduce)
-            {
-                float v16[16];
-                const bool up16 = lane & 16;
-#pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    const float send = up16 ? th[c] : th[c + 16];
-                    const float keep = up16 ? th[c + 16] : th[c];
-                    v16[c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                }
-                float v8[8];
-                const bool up8 = lane & 8;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float send = up8 ? v16[c] : v16[c + 8];
-                    const float keep = up8 ? v16[c + 8] : v16[c];
-                    v8[c] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                }
-                float v4[4];
-                const bool up4 = lane & 4;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const float send = up4 ? v8[c] : v8[c + 4];
-                    const float keep = up4 ? v8[c + 4] : v8[c];
-                    v4[c] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-                }
-                float v2[2];
-                const bool up2 = lane & 2;
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const float send = up2 ? v4[c] : v4[c + 2];
-                    const float keep = up2 ? v4[c + 2] : v4[c];
-                    v2[c] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-                }
-                const bool up1 = lane & 1;
-                const float send = up1 ? v2[0] : v2[1];
-                const float keep = up1 ? v2[1] : v2[0];
-                const float csum = keep + __shfl_xor_sync(0xffffffffu, send, 1);   // column = lane
-                colS[((u & 1) * 4 + q) * 32 + lane] = csum;
-            }
             fence_proxy_async_smem();
-            named_barrier(1, 128);
-            if (store_thread) {
-                tma_store_2d(&tmB2, (int)(cb * TBN), (int)(rb * TBM), st + TILE_BYTES, policy_evict_first());
-                bulk_commit();
-                bulk_wait_read<1>();                      // store of the previous tile has read its slot
-                if (prev_s >= 0) mbar_arrive(&bar->empty[prev_s]);
-                prev_s = s;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar->st_full[wg]);
+            // ---- column sums over this warp's 32 rows (butterfly transpose-reduce), then over warps
+            {
+                float v16[16], v8[8], v4[4], v2[2], v1[1];
+                bfly<16>(th, v16, lane);
+                bfly<8>(v16, v8, lane);
+                bfly<4>(v8, v4, lane);
+                bfly<2>(v4, v2, lane);
+                bfly<1>(v2, v1, lane);                                            // column = lane
+                my_colS[((((u >> 1) & 1) * 4) + q) * 32 + lane] = v1[0];
             }
+            named_barrier(1 + wg, 128);
             if (q == 0) {
-                const float *cs = colS + (u & 1) * 4 * 32;
+                const float *cs = my_colS + ((u >> 1) & 1) * 4 * 32;
                 const float c4 = (cs[lane] + cs[32 + lane]) + (cs[64 + lane] + cs[96 + lane]);
                 p.colpart[rb * p.ldT + cb * TBN + lane] = c4;
             }
-            // ---- row accumulator flush (fp64, per CTA run slot)
-            if (flush_after(t)) {
-                mbar_wait(&bar->d2_full, (uint32_t)(flushes & 1));
-                tc_fence_after();
-                double *dst = p.rowpart + ((int64_t)slot * TBM + r) * NP2;
-                for (int d0 = 0; d0 < NP2; d0 += 16) {
-                    uint32_t a[16];
-                    tmem_ld16(tmem + lane_off + c_d2 + (uint32_t)d0, a);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const double v = (double)__uint_as_float(a[e]);
-                        if (first_flush) dst[d0 + e] = v;
-                        else atomicAdd(dst + d0 + e, v);          // exclusive owner: ordered, deterministic
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar->d2_empty);
-                ++flushes;
-                first_flush = false;
-                if (t + 1 == t1 || ((t + 1) % nCB) == 0) { ++slot; first_flush = true; }
+            // ---- row accumulator flushes (warpgroup 0 handles those after tiles u and u+1)
+            if (wg == 0) {
+                if (flush_after(t)) flush(t);
+                if (u + 1 < U && flush_after(t + 1)) flush(t + 1);
             }
         }
-        if (store_thread) bulk_wait<0>();
-        (void)run;
     }
     tc_fence_before();
     __syncthreads();
@@ -389,7 +387,7 @@ cudaError_t pass_tc_prepare(int smem_bytes) {
     return cudaFuncSetAttribute(pass_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
 }
 
-size_t tc_barrier_bytes() { return sizeof(TcBarriers) + 8 + 2 * 4 * 32 * 4; }
+size_t tc_barrier_bytes() { return sizeof(TcBarriers) + 8 + 2 * 2 * 4 * 32 * 4; }
 
 // X-hat images for the TC pass: per 32-column tile, NPAN panels of [32 rows j][32 d] fp32,
 // 128-B rows with the SW128 chunk swizzle (chunk' = chunk ^ (j & 7)); hi = tf32 truncation,
