@@ -170,6 +170,12 @@ cr_status cr_primal(cr_ctx *ctx, double *y, double *xi, cr_step_stats *out);
  * recent cr_primal: y (HOST, all N), xi (HOST, this rank's rows x n). */
 cr_status cr_get_eta(cr_ctx *ctx, double *y, double *xi);
 
+/* The linear sums of Theta^k (which = 0) or Theta^{k-1} (which = 1) that Step 1 of the next
+ * iteration combines (Def. A1A2: A1^T theta = c - r, A2^T theta = r x - Theta X):
+ * r (HOST, this rank's rows), c (HOST, this rank's rows; column sums over ALL rows of all
+ * ranks), P (HOST, rows x n, Theta X).  Any pointer may be NULL.  Synchronizes. */
+cr_status cr_get_sums(cr_ctx *ctx, int32_t which, double *r, double *c, double *P);
+
 /* Step constant in use. */
 double cr_lipschitz(const cr_ctx *ctx);
 

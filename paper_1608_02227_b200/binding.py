@@ -23,7 +23,7 @@ KERNEL_NAME = {v: k for k, v in KERNEL.items()}
 # Symbols include/cr.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "cr_workspace_size", "cr_max_dim", "cr_nccl_get_unique_id", "cr_init", "cr_set_theta", "cr_get_theta",
-    "cr_get_theta_rows", "cr_dual_step", "cr_solve", "cr_primal", "cr_get_eta", "cr_lipschitz",
+    "cr_get_theta_rows", "cr_get_sums", "cr_dual_step", "cr_solve", "cr_primal", "cr_get_eta", "cr_lipschitz",
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
     "cr_last_error", "cr_status_string", "cr_destroy",
 )
@@ -79,6 +79,7 @@ def load(path: str = LIB_PATH):
         "cr_set_theta": (C.c_int, [vp, vp, vp, d, d]),
         "cr_get_theta": (C.c_int, [vp, vp, vp, C.POINTER(d), C.POINTER(d)]),
         "cr_get_theta_rows": (C.c_int, [vp, i32, i64, i64, vp]),
+        "cr_get_sums": (C.c_int, [vp, i32, vp, vp, vp]),
         "cr_dual_step": (C.c_int, [vp, C.POINTER(CrStepStats)]),
         "cr_solve": (C.c_int, [vp, i64, C.POINTER(CrStop), C.POINTER(CrReport)]),
         "cr_primal": (C.c_int, [vp, vp, vp, C.POINTER(CrStepStats)]),
@@ -248,6 +249,15 @@ class Solver:
         self._check(self.lib.cr_get_theta_rows(self.h, int(which), int(row0), int(nrows), out.ctypes.data),
                     "cr_get_theta_rows")
         return out
+
+    def get_sums(self, which: int = 0):
+        """(r, c, Theta X) of Theta^k (which=0) or Theta^{k-1} (which=1), this rank's rows."""
+        r = np.empty(self.rows)
+        c = np.empty(self.rows)
+        P = np.empty((self.rows, self.n))
+        self._check(self.lib.cr_get_sums(self.h, int(which), r.ctypes.data, c.ctypes.data, P.ctypes.data),
+                    "cr_get_sums")
+        return r, c, P
 
     def set_pass_timing(self, on: bool):
         self._check(self.lib.cr_set_pass_timing(self.h, 1 if on else 0), "cr_set_pass_timing")

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -38,10 +39,10 @@ struct Layout {
     size_t es = 4;
     // tensor-core pass
     bool tc = false;
-    int NK = 0, NP2 = 0, NPAN = 0, nCBtc = 0, nRBtc = 0;
+    int NK = 0, NP2 = 0, nCBtc = 0, nRBtc = 0;
     // byte offsets
     size_t th[2], XT, Xh, X64, ybar, r[2], c[2], P[2], y64, yv, bv, XiT, Xi64, a64, colpart, rowpart,
-        slot0, rb_ptr, rb_slots, cfull, ts, statpro, statres, xhi, xlo, XiR, slot0_tc, rb_ptr_tc, rb_slots_tc,
+        slot0, rb_ptr, rb_slots, cfull, ts, statpro, statres, g1h, g1l, g2h, g2l, XiR, slot0_tc, rb_ptr_tc, rb_slots_tc,
         total;
 };
 
@@ -96,12 +97,11 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     size_t rp_simt = (size_t)(L->nRB + kGMax) * kBM * L->NBP * 8;
     if (L->tc) {
         L->NK = (n + 7) / 8 * 8;
-        L->NP2 = (n + 1 + 15) / 16 * 16;
-        L->NPAN = (L->NP2 + 31) / 32;
+        L->NP2 = (n + 15) / 16 * 16;
         L->nCBtc = (int)((N + kTcBN - 1) / kTcBN);
         L->nRBtc = (int)(L->Rp / kTcBM);
         if (192 + L->NP2 + 2 * L->NK > 512) return false;     // TMEM columns
-        rp_simt = std::max(rp_simt, (size_t)(L->nRBtc + kGMax) * kTcBM * L->NP2 * 8);
+        rp_simt = std::max(rp_simt, (size_t)(L->nRBtc + kGMax) * kTcBM * (L->NP2 + 2) * 8);
     }
     L->rowpart = take(rp_simt);
     L->slot0 = take((size_t)kGMax * 4);
@@ -112,9 +112,10 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     L->statpro = take((size_t)(L->Rp / 256 + 2) * 8 * 8);
     L->statres = take((size_t)kStatBlocks * 8 * 8);
     if (L->tc) {
-        const size_t img = (size_t)L->nCBtc * L->NPAN * kTcBN * 128;
-        L->xhi = take(img);
-        L->xlo = take(img);
+        L->g1h = take((size_t)L->nCBtc * L->NK * 128);
+        L->g1l = take((size_t)L->nCBtc * L->NK * 128);
+        L->g2h = take((size_t)L->nCBtc * L->NP2 * 128);
+        L->g2l = take((size_t)L->nCBtc * L->NP2 * 128);
         L->XiR = take((size_t)L->Rp * L->NK * 4);
         L->slot0_tc = take((size_t)kGMax * 4);
         L->rb_ptr_tc = take((size_t)(L->nRBtc + 1) * 4);
@@ -277,7 +278,9 @@ ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance, bool tc = false) 
     q.Rp = Ly.Rp;
     q.ldT = Ly.ldT;
     q.n = Ly.n;
-    q.NBP = tc ? Ly.NP2 : Ly.NBP;
+    q.NBP = tc ? Ly.NP2 + 2 : Ly.NBP;
+    q.rcol0 = tc ? Ly.NP2 : Ly.n;
+    q.rcol1 = tc ? Ly.NP2 + 1 : -1;
     q.nRB = tc ? Ly.nRBtc : Ly.nRB;
     q.rbm = tc ? kTcBM : kBM;
     q.colpart = ctx->ws + Ly.colpart;
@@ -335,13 +338,14 @@ TcParams tc_params(cr_ctx *ctx) {
     p.nCB = Ly.nCBtc;
     p.NK = Ly.NK;
     p.NP2 = Ly.NP2;
-    p.NPAN = Ly.NPAN;
     p.stages = ctx->stages;
     p.window = ctx->window;
     p.stage_bytes = ctx->stage_bytes;
     p.smem_bytes = ctx->smem_tc;
-    p.xhi_img = ctx->at<float>(Ly.xhi);
-    p.xlo_img = ctx->at<float>(Ly.xlo);
+    p.g1_hi = ctx->at<float>(Ly.g1h);
+    p.g1_lo = ctx->at<float>(Ly.g1l);
+    p.g2_hi = ctx->at<float>(Ly.g2h);
+    p.g2_lo = ctx->at<float>(Ly.g2l);
     p.yv = ctx->at<float>(Ly.yv);
     p.XiR = ctx->at<float>(Ly.XiR);
     p.bv = ctx->at<float>(Ly.bv);
@@ -650,7 +654,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         // tcgen05 pass: one persistent CTA per SM (512 TMEM columns, ~200 KB smem each)
         ctx->T_tc = (int64_t)Ly.nRBtc * Ly.nCBtc;
         ctx->G_tc = (int)std::min<int64_t>({ctx->T_tc, (int64_t)nsm, (int64_t)kGMax});
-        ctx->stage_bytes = (uint32_t)((2 * kTcBM * kTcBN * 4 + 2 * Ly.NPAN * kTcBN * 128 + kTcBN * 4 + 1023) / 1024 * 1024);
+        ctx->stage_bytes = (uint32_t)((2 * kTcBM * kTcBN * 4 + 2 * Ly.NK * 128 + 2 * Ly.NP2 * 128 + kTcBN * 4 + 1023) / 1024 * 1024);
         const size_t fixed = tc_barrier_bytes() + 1024 + 64;
         const size_t budget = 227 * 1024;
         ctx->stages = (int)std::min<size_t>(kTcMaxStages, (budget - fixed) / ctx->stage_bytes);
@@ -663,8 +667,8 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
                            ctx->stream));
         IK(cudaMemcpyAsync(ctx->ws + Ly.rb_slots_tc, slotst.data(), slotst.size() * 4, cudaMemcpyHostToDevice,
                            ctx->stream));
-        IK(launch_tc_xhat(ctx->at<double>(Ly.X64), N, n, Ly.NPAN, Ly.nCBtc, ctx->at<float>(Ly.xhi),
-                          ctx->at<float>(Ly.xlo), ctx->stream));
+        IK(launch_tc_images(ctx->at<double>(Ly.X64), N, n, Ly.NK, Ly.NP2, Ly.nCBtc, ctx->at<float>(Ly.g1h),
+                            ctx->at<float>(Ly.g1l), ctx->at<float>(Ly.g2h), ctx->at<float>(Ly.g2l), ctx->stream));
         ctx->launches += 1;
         for (int b = 0; b < 2; ++b)
             if (!make_theta_tmap(&ctx->tm[b], ctx->th[b], Ly.Rp, Ly.ldT)) {
@@ -840,6 +844,21 @@ cr_status cr_get_eta(cr_ctx *ctx, double *y, double *xi) {
     if (y) CK(cudaMemcpyAsync(y, y64, (size_t)Ly.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
     if (xi && Ly.Ns > 0)
         CK(cudaMemcpyAsync(xi, ctx->ws + Ly.Xi64, (size_t)Ly.Ns * Ly.n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CR_OK;
+}
+
+cr_status cr_get_sums(cr_ctx *ctx, int32_t which, double *r, double *c, double *P) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    if (which != 0 && which != 1) return fail(ctx, CR_ERR_INVALID_ARG, "cr_get_sums: which");
+    const Layout &Ly = ctx->lay;
+    const int s = which == 0 ? ctx->s1 : 1 - ctx->s1;
+    if (Ly.Ns > 0) {
+        if (r) CK(cudaMemcpyAsync(r, ctx->r[s], (size_t)Ly.Ns * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (c) CK(cudaMemcpyAsync(c, ctx->c[s], (size_t)Ly.Ns * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (P) CK(cudaMemcpyAsync(P, ctx->P[s], (size_t)Ly.Ns * Ly.n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     return CR_OK;
 }

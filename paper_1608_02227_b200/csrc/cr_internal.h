@@ -79,6 +79,7 @@ cudaError_t launch_prologue(const SmallParams &p, int prec_fp64, cudaStream_t s,
 struct ReduceParams {
     int64_t N, Ns, Rp, ldT;
     int n, NBP, nRB, rbm;  // rbm: rows per row block of the pass that wrote the partials
+    int rcol0, rcol1;      // slot-row columns holding row-sum partials (rcol1 < 0: none)
     const void *colpart;   // [nRB][ldT]
     const double *rowpart; // [slots][kBM][NBP]
     const int *rb_ptr;     // [nRB + 1]
@@ -109,10 +110,11 @@ cudaError_t launch_stats_finalize(const double *pro, int nb_pro, const double *r
 
 struct TcParams {
     int64_t N, Ns, row0, ldT, T;
-    int G, nCB, NK, NP2, NPAN, stages, window;
+    int G, nCB, NK, NP2, stages, window;
     uint32_t stage_bytes;
     int smem_bytes;
-    const float *xhi_img, *xlo_img;  // [nCB][NPAN][32 x 128 B] swizzled X-hat tiles
+    const float *g1_hi, *g1_lo;      // [nCB][NK * 32]  X_J  tiles (K-major interleave), tf32 hi / lo
+    const float *g2_hi, *g2_lo;      // [nCB][NP2 * 32] X_J^T tiles (K-major interleave), tf32 hi / lo
     const float *yv;                 // y * scale, gathered
     const float *XiR;                // [Rp][NK] xi * scale
     const float *bv;                 // [Rp] (a - y) * scale
@@ -126,8 +128,8 @@ struct TcParams {
 cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const TcParams &p, cudaStream_t s);
 cudaError_t pass_tc_prepare(int smem_bytes);
 size_t tc_barrier_bytes();
-cudaError_t launch_tc_xhat(const double *X64, int64_t N, int n, int NPAN, int nCB, float *hi, float *lo,
-                           cudaStream_t s);
+cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,
+                             float *g2h, float *g2l, cudaStream_t s);
 
 // Column-major helpers for initialisation.
 cudaError_t launch_fill_inputs(const double *X64, int64_t N, int n, int NB, int NBP, int64_t ldT,

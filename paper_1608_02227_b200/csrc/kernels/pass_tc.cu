@@ -3,18 +3,23 @@
 // Same mathematics as pass_simt.cu (Steps 2 and 4 of P-APG Fig. 2, plus the
 // sums Step 1 of the next iteration needs), organised like a flash-attention forward:
 //
-//   GEMM1  S'  = Xi'_I X_J^T          M=128 rows i, N=32 cols j, K=n   (A = Xi' in TMEM)
-//   epilogue   Theta^k = (Theta^{k-1} + beta (Theta^{k-1} - Theta^{k-2}) + S' - y'_j - b'_i)_+
-//   GEMM2  P_I += Theta^k_IJ [X | 1]_J M=128 rows i, N=n+1, K=32 cols j (A = Theta^k in TMEM)
-//   column sums of Theta^k on CUDA cores (warp butterfly), per (row block, column tile)
+//   GEMM1  S' = Xi'_I X_J^T        M=128 rows i, N=32 cols j, K=n  (A = Xi' in TMEM, B = X_J smem)
+//   epilogue  Theta^k = (Theta^{k-1} + beta (Theta^{k-1} - Theta^{k-2}) + S' - y'_j - b'_i)_+
+//   GEMM2  P_I += Theta^k_IJ X_J   M=128 rows i, N=n,  K=32 cols j  (A = Theta^k in TMEM, B = X_J^T smem)
+//   row / column sums of Theta^k on CUDA cores (thread row sums, warp-butterfly column sums)
 //
 // Both GEMMs use 3xTF32 (hi*hi + hi*lo + lo*hi, hi = fp32 with the low 13 mantissa bits
-// cleared) so products carry ~fp32 accuracy.  Theta^{k-1}, Theta^{k-2} tiles arrive by TMA
-// (128B-swizzled 128x32 boxes), Theta^k leaves by TMA store from the same smem slot; the
-// row accumulator lives in TMEM and is flushed to fp64 (global, per CTA run slot) every
-// `window` tiles.  Warp roles: 0 = TMA producer, 1 = MMA issuer (+ TMEM owner),
-// 2..5 = epilogue (one TMEM lane quarter each).  Persistent: CTA g owns tiles
-// [g T / G, (g+1) T / G) of the row-major (row block, column tile) order, like the SIMT pass.
+// cleared, lo = remainder) so products carry ~fp32 accuracy.  Both B operands are K-major
+// no-swizzle ("interleave") tiles prepared once at init: X_J as [j][k] and X_J^T as [d][j]
+// core matrices (8 rows x 16 B), so each per-tile image is exactly 32 n fp32.  (MN-major
+// tf32 operands would need the SW128_32B layout; two K-major images avoid it.)
+// Theta^{k-1}, Theta^{k-2} tiles arrive by TMA (128B-swizzled 128x32 boxes); Theta^k leaves by
+// TMA store from the same smem slot.  The Theta X accumulator lives in TMEM and is flushed to
+// fp64 (global, per CTA run slot) every `window` tiles.
+// Warp roles: 0 = TMA producer, 1 = MMA issuer (+ TMEM owner), 2 = TMA storer, 3 = spare,
+// 4..7 / 8..11 = two epilogue warpgroups that take alternate tiles (ping-pong).
+// Persistent: CTA g owns tiles [g T / G, (g+1) T / G) of the row-major (row block, column
+// tile) order, like the SIMT pass.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -28,9 +33,8 @@ using namespace sm100;
 
 constexpr int TBM = kTcBM;      // 128 rows per tile (TMEM lanes)
 constexpr int TBN = kTcBN;      // 32 columns per tile
-constexpr int NTHR = 384;       // 12 warps: producer, MMA, storer, spare, 2 x 4 epilogue
+constexpr int NTHR = 384;       // 12 warps
 constexpr uint32_t TILE_BYTES = TBM * TBN * 4;     // 16 KB
-constexpr uint32_t PANEL_BYTES = TBN * 128;        // 4 KB: 32 rows j x 32 fp32 (128 B)
 
 struct __align__(8) TcBarriers {
     uint64_t full[kTcMaxStages], empty[kTcMaxStages];
@@ -39,7 +43,12 @@ struct __align__(8) TcBarriers {
     uint32_t tmem_base;
 };
 
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// tf32 "hi" part of x: round to the nearest 10-bit-mantissa value (ties away), low 13 bits
+// cleared, so the remainder x - hi (exact in fp32) is at most 2^-12 |x| and the product error
+// of the 3xTF32 split is ~2^-23 relative.  The MMA reads hi exactly (its low bits are zero).
+__device__ __forceinline__ float tf32_hi(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 
 // butterfly step: lane keeps the half of v selected by its bit, adds the partner's other half
 template <int H>
@@ -67,11 +76,13 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     if (t0 >= t1) return;
     const int64_t U = t1 - t0;
     const int nCB = p.nCB;
-    const int NK = p.NK, NP2 = p.NP2, NPAN = p.NPAN;
-    const uint32_t xpan_bytes = (uint32_t)NPAN * PANEL_BYTES;
+    const int NK = p.NK, NP2 = p.NP2, W = p.NP2 + 2;
+    // stage image: [B1 16K][B2 16K][X hi][X lo][X^T hi][X^T lo][y' 128 B]
+    const uint32_t g1_bytes = (uint32_t)NK * 128, g2_bytes = (uint32_t)NP2 * 128;
+    const uint32_t o_g1 = 2 * TILE_BYTES, o_g2 = o_g1 + 2 * g1_bytes, o_y = o_g2 + 2 * g2_bytes;
+    const uint32_t lbo2 = (uint32_t)NP2 * 16;          // X^T image: K-chunk (4 j) stride
 
     auto stage_ptr = [&](int s) { return smem + (size_t)s * stage_bytes; };
-    // stage image: [B1 16K][B2 16K][Xhi NPAN*4K][Xlo NPAN*4K][y' 128B]
     auto run_start = [&](int64_t t) { return t == t0 || (t % nCB) == 0; };
     auto run_end = [&](int64_t t) { return t + 1 == t1 || ((t + 1) % nCB) == 0; };
     auto flush_after = [&](int64_t t) {
@@ -79,6 +90,8 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         const int64_t rs = (t / nCB) * nCB > t0 ? (t / nCB) * nCB : t0;
         return ((t - rs + 1) % p.window) == 0;
     };
+    const int slot0 = p.cta_slot0[blockIdx.x];
+    auto slot_of = [&](int64_t t) { return slot0 + (int)(t / nCB - t0 / nCB); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 2); }
@@ -98,7 +111,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bar->tmem_base;
-    // TMEM column map: D1[2] 0..63, Theta^k A operand [2] x (hi 32, lo 32) 64..191, D2, Xi' (hi, lo)
+    // TMEM columns: D1[2] 0..63 | Theta^k A operand [2] x (hi 32, lo 32) 64..191 | D2 (NP2) | Xi' hi, lo
     const uint32_t c_d1 = 0, c_at = 64, c_d2 = 192, c_xi = 192 + (uint32_t)NP2;
 
     if (warp == 0) {
@@ -111,20 +124,21 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 mbar_wait(&bar->empty[s], (uint32_t)(((u / S) & 1) ^ 1));
                 const int64_t rb = t / nCB, cb = t % nCB;
                 uint8_t *st = stage_ptr(s);
-                mbar_arrive_expect_tx(&bar->full[s], 2 * TILE_BYTES + 2 * xpan_bytes + TBN * 4);
+                mbar_arrive_expect_tx(&bar->full[s], 2 * TILE_BYTES + 2 * g1_bytes + 2 * g2_bytes + TBN * 4);
                 tma_load_2d(st, &tmB1, (int)(cb * TBN), (int)(rb * TBM), &bar->full[s], pol_stream);
                 tma_load_2d(st + TILE_BYTES, &tmB2, (int)(cb * TBN), (int)(rb * TBM), &bar->full[s], pol_stream);
-                bulk_load(st + 2 * TILE_BYTES, p.xhi_img + (size_t)cb * xpan_bytes / 4, xpan_bytes, &bar->full[s], pol_keep);
-                bulk_load(st + 2 * TILE_BYTES + xpan_bytes, p.xlo_img + (size_t)cb * xpan_bytes / 4, xpan_bytes,
-                          &bar->full[s], pol_keep);
-                bulk_load(st + 2 * TILE_BYTES + 2 * xpan_bytes, p.yv + cb * TBN, TBN * 4, &bar->full[s], pol_keep);
+                bulk_load(st + o_g1, p.g1_hi + (size_t)cb * NK * 32, g1_bytes, &bar->full[s], pol_keep);
+                bulk_load(st + o_g1 + g1_bytes, p.g1_lo + (size_t)cb * NK * 32, g1_bytes, &bar->full[s], pol_keep);
+                bulk_load(st + o_g2, p.g2_hi + (size_t)cb * NP2 * 32, g2_bytes, &bar->full[s], pol_keep);
+                bulk_load(st + o_g2 + g2_bytes, p.g2_lo + (size_t)cb * NP2 * 32, g2_bytes, &bar->full[s], pol_keep);
+                bulk_load(st + o_y, p.yv + cb * TBN, TBN * 4, &bar->full[s], pol_keep);
             }
         }
     } else if (warp == 1) {
         // ============================================================ MMA issuer
         if (lane == 0) {
-            const uint32_t id1 = idesc_tf32(TBM, TBN, 0, 0);   // A K-major (TMEM), B K-major (X tile, k inner)
-            const uint32_t id2 = idesc_tf32(TBM, NP2, 0, 1);   // A K-major (TMEM), B MN-major (X tile, d inner)
+            const uint32_t id1 = idesc_tf32(TBM, TBN, 0, 0);   // A K-major (TMEM), B K-major
+            const uint32_t id2 = idesc_tf32(TBM, NP2, 0, 0);
             int64_t run = 0, flushes = 0;
             bool window_start = true;
             auto gemm1 = [&](int64_t u) {
@@ -132,15 +146,15 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 mbar_wait(&bar->full[s], (uint32_t)((u / S) & 1));
                 mbar_wait(&bar->d1_empty[b], (uint32_t)(((u >> 1) & 1) ^ 1));
                 tc_fence_after();
-                const uint8_t *xh = stage_ptr(s) + 2 * TILE_BYTES, *xl = xh + xpan_bytes;
+                const uint8_t *xh = stage_ptr(s) + o_g1, *xl = xh + g1_bytes;
                 const uint32_t d = tmem + c_d1 + (uint32_t)b * TBN;
                 uint32_t acc = 0;
                 for (int pass = 0; pass < 3; ++pass) {
                     const uint8_t *xb = pass == 1 ? xl : xh;
                     const uint32_t a_col = c_xi + (pass == 2 ? (uint32_t)NK : 0u);
                     for (int kk = 0; kk < NK / 8; ++kk) {
-                        // K-major SW128 B: panel kk/4, 32-byte step kk%4 inside the 128-B row
-                        const uint64_t bd = smem_desc(xb + (kk >> 2) * PANEL_BYTES + (kk & 3) * 32, 16, 1024);
+                        // K-major interleave: 4-k chunks LBO = 512 B apart, 8-row j groups SBO = 128 B
+                        const uint64_t bd = smem_desc(xb + kk * 1024, 512, 128, 0);
                         mma_tf32_ts(d, tmem + a_col + (uint32_t)kk * 8, bd, id1, acc);
                         acc = 1;
                     }
@@ -158,15 +172,14 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 mbar_wait(&bar->at_full[a], (uint32_t)((u >> 1) & 1));
                 if (window_start && flushes > 0) mbar_wait(&bar->d2_empty, (uint32_t)((flushes - 1) & 1));
                 tc_fence_after();
-                const uint8_t *xh = stage_ptr(s) + 2 * TILE_BYTES, *xl = xh + xpan_bytes;
+                const uint8_t *xh = stage_ptr(s) + o_g2, *xl = xh + g2_bytes;
                 uint32_t acc = window_start ? 0u : 1u;
                 for (int pass = 0; pass < 3; ++pass) {
                     const uint8_t *xb = pass == 1 ? xl : xh;
                     const uint32_t a_col = c_at + (uint32_t)a * 64 + (pass == 2 ? 32u : 0u);
                     for (int jj = 0; jj < TBN / 8; ++jj) {
-                        // MN-major SW128 B: rows j = 8 jj .. 8 jj + 7 (one swizzle atom along K),
-                        // 32-wide d panels LBO = PANEL_BYTES apart
-                        const uint64_t bd = smem_desc(xb + jj * 1024, PANEL_BYTES, 1024);
+                        // X^T image, K-major interleave: 4-j chunks lbo2 apart, 8-row d groups 128 B
+                        const uint64_t bd = smem_desc(xb + jj * 2 * lbo2, lbo2, 128, 0);
                         mma_tf32_ts(tmem + c_d2, tmem + a_col + (uint32_t)jj * 8, bd, id2, acc);
                         acc = 1;
                     }
@@ -211,9 +224,8 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const float beta = (float)((p.ts[0] - 1.0) / p.ts[1]);   // beta_{k-1} = (t_{k-1}-1)/t_k
         int64_t flushes = 0;
-        int flush_in_run = 0;
-        int slot = p.cta_slot0[blockIdx.x];
-        float bi = 0.f;
+        int last_flush_slot = -1;
+        double rrun = 0.0;                            // this warpgroup's row sum over the current run
         float *my_colS = colS + wg * 2 * 4 * 32;
 
         auto load_xi = [&](int64_t rb) {
@@ -236,12 +248,15 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->xi_full);
         };
-        // flush of the row accumulator after tile tf (done by warpgroup 0 only, in tile order,
-        // so every slot sees its window partials added in a fixed order)
+        // Theta X flush after tile tf (warpgroup 0 only, in tile order: each slot receives its
+        // window partials from one thread in a fixed order -> deterministic)
         auto flush = [&](int64_t tf) {
             mbar_wait(&bar->d2_full, (uint32_t)(flushes & 1));
             tc_fence_after();
-            double *dst = p.rowpart + ((int64_t)slot * TBM + r) * NP2;
+            const int sl = slot_of(tf);
+            const bool first = sl != last_flush_slot;
+            last_flush_slot = sl;
+            double *dst = p.rowpart + ((int64_t)sl * TBM + r) * W;
             for (int d0 = 0; d0 < NP2; d0 += 16) {
                 uint32_t a[16];
                 tmem_ld16(tmem + lane_off + c_d2 + (uint32_t)d0, a);
@@ -249,16 +264,14 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     const double v = (double)__uint_as_float(a[e]);
-                    if (flush_in_run == 0) dst[d0 + e] = v;
-                    else dst[d0 + e] += v;                 // same thread, in order: deterministic
+                    if (first) dst[d0 + e] = v;
+                    else dst[d0 + e] += v;
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->d2_empty);
             ++flushes;
-            ++flush_in_run;
-            if (run_end(tf)) { ++slot; flush_in_run = 0; }
         };
 
         if (wg == 0) load_xi(t0 / nCB);
@@ -272,11 +285,11 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 load_xi(rb);
             }
             const int64_t lr = rb * TBM + r, gr = p.row0 + lr;
-            bi = p.bv[lr];
+            const float bi = p.bv[lr];
             // ---- Theta tiles landed? (B1, B2, y' of this tile)
             mbar_wait(&bar->full[s], (uint32_t)((u / S) & 1));
             uint8_t *st = stage_ptr(s);
-            const float *yt = reinterpret_cast<const float *>(st + 2 * TILE_BYTES + 2 * xpan_bytes);
+            const float *yt = reinterpret_cast<const float *>(st + o_y);
             uint8_t *rowB1 = st + r * 128, *rowB2 = st + TILE_BYTES + r * 128;
             // ---- S' = Xi' X^T from TMEM
             mbar_wait(&bar->d1_full[b], (uint32_t)((u >> 1) & 1));
@@ -348,6 +361,17 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->st_full[wg]);
+            // ---- row sum (this thread's row, pairwise in fp32, fp64 across tiles)
+            {
+                float s16[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) s16[c] = th[c] + th[c + 16];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) s16[c] += s16[c + 8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) s16[c] += s16[c + 4];
+                rrun += (double)((s16[0] + s16[2]) + (s16[1] + s16[3]));
+            }
             // ---- column sums over this warp's 32 rows (butterfly transpose-reduce), then over warps
             {
                 float v16[16], v8[8], v4[4], v2[2], v1[1];
@@ -364,7 +388,12 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 const float c4 = (cs[lane] + cs[32 + lane]) + (cs[64 + lane] + cs[96 + lane]);
                 p.colpart[rb * p.ldT + cb * TBN + lane] = c4;
             }
-            // ---- row accumulator flushes (warpgroup 0 handles those after tiles u and u+1)
+            // ---- this warpgroup's last tile of the run: its row-sum partial into the slot
+            if (u + 2 >= U || (t + 2) / nCB != rb) {
+                p.rowpart[((int64_t)slot_of(t) * TBM + r) * W + NP2 + wg] = rrun;
+                rrun = 0.0;
+            }
+            // ---- Theta X flushes (warpgroup 0 handles those after tiles u and u+1)
             if (wg == 0) {
                 if (flush_after(t)) flush(t);
                 if (u + 1 < U && flush_after(t + 1)) flush(t + 1);
@@ -374,6 +403,31 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// Per-32-column-tile B-operand images (K-major, no swizzle: 8-row x 16-B core matrices):
+//   g1 = X_J   [j][k]: byte ((k/4) * 4 + j/8) * 128 + (j%8) * 16 + (k%4) * 4,      NK * 128 B / tile
+//   g2 = X_J^T [d][j]: byte ((j/4) * NP2/8 + d/8) * 128 + (d%8) * 16 + (j%4) * 4, NP2 * 128 B / tile
+// hi = tf32 truncation, lo = remainder; k >= n, d >= n and j >= N hold 0.
+__global__ void tc_images_kernel(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h,
+                                 float *g1l, float *g2h, float *g2l) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)nCB * TBN * NP2;
+    if (e >= total) return;
+    const int d = (int)(e % NP2);
+    const int64_t j = e / NP2;
+    const int64_t cb = j / TBN;
+    const int jj = (int)(j % TBN);
+    const float x = (j < N && d < n) ? (float)X64[j * n + d] : 0.f;
+    const float h = tf32_hi(x), l = x - h;
+    if (d < NK) {
+        const int64_t o = cb * (int64_t)NK * 32 + ((d / 4) * 4 + jj / 8) * 32 + (jj % 8) * 4 + (d % 4);
+        g1h[o] = h;
+        g1l[o] = l;
+    }
+    const int64_t o2 = cb * (int64_t)NP2 * 32 + ((jj / 4) * (NP2 / 8) + d / 8) * 32 + (d % 8) * 4 + (jj % 4);
+    g2h[o2] = h;
+    g2l[o2] = l;
 }
 
 }  // namespace
@@ -389,31 +443,10 @@ cudaError_t pass_tc_prepare(int smem_bytes) {
 
 size_t tc_barrier_bytes() { return sizeof(TcBarriers) + 8 + 2 * 2 * 4 * 32 * 4; }
 
-// X-hat images for the TC pass: per 32-column tile, NPAN panels of [32 rows j][32 d] fp32,
-// 128-B rows with the SW128 chunk swizzle (chunk' = chunk ^ (j & 7)); hi = tf32 truncation,
-// lo = remainder; column d = n holds 1 (row sums), d > n and j >= N hold 0.
-__global__ void tc_xhat_kernel(const double *X64, int64_t N, int n, int NPAN, int nCB, float *hi, float *lo) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;     // one element (j, d)
-    const int64_t total = (int64_t)nCB * TBN * NPAN * 32;
-    if (e >= total) return;
-    const int d = (int)(e % (NPAN * 32));
-    const int64_t j = e / (NPAN * 32);
-    const int64_t cb = j / TBN;
-    const int jj = (int)(j % TBN);
-    float x = 0.f;
-    if (j < N) x = d < n ? (float)X64[j * n + d] : (d == n ? 1.f : 0.f);
-    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-    const int pan = d / 32, dd = d % 32;
-    const int64_t byte = cb * (int64_t)NPAN * PANEL_BYTES + pan * PANEL_BYTES + jj * 128 +
-                         (((dd >> 2) ^ (jj & 7)) << 4) + (dd & 3) * 4;
-    hi[byte / 4] = h;
-    lo[byte / 4] = x - h;
-}
-
-cudaError_t launch_tc_xhat(const double *X64, int64_t N, int n, int NPAN, int nCB, float *hi, float *lo,
-                           cudaStream_t s) {
-    const int64_t total = (int64_t)nCB * TBN * NPAN * 32;
-    tc_xhat_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(X64, N, n, NPAN, nCB, hi, lo);
+cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,
+                             float *g2h, float *g2l, cudaStream_t s) {
+    const int64_t total = (int64_t)nCB * TBN * NP2;
+    tc_images_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(X64, N, n, NK, NP2, nCB, g1h, g1l, g2h, g2l);
     return cudaGetLastError();
 }
 

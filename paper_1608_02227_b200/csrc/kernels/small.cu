@@ -72,8 +72,21 @@ __global__ void reduce_kernel(const ReduceParams p) {
         const int d = (int)(g % (p.n + 1));
         const int rb = (int)(i / p.rbm), ii = (int)(i % p.rbm);
         double s = 0.0;
-        for (int e = p.rb_ptr[rb]; e < p.rb_ptr[rb + 1]; ++e)
-            s += p.rowpart[((int64_t)p.rb_slots[e] * p.rbm + ii) * p.NBP + d];
+        // fixed slot order; each consumed partial is reset to 0 (passes may rely on zeroed slots)
+        for (int e = p.rb_ptr[rb]; e < p.rb_ptr[rb + 1]; ++e) {
+            double *row = const_cast<double *>(p.rowpart) + ((int64_t)p.rb_slots[e] * p.rbm + ii) * p.NBP;
+            if (d < p.n) {
+                s += row[d];
+                row[d] = 0.0;
+            } else {
+                s += row[p.rcol0];
+                row[p.rcol0] = 0.0;
+                if (p.rcol1 >= 0) {
+                    s += row[p.rcol1];
+                    row[p.rcol1] = 0.0;
+                }
+            }
+        }
         if (d < p.n) p.P[i * p.n + d] = s;
         else p.r[i] = s;
     } else if (g < nrow + p.N) {

@@ -240,3 +240,23 @@ def test_full_size_C4_sampled_step(crp):
     want = oracle.project_rows(X, yo, xio, L, rows, Tt[rows])
     got = np.concatenate([s.get_theta_rows(0, int(r), 1) for r in rows])
     assert rel(got, want) <= 1e-5
+
+
+@pytest.mark.parametrize("kernel", ["simt", "tc"])
+@pytest.mark.parametrize("N,n", [(128, 20), (300, 20), (1000, 40), (257, 80), (2100, 17)])
+def test_pass_sums_match_returned_theta(crp, kernel, N, n):
+    """The row sums, column sums and Theta X each fused pass accumulates (the inputs of the next
+    Step 1, Def. A1A2) equal those of the Theta^k it stored, summed in fp64."""
+    X, ybar = crdata.random_problem(N, n, seed=N + n, fp32=True)
+    s = crp.Solver(X, ybar, 1e-3, kernel=kernel)
+    # r, c: fp32 adds of the stored values (fp64 across tiles) -> ~1e-7.  Theta X on the tensor
+    # cores: 3xTF32 products carry ~3 * 2^-23 relative error each, and sum_j Theta_ij x_j cancels
+    # (x of both signs), so its Frobenius-relative error is bounded by 1e-5; CUDA cores: 1e-6.
+    tol_P = 1e-5 if kernel == "tc" else 1e-6
+    for it in range(3):
+        s.step()
+        T = s.get_theta()[0]
+        r, c, P = s.get_sums(0)
+        assert rel(r, T.sum(1)) <= 1e-6, (it, rel(r, T.sum(1)))
+        assert rel(c, T.sum(0)) <= 1e-6, (it, rel(c, T.sum(0)))
+        assert rel(P, T @ X) <= tol_P, (it, rel(P, T @ X))
