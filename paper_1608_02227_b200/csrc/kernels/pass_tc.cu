@@ -62,6 +62,12 @@ __device__ __forceinline__ void bfly(const float *v, float *o, int lane) {
     }
 }
 
+// Position of tile u within a CTA's contiguous tile range: row block, column tile, and the
+// stage slot / phase parity of the smem ring (all maintained incrementally: no divisions).
+struct Cursor {
+    int u, rb, cb, s, ph;
+};
+
 __global__ void __launch_bounds__(NTHR, 1)
 pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2, const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -72,26 +78,35 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     float *colS = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + sizeof(TcBarriers) + 8);  // [2 wg][2][4][32]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t t0 = (int64_t)blockIdx.x * p.T / p.G, t1 = (int64_t)(blockIdx.x + 1) * p.T / p.G;
+    const int t0 = (int)((int64_t)blockIdx.x * p.T / p.G), t1 = (int)((int64_t)(blockIdx.x + 1) * p.T / p.G);
     if (t0 >= t1) return;
-    const int64_t U = t1 - t0;
+    const int U = t1 - t0;
     const int nCB = p.nCB;
     const int NK = p.NK, NP2 = p.NP2, W = p.NP2 + 2;
+    const int wmask = p.window - 1;                    // flush window (power of two)
     // stage image: [B1 16K][B2 16K][X hi][X lo][X^T hi][X^T lo][y' 128 B]
     const uint32_t g1_bytes = (uint32_t)NK * 128, g2_bytes = (uint32_t)NP2 * 128;
     const uint32_t o_g1 = 2 * TILE_BYTES, o_g2 = o_g1 + 2 * g1_bytes, o_y = o_g2 + 2 * g2_bytes;
     const uint32_t lbo2 = (uint32_t)NP2 * 16;          // X^T image: K-chunk (4 j) stride
+    const int rb0 = t0 / nCB, cb0 = t0 - rb0 * nCB;
+    const int slot0 = p.cta_slot0[blockIdx.x];
 
     auto stage_ptr = [&](int s) { return smem + (size_t)s * stage_bytes; };
-    auto run_start = [&](int64_t t) { return t == t0 || (t % nCB) == 0; };
-    auto run_end = [&](int64_t t) { return t + 1 == t1 || ((t + 1) % nCB) == 0; };
-    auto flush_after = [&](int64_t t) {
-        if (run_end(t)) return true;
-        const int64_t rs = (t / nCB) * nCB > t0 ? (t / nCB) * nCB : t0;
-        return ((t - rs + 1) % p.window) == 0;
+    auto adv = [&](Cursor &c, int k) {
+        c.u += k;
+        c.cb += k;
+        while (c.cb >= nCB) { c.cb -= nCB; ++c.rb; }
+        c.s += k;
+        while (c.s >= S) { c.s -= S; c.ph ^= 1; }
     };
-    const int slot0 = p.cta_slot0[blockIdx.x];
-    auto slot_of = [&](int64_t t) { return slot0 + (int)(t / nCB - t0 / nCB); };
+    auto start = [&]() { return Cursor{0, rb0, cb0, 0, 0}; };
+    auto run_start = [&](const Cursor &c) { return c.u == 0 || c.cb == 0; };
+    auto run_end = [&](const Cursor &c) { return c.u + 1 == U || c.cb + 1 == nCB; };
+    auto flush_after = [&](const Cursor &c) {
+        if (run_end(c)) return true;
+        const int rs = c.rb * nCB > t0 ? c.rb * nCB : t0;          // first tile of this run
+        return ((t0 + c.u - rs + 1) & wmask) == 0;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 2); }
@@ -118,20 +133,18 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         // ============================================================ TMA producer
         if (lane == 0) {
             const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-            for (int64_t u = 0; u < U; ++u) {
-                const int64_t t = t0 + u;
-                const int s = (int)(u % S);
-                mbar_wait(&bar->empty[s], (uint32_t)(((u / S) & 1) ^ 1));
-                const int64_t rb = t / nCB, cb = t % nCB;
-                uint8_t *st = stage_ptr(s);
-                mbar_arrive_expect_tx(&bar->full[s], 2 * TILE_BYTES + 2 * g1_bytes + 2 * g2_bytes + TBN * 4);
-                tma_load_2d(st, &tmB1, (int)(cb * TBN), (int)(rb * TBM), &bar->full[s], pol_stream);
-                tma_load_2d(st + TILE_BYTES, &tmB2, (int)(cb * TBN), (int)(rb * TBM), &bar->full[s], pol_stream);
-                bulk_load(st + o_g1, p.g1_hi + (size_t)cb * NK * 32, g1_bytes, &bar->full[s], pol_keep);
-                bulk_load(st + o_g1 + g1_bytes, p.g1_lo + (size_t)cb * NK * 32, g1_bytes, &bar->full[s], pol_keep);
-                bulk_load(st + o_g2, p.g2_hi + (size_t)cb * NP2 * 32, g2_bytes, &bar->full[s], pol_keep);
-                bulk_load(st + o_g2 + g2_bytes, p.g2_lo + (size_t)cb * NP2 * 32, g2_bytes, &bar->full[s], pol_keep);
-                bulk_load(st + o_y, p.yv + cb * TBN, TBN * 4, &bar->full[s], pol_keep);
+            for (Cursor c = start(); c.u < U; adv(c, 1)) {
+                mbar_wait(&bar->empty[c.s], (uint32_t)(c.ph ^ 1));
+                uint8_t *st = stage_ptr(c.s);
+                uint64_t *fb = &bar->full[c.s];
+                mbar_arrive_expect_tx(fb, 2 * TILE_BYTES + 2 * g1_bytes + 2 * g2_bytes + TBN * 4);
+                tma_load_2d(st, &tmB1, c.cb * TBN, c.rb * TBM, fb, pol_stream);
+                tma_load_2d(st + TILE_BYTES, &tmB2, c.cb * TBN, c.rb * TBM, fb, pol_stream);
+                bulk_load(st + o_g1, p.g1_hi + (size_t)c.cb * NK * 32, g1_bytes, fb, pol_keep);
+                bulk_load(st + o_g1 + g1_bytes, p.g1_lo + (size_t)c.cb * NK * 32, g1_bytes, fb, pol_keep);
+                bulk_load(st + o_g2, p.g2_hi + (size_t)c.cb * NP2 * 32, g2_bytes, fb, pol_keep);
+                bulk_load(st + o_g2 + g2_bytes, p.g2_lo + (size_t)c.cb * NP2 * 32, g2_bytes, fb, pol_keep);
+                bulk_load(st + o_y, p.yv + c.cb * TBN, TBN * 4, fb, pol_keep);
             }
         }
     } else if (warp == 1) {
@@ -139,64 +152,67 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         if (lane == 0) {
             const uint32_t id1 = idesc_tf32(TBM, TBN, 0, 0);   // A K-major (TMEM), B K-major
             const uint32_t id2 = idesc_tf32(TBM, NP2, 0, 0);
-            int64_t run = 0, flushes = 0;
+            int run = 0, flushes = 0;
             bool window_start = true;
-            auto gemm1 = [&](int64_t u) {
-                const int s = (int)(u % S), b = (int)(u & 1);
-                mbar_wait(&bar->full[s], (uint32_t)((u / S) & 1));
-                mbar_wait(&bar->d1_empty[b], (uint32_t)(((u >> 1) & 1) ^ 1));
+            auto gemm1 = [&](const Cursor &c) {
+                const int b = c.u & 1;
+                mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
+                mbar_wait(&bar->d1_empty[b], (uint32_t)(((c.u >> 1) & 1) ^ 1));
                 tc_fence_after();
-                const uint8_t *xh = stage_ptr(s) + o_g1, *xl = xh + g1_bytes;
+                const uint8_t *xh = stage_ptr(c.s) + o_g1;
                 const uint32_t d = tmem + c_d1 + (uint32_t)b * TBN;
-                uint32_t acc = 0;
+#pragma unroll 1
                 for (int pass = 0; pass < 3; ++pass) {
-                    const uint8_t *xb = pass == 1 ? xl : xh;
+                    const uint8_t *xb = pass == 1 ? xh + g1_bytes : xh;
                     const uint32_t a_col = c_xi + (pass == 2 ? (uint32_t)NK : 0u);
+#pragma unroll 1
                     for (int kk = 0; kk < NK / 8; ++kk) {
                         // K-major interleave: 4-k chunks LBO = 512 B apart, 8-row j groups SBO = 128 B
                         const uint64_t bd = smem_desc(xb + kk * 1024, 512, 128, 0);
-                        mma_tf32_ts(d, tmem + a_col + (uint32_t)kk * 8, bd, id1, acc);
-                        acc = 1;
+                        mma_tf32_ts(d, tmem + a_col + (uint32_t)kk * 8, bd, id1, (pass | kk) != 0);
                     }
                 }
                 mma_commit(&bar->d1_full[b]);
             };
             mbar_wait(&bar->xi_full, 0);
             tc_fence_after();
-            gemm1(0);
-            for (int64_t u = 0; u < U; ++u) {
-                const int64_t t = t0 + u;
-                const bool next_same_run = (u + 1 < U) && !run_start(t + 1);
-                if (next_same_run) gemm1(u + 1);
-                const int s = (int)(u % S), a = (int)(u & 1);
-                mbar_wait(&bar->at_full[a], (uint32_t)((u >> 1) & 1));
+            Cursor c = start();
+            gemm1(c);
+            for (; c.u < U; adv(c, 1)) {
+                Cursor n = c;
+                adv(n, 1);
+                const bool next_same_run = (n.u < U) && n.cb != 0;
+                if (next_same_run) gemm1(n);
+                const int a = c.u & 1;
+                mbar_wait(&bar->at_full[a], (uint32_t)((c.u >> 1) & 1));
                 if (window_start && flushes > 0) mbar_wait(&bar->d2_empty, (uint32_t)((flushes - 1) & 1));
                 tc_fence_after();
-                const uint8_t *xh = stage_ptr(s) + o_g2, *xl = xh + g2_bytes;
-                uint32_t acc = window_start ? 0u : 1u;
+                const uint8_t *xh = stage_ptr(c.s) + o_g2;
+#pragma unroll 1
                 for (int pass = 0; pass < 3; ++pass) {
-                    const uint8_t *xb = pass == 1 ? xl : xh;
+                    const uint8_t *xb = pass == 1 ? xh + g2_bytes : xh;
                     const uint32_t a_col = c_at + (uint32_t)a * 64 + (pass == 2 ? 32u : 0u);
+#pragma unroll 1
                     for (int jj = 0; jj < TBN / 8; ++jj) {
                         // X^T image, K-major interleave: 4-j chunks lbo2 apart, 8-row d groups 128 B
                         const uint64_t bd = smem_desc(xb + jj * 2 * lbo2, lbo2, 128, 0);
-                        mma_tf32_ts(tmem + c_d2, tmem + a_col + (uint32_t)jj * 8, bd, id2, acc);
-                        acc = 1;
+                        mma_tf32_ts(tmem + c_d2, tmem + a_col + (uint32_t)jj * 8, bd, id2,
+                                    !(window_start && pass == 0 && jj == 0));
                     }
                 }
                 mma_commit(&bar->at_empty[a]);
-                mma_commit(&bar->empty[s]);
+                mma_commit(&bar->empty[c.s]);
                 window_start = false;
-                if (flush_after(t)) {
+                if (flush_after(c)) {
                     mma_commit(&bar->d2_full);
                     ++flushes;
                     window_start = true;
                 }
-                if (u + 1 < U && !next_same_run) {
+                if (n.u < U && !next_same_run) {
                     ++run;
                     mbar_wait(&bar->xi_full, (uint32_t)(run & 1));
                     tc_fence_after();
-                    gemm1(u + 1);
+                    gemm1(n);
                 }
             }
         }
@@ -204,15 +220,12 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         // ============================================================ TMA storer
         if (lane == 0) {
             const uint64_t pol_stream = policy_evict_first();
-            for (int64_t u = 0; u < U; ++u) {
-                const int64_t t = t0 + u;
-                const int s = (int)(u % S), w = (int)(u & 1);
-                mbar_wait(&bar->st_full[w], (uint32_t)((u >> 1) & 1));
-                tma_store_2d(&tmB2, (int)((t % nCB) * TBN), (int)((t / nCB) * TBM), stage_ptr(s) + TILE_BYTES,
-                             pol_stream);
+            for (Cursor c = start(); c.u < U; adv(c, 1)) {
+                mbar_wait(&bar->st_full[c.u & 1], (uint32_t)((c.u >> 1) & 1));
+                tma_store_2d(&tmB2, c.cb * TBN, c.rb * TBM, stage_ptr(c.s) + TILE_BYTES, pol_stream);
                 bulk_commit();
                 bulk_wait_read<0>();                      // slot read by the store engine
-                mbar_arrive(&bar->empty[s]);
+                mbar_arrive(&bar->empty[c.s]);
             }
             bulk_wait<0>();
         }
@@ -223,14 +236,17 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         const int r = q * 32 + lane;                  // row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const float beta = (float)((p.ts[0] - 1.0) / p.ts[1]);   // beta_{k-1} = (t_{k-1}-1)/t_k
-        int64_t flushes = 0;
+        int flushes = 0;
         int last_flush_slot = -1;
         double rrun = 0.0;                            // this warpgroup's row sum over the current run
+        float bi = 0.f;
+        int cur_rb = -1;
         float *my_colS = colS + wg * 2 * 4 * 32;
 
-        auto load_xi = [&](int64_t rb) {
+        auto load_xi = [&](int rb) {
             // Xi' row r of row block rb into TMEM (hi and lo columns)
-            const float *src = p.XiR + (rb * TBM + r) * NK;
+            const float *src = p.XiR + ((int64_t)rb * TBM + r) * NK;
+#pragma unroll 1
             for (int k0 = 0; k0 < NK; k0 += 8) {
                 uint32_t hi[8], lo[8];
 #pragma unroll
@@ -248,15 +264,16 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->xi_full);
         };
-        // Theta X flush after tile tf (warpgroup 0 only, in tile order: each slot receives its
+        // Theta X flush after tile c (warpgroup 0 only, in tile order: each slot receives its
         // window partials from one thread in a fixed order -> deterministic)
-        auto flush = [&](int64_t tf) {
+        auto flush = [&](const Cursor &c) {
             mbar_wait(&bar->d2_full, (uint32_t)(flushes & 1));
             tc_fence_after();
-            const int sl = slot_of(tf);
+            const int sl = slot0 + (c.rb - rb0);
             const bool first = sl != last_flush_slot;
             last_flush_slot = sl;
             double *dst = p.rowpart + ((int64_t)sl * TBM + r) * W;
+#pragma unroll 1
             for (int d0 = 0; d0 < NP2; d0 += 16) {
                 uint32_t a[16];
                 tmem_ld16(tmem + lane_off + c_d2 + (uint32_t)d0, a);
@@ -274,36 +291,41 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             ++flushes;
         };
 
-        if (wg == 0) load_xi(t0 / nCB);
-        for (int64_t u = wg; u < U; u += 2) {
-            const int64_t t = t0 + u;
-            const int s = (int)(u % S), b = (int)(u & 1);
-            const int64_t rb = t / nCB, cb = t % nCB;
-            if (u > 0 && run_start(t)) {
+        Cursor c = start();
+        if (wg == 1) adv(c, 1);
+        if (wg == 0) load_xi(rb0);
+        for (; c.u < U; adv(c, 2)) {
+            const int b = c.u & 1;
+            const int rb = c.rb, cb = c.cb;
+            if (c.u > 0 && run_start(c)) {
                 // new run: all GEMM1 of the previous run are complete once D1 of tile u-1 is
-                mbar_wait(&bar->d1_full[b ^ 1], (uint32_t)(((u - 1) >> 1) & 1));
+                mbar_wait(&bar->d1_full[b ^ 1], (uint32_t)(((c.u - 1) >> 1) & 1));
                 load_xi(rb);
             }
-            const int64_t lr = rb * TBM + r, gr = p.row0 + lr;
-            const float bi = p.bv[lr];
-            // ---- Theta tiles landed? (B1, B2, y' of this tile)
-            mbar_wait(&bar->full[s], (uint32_t)((u / S) & 1));
-            uint8_t *st = stage_ptr(s);
+            const int64_t lr = (int64_t)rb * TBM + r, gr = p.row0 + lr;
+            if (rb != cur_rb) { bi = p.bv[lr]; cur_rb = rb; }
+            // ---- Theta tiles landed? (B1, B2, y' of this tile); S' = Xi' X^T ready in TMEM?
+            mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
+            mbar_wait(&bar->d1_full[b], (uint32_t)((c.u >> 1) & 1));
+            mbar_wait(&bar->at_empty[b], (uint32_t)(((c.u >> 1) & 1) ^ 1));   // GEMM2 of tile u-2 done
+            tc_fence_after();
+            uint8_t *st = stage_ptr(c.s);
             const float *yt = reinterpret_cast<const float *>(st + o_y);
             uint8_t *rowB1 = st + r * 128, *rowB2 = st + TILE_BYTES + r * 128;
-            // ---- S' = Xi' X^T from TMEM
-            mbar_wait(&bar->d1_full[b], (uint32_t)((u >> 1) & 1));
-            tc_fence_after();
-            const bool clean = (gr < cb * TBN || gr >= cb * TBN + TBN) && (cb * TBN + TBN <= p.N) && (lr < p.Ns);
-            float th[32];
-#pragma unroll
+            const int64_t j0 = (int64_t)cb * TBN;
+            const bool clean = (gr < j0 || gr >= j0 + TBN) && (j0 + TBN <= p.N) && (lr < p.Ns);
+            float rtile = 0.f;
+            float *colw = my_colS + ((((c.u >> 1) & 1) * 4) + q) * 32;
+            // two 16-column halves, rolled (keeps the loop body small: instruction-cache resident)
+#pragma unroll 1
             for (int half = 0; half < 2; ++half) {
                 uint32_t sv[16];
                 tmem_ld16(tmem + lane_off + c_d1 + (uint32_t)b * TBN + 16 * half, sv);
                 tmem_wait_ld();
+                float th[16];
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4) {
-                    const int k = 4 * half + k4;
+                    const int k = 4 * half + k4;                       // 16-byte chunk in the 128-B row
                     const int off = ((k ^ (r & 7)) << 4);
                     const float4 v1 = *reinterpret_cast<const float4 *>(rowB1 + off);
                     const float4 v2 = *reinterpret_cast<const float4 *>(rowB2 + off);
@@ -312,7 +334,6 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     const float yj[4] = {yv4.x, yv4.y, yv4.z, yv4.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int c = 4 * k + e;
                         const float acc = __uint_as_float(sv[4 * k4 + e]) - (yj[e] + bi);   // -(C eta)_ij / L
                         // theta~ + acc: b1 + acc formed exactly (TwoSum), one final rounding
                         const float dd = b1[e] - b2[e];
@@ -322,81 +343,77 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                         const float v = fmaf(beta, dd, sm) + er;
                         float o = fmaxf(v, 0.f);                                            // ( . )_+
                         if (!clean) {
-                            const int64_t j = cb * TBN + c;
+                            const int64_t j = j0 + 4 * k + e;
                             if (!(lr < p.Ns && j < p.N && j != gr)) o = 0.f;                // diag / tails
                         }
-                        th[c] = o;
+                        th[4 * k4 + e] = o;
                     }
+                    *reinterpret_cast<float4 *>(rowB2 + off) =                              // in place, for the store
+                        make_float4(th[4 * k4], th[4 * k4 + 1], th[4 * k4 + 2], th[4 * k4 + 3]);
                 }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar->d1_empty[b]);
-            // ---- Theta^k (hi = tf32 truncation, lo = remainder) into TMEM as GEMM2's A operand
-            mbar_wait(&bar->at_empty[b], (uint32_t)(((u >> 1) & 1) ^ 1));
-            tc_fence_after();
+                // Theta^k (hi = tf32 rounding, lo = remainder) into TMEM: GEMM2's A operand
+                {
+                    uint32_t h[16], l[16];
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint32_t h[16], l[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const float x = th[16 * half + e];
-                    const float hx = tf32_hi(x);
-                    h[e] = __float_as_uint(hx);
-                    l[e] = __float_as_uint(x - hx);
+                    for (int e = 0; e < 16; ++e) {
+                        const float hx = tf32_hi(th[e]);
+                        h[e] = __float_as_uint(hx);
+                        l[e] = __float_as_uint(th[e] - hx);
+                    }
+                    tmem_st16(tmem + lane_off + c_at + (uint32_t)b * 64 + 16 * half, h);
+                    tmem_st16(tmem + lane_off + c_at + (uint32_t)b * 64 + 32 + 16 * half, l);
                 }
-                tmem_st16(tmem + lane_off + c_at + (uint32_t)b * 64 + 16 * half, h);
-                tmem_st16(tmem + lane_off + c_at + (uint32_t)b * 64 + 32 + 16 * half, l);
+                // row sum of the half (pairwise)
+                {
+                    float s8[8];
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc) s8[cc] = th[cc] + th[cc + 8];
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) s8[cc] += s8[cc + 4];
+                    rtile += (s8[0] + s8[2]) + (s8[1] + s8[3]);
+                }
+                // column sums of the half over this warp's 32 rows: butterfly on lane bits 3..0,
+                // then across bit 4; lane l (< 16) ends with column 16 half + l
+                {
+                    float v8[8], v4[4], v2[2], v1[1];
+                    bfly<8>(th, v8, lane);
+                    bfly<4>(v8, v4, lane);
+                    bfly<2>(v4, v2, lane);
+                    bfly<1>(v2, v1, lane);
+                    const float cs = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 16);
+                    if (lane < 16) colw[16 * half + lane] = cs;
+                }
             }
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar->at_full[b]);
-            // ---- Theta^k into the B2 slot (in place) for the TMA store
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int off = ((k ^ (r & 7)) << 4);
-                *reinterpret_cast<float4 *>(rowB2 + off) = make_float4(th[4 * k], th[4 * k + 1], th[4 * k + 2], th[4 * k + 3]);
+            if (lane == 0) {
+                mbar_arrive(&bar->d1_empty[b]);
+                mbar_arrive(&bar->at_full[b]);
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->st_full[wg]);
-            // ---- row sum (this thread's row, pairwise in fp32, fp64 across tiles)
-            {
-                float s16[16];
-#pragma unroll
-                for (int c = 0; c < 16; ++c) s16[c] = th[c] + th[c + 16];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) s16[c] += s16[c + 8];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) s16[c] += s16[c + 4];
-                rrun += (double)((s16[0] + s16[2]) + (s16[1] + s16[3]));
-            }
-            // ---- column sums over this warp's 32 rows (butterfly transpose-reduce), then over warps
-            {
-                float v16[16], v8[8], v4[4], v2[2], v1[1];
-                bfly<16>(th, v16, lane);
-                bfly<8>(v16, v8, lane);
-                bfly<4>(v8, v4, lane);
-                bfly<2>(v4, v2, lane);
-                bfly<1>(v2, v1, lane);                                            // column = lane
-                my_colS[((((u >> 1) & 1) * 4) + q) * 32 + lane] = v1[0];
-            }
+            rrun += (double)rtile;
             named_barrier(1 + wg, 128);
             if (q == 0) {
-                const float *cs = my_colS + ((u >> 1) & 1) * 4 * 32;
+                const float *cs = my_colS + ((c.u >> 1) & 1) * 4 * 32;
                 const float c4 = (cs[lane] + cs[32 + lane]) + (cs[64 + lane] + cs[96 + lane]);
-                p.colpart[rb * p.ldT + cb * TBN + lane] = c4;
+                p.colpart[(int64_t)rb * p.ldT + j0 + lane] = c4;
             }
             // ---- this warpgroup's last tile of the run: its row-sum partial into the slot
-            if (u + 2 >= U || (t + 2) / nCB != rb) {
-                p.rowpart[((int64_t)slot_of(t) * TBM + r) * W + NP2 + wg] = rrun;
+            Cursor n2 = c;
+            adv(n2, 2);
+            if (n2.u >= U || n2.rb != rb) {
+                p.rowpart[((int64_t)(slot0 + rb - rb0) * TBM + r) * W + NP2 + wg] = rrun;
                 rrun = 0.0;
             }
             // ---- Theta X flushes (warpgroup 0 handles those after tiles u and u+1)
             if (wg == 0) {
-                if (flush_after(t)) flush(t);
-                if (u + 1 < U && flush_after(t + 1)) flush(t + 1);
+                if (flush_after(c)) flush(c);
+                Cursor n1 = c;
+                adv(n1, 1);
+                if (n1.u < U && flush_after(n1)) flush(n1);
             }
         }
     }
