@@ -207,6 +207,7 @@ struct cr_ctx {
     int G_tc = 0, stages = 0, window = 64, smem_tc = 0;
     uint32_t stage_bytes = 0;
     int64_t T_tc = 0;
+    unsigned long long *trace = nullptr;   // debug timeline buffer (CR_TC_TRACE=<file>)
     ncclComm_t comm = nullptr;
 
     template <typename P> P *at(size_t off) { return reinterpret_cast<P *>(ws + off); }
@@ -352,6 +353,7 @@ TcParams tc_params(cr_ctx *ctx) {
     p.colpart = ctx->at<float>(Ly.colpart);
     p.rowpart = ctx->at<double>(Ly.rowpart);
     p.cta_slot0 = ctx->at<int>(Ly.slot0_tc);
+    p.trace = ctx->trace;
     p.ts = ctx->at<double>(Ly.ts);
     return p;
 }
@@ -660,7 +662,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         ctx->stages = (int)std::min<size_t>(kTcMaxStages, (budget - fixed) / ctx->stage_bytes);
         if (ctx->stages < 2) { fail(ctx, CR_ERR_UNSUPPORTED, "tc pass: smem"); return bail(CR_ERR_UNSUPPORTED); }
         ctx->smem_tc = (int)(ctx->stages * (size_t)ctx->stage_bytes + fixed);
-        IK(pass_tc_prepare(ctx->smem_tc));
+        IK(pass_tc_prepare(Ly.NK, ctx->smem_tc));
         slot_tables(ctx->G_tc, ctx->T_tc, Ly.nRBtc, Ly.nCBtc, slot0t, rb_ptrt, slotst);
         IK(cudaMemcpyAsync(ctx->ws + Ly.slot0_tc, slot0t.data(), slot0t.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
         IK(cudaMemcpyAsync(ctx->ws + Ly.rb_ptr_tc, rb_ptrt.data(), rb_ptrt.size() * 4, cudaMemcpyHostToDevice,
@@ -670,6 +672,10 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         IK(launch_tc_images(ctx->at<double>(Ly.X64), N, n, Ly.NK, Ly.NP2, Ly.nCBtc, ctx->at<float>(Ly.g1h),
                             ctx->at<float>(Ly.g1l), ctx->at<float>(Ly.g2h), ctx->at<float>(Ly.g2l), ctx->stream));
         ctx->launches += 1;
+        if (std::getenv("CR_TC_TRACE")) {
+            IK(cudaMalloc(&ctx->trace, 5 * 256 * 8 * 8));
+            IK(cudaMemsetAsync(ctx->trace, 0, 5 * 256 * 8 * 8, ctx->stream));
+        }
         for (int b = 0; b < 2; ++b)
             if (!make_theta_tmap(&ctx->tm[b], ctx->th[b], Ly.Rp, Ly.ldT)) {
                 fail(ctx, CR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -784,6 +790,15 @@ cr_status cr_dual_step(cr_ctx *ctx, cr_step_stats *out) {
     cr_status st = check_ctx(ctx);
     if (st != CR_OK) return st;
     if ((st = enqueue_step(ctx, true)) != CR_OK) return st;
+    if (ctx->trace) {   // debug: dump the tensor-core pass timeline of CTA 0
+        std::vector<unsigned long long> h(5 * 256 * 8);
+        CK(cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (FILE *f = std::fopen(std::getenv("CR_TC_TRACE"), "wb")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
     advance_host(ctx);
     if (out) return eval_stats(ctx, out);
     return CR_OK;
@@ -897,6 +912,7 @@ void cr_destroy(cr_ctx *ctx) {
     cudaSetDevice(ctx->device);
     drop_graphs(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->trace) cudaFree(ctx->trace);
     for (auto e : ctx->ev) cudaEventDestroy(e);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     delete ctx;

@@ -121,12 +121,13 @@ struct TcParams {
     float *colpart;                  // [nRB128][ldT]
     double *rowpart;                 // [slots][128][NP2]
     const int *cta_slot0;
+    unsigned long long *trace;       // debug: clock64 timeline of CTA 0 (nullptr = off)
     const double *ts;
 };
 
 // tcgen05 fused pass (kernels/pass_tc.cu).
 cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const TcParams &p, cudaStream_t s);
-cudaError_t pass_tc_prepare(int smem_bytes);
+cudaError_t pass_tc_prepare(int NK, int smem_bytes);
 size_t tc_barrier_bytes();
 cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,
                              float *g2h, float *g2l, cudaStream_t s);

@@ -68,8 +68,17 @@ struct Cursor {
     int u, rb, cb, s, ph;
 };
 
+// debug timeline (p.trace != nullptr): clock64 of role events for the first 256 tiles of CTA 0
+#define TC_TRACE(role, u, ev)                                                                   \
+    do {                                                                                        \
+        if (p.trace && blockIdx.x == 0 && (u) < 256)                                            \
+            p.trace[((role) * 256 + (u)) * 8 + (ev)] = clock64();                               \
+    } while (0)
+
+template <int NK>
 __global__ void __launch_bounds__(NTHR, 1)
 pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2, const TcParams p) {
+    constexpr int NP2 = (NK + 15) / 16 * 16;           // GEMM2 N (multiple of 16 for M = 128)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = p.stages;
@@ -82,12 +91,12 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     if (t0 >= t1) return;
     const int U = t1 - t0;
     const int nCB = p.nCB;
-    const int NK = p.NK, NP2 = p.NP2, W = p.NP2 + 2;
+    constexpr int W = NP2 + 2;
     const int wmask = p.window - 1;                    // flush window (power of two)
     // stage image: [B1 16K][B2 16K][X hi][X lo][X^T hi][X^T lo][y' 128 B]
-    const uint32_t g1_bytes = (uint32_t)NK * 128, g2_bytes = (uint32_t)NP2 * 128;
-    const uint32_t o_g1 = 2 * TILE_BYTES, o_g2 = o_g1 + 2 * g1_bytes, o_y = o_g2 + 2 * g2_bytes;
-    const uint32_t lbo2 = (uint32_t)NP2 * 16;          // X^T image: K-chunk (4 j) stride
+    constexpr uint32_t g1_bytes = (uint32_t)NK * 128, g2_bytes = (uint32_t)NP2 * 128;
+    constexpr uint32_t o_g1 = 2 * TILE_BYTES, o_g2 = o_g1 + 2 * g1_bytes, o_y = o_g2 + 2 * g2_bytes;
+    constexpr uint32_t lbo2 = (uint32_t)NP2 * 16;      // X^T image: K-chunk (4 j) stride
     const int rb0 = t0 / nCB, cb0 = t0 - rb0 * nCB;
     const int slot0 = p.cta_slot0[blockIdx.x];
 
@@ -134,7 +143,9 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         if (lane == 0) {
             const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
             for (Cursor c = start(); c.u < U; adv(c, 1)) {
+                TC_TRACE(0, c.u, 0);
                 mbar_wait(&bar->empty[c.s], (uint32_t)(c.ph ^ 1));
+                TC_TRACE(0, c.u, 1);
                 uint8_t *st = stage_ptr(c.s);
                 uint64_t *fb = &bar->full[c.s];
                 mbar_arrive_expect_tx(fb, 2 * TILE_BYTES + 2 * g1_bytes + 2 * g2_bytes + TBN * 4);
@@ -156,16 +167,18 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             bool window_start = true;
             auto gemm1 = [&](const Cursor &c) {
                 const int b = c.u & 1;
+                TC_TRACE(1, c.u, 0);
                 mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
                 mbar_wait(&bar->d1_empty[b], (uint32_t)(((c.u >> 1) & 1) ^ 1));
+                TC_TRACE(1, c.u, 1);
                 tc_fence_after();
                 const uint8_t *xh = stage_ptr(c.s) + o_g1;
                 const uint32_t d = tmem + c_d1 + (uint32_t)b * TBN;
-#pragma unroll 1
+#pragma unroll
                 for (int pass = 0; pass < 3; ++pass) {
                     const uint8_t *xb = pass == 1 ? xh + g1_bytes : xh;
                     const uint32_t a_col = c_xi + (pass == 2 ? (uint32_t)NK : 0u);
-#pragma unroll 1
+#pragma unroll
                     for (int kk = 0; kk < NK / 8; ++kk) {
                         // K-major interleave: 4-k chunks LBO = 512 B apart, 8-row j groups SBO = 128 B
                         const uint64_t bd = smem_desc(xb + kk * 1024, 512, 128, 0);
@@ -173,6 +186,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     }
                 }
                 mma_commit(&bar->d1_full[b]);
+                TC_TRACE(1, c.u, 2);
             };
             mbar_wait(&bar->xi_full, 0);
             tc_fence_after();
@@ -184,15 +198,17 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 const bool next_same_run = (n.u < U) && n.cb != 0;
                 if (next_same_run) gemm1(n);
                 const int a = c.u & 1;
+                TC_TRACE(1, c.u, 3);
                 mbar_wait(&bar->at_full[a], (uint32_t)((c.u >> 1) & 1));
                 if (window_start && flushes > 0) mbar_wait(&bar->d2_empty, (uint32_t)((flushes - 1) & 1));
+                TC_TRACE(1, c.u, 4);
                 tc_fence_after();
                 const uint8_t *xh = stage_ptr(c.s) + o_g2;
-#pragma unroll 1
+#pragma unroll
                 for (int pass = 0; pass < 3; ++pass) {
                     const uint8_t *xb = pass == 1 ? xh + g2_bytes : xh;
                     const uint32_t a_col = c_at + (uint32_t)a * 64 + (pass == 2 ? 32u : 0u);
-#pragma unroll 1
+#pragma unroll
                     for (int jj = 0; jj < TBN / 8; ++jj) {
                         // X^T image, K-major interleave: 4-j chunks lbo2 apart, 8-row d groups 128 B
                         const uint64_t bd = smem_desc(xb + jj * 2 * lbo2, lbo2, 128, 0);
@@ -202,6 +218,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 }
                 mma_commit(&bar->at_empty[a]);
                 mma_commit(&bar->empty[c.s]);
+                TC_TRACE(1, c.u, 5);
                 window_start = false;
                 if (flush_after(c)) {
                     mma_commit(&bar->d2_full);
@@ -221,10 +238,13 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         if (lane == 0) {
             const uint64_t pol_stream = policy_evict_first();
             for (Cursor c = start(); c.u < U; adv(c, 1)) {
+                TC_TRACE(2, c.u, 0);
                 mbar_wait(&bar->st_full[c.u & 1], (uint32_t)((c.u >> 1) & 1));
+                TC_TRACE(2, c.u, 1);
                 tma_store_2d(&tmB2, c.cb * TBN, c.rb * TBM, stage_ptr(c.s) + TILE_BYTES, pol_stream);
                 bulk_commit();
                 bulk_wait_read<0>();                      // slot read by the store engine
+                TC_TRACE(2, c.u, 2);
                 mbar_arrive(&bar->empty[c.s]);
             }
             bulk_wait<0>();
@@ -246,7 +266,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         auto load_xi = [&](int rb) {
             // Xi' row r of row block rb into TMEM (hi and lo columns)
             const float *src = p.XiR + ((int64_t)rb * TBM + r) * NK;
-#pragma unroll 1
+#pragma unroll
             for (int k0 = 0; k0 < NK; k0 += 8) {
                 uint32_t hi[8], lo[8];
 #pragma unroll
@@ -294,9 +314,11 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         Cursor c = start();
         if (wg == 1) adv(c, 1);
         if (wg == 0) load_xi(rb0);
+        const bool tr = (q == 0 && lane == 0);
         for (; c.u < U; adv(c, 2)) {
             const int b = c.u & 1;
             const int rb = c.rb, cb = c.cb;
+            if (tr) TC_TRACE(3 + wg, c.u, 0);
             if (c.u > 0 && run_start(c)) {
                 // new run: all GEMM1 of the previous run are complete once D1 of tile u-1 is
                 mbar_wait(&bar->d1_full[b ^ 1], (uint32_t)(((c.u - 1) >> 1) & 1));
@@ -306,8 +328,11 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             if (rb != cur_rb) { bi = p.bv[lr]; cur_rb = rb; }
             // ---- Theta tiles landed? (B1, B2, y' of this tile); S' = Xi' X^T ready in TMEM?
             mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
+            if (tr) TC_TRACE(3 + wg, c.u, 1);
             mbar_wait(&bar->d1_full[b], (uint32_t)((c.u >> 1) & 1));
+            if (tr) TC_TRACE(3 + wg, c.u, 2);
             mbar_wait(&bar->at_empty[b], (uint32_t)(((c.u >> 1) & 1) ^ 1));   // GEMM2 of tile u-2 done
+            if (tr) TC_TRACE(3 + wg, c.u, 3);
             tc_fence_after();
             uint8_t *st = stage_ptr(c.s);
             const float *yt = reinterpret_cast<const float *>(st + o_y);
@@ -387,6 +412,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
+            if (tr) TC_TRACE(3 + wg, c.u, 4);
             if (lane == 0) {
                 mbar_arrive(&bar->d1_empty[b]);
                 mbar_arrive(&bar->at_full[b]);
@@ -396,6 +422,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             if (lane == 0) mbar_arrive(&bar->st_full[wg]);
             rrun += (double)rtile;
             named_barrier(1 + wg, 128);
+            if (tr) TC_TRACE(3 + wg, c.u, 5);
             if (q == 0) {
                 const float *cs = my_colS + ((c.u >> 1) & 1) * 4 * 32;
                 const float c4 = (cs[lane] + cs[32 + lane]) + (cs[64 + lane] + cs[96 + lane]);
@@ -415,6 +442,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 adv(n1, 1);
                 if (n1.u < U && flush_after(n1)) flush(n1);
             }
+            if (tr) TC_TRACE(3 + wg, c.u, 6);
         }
     }
     tc_fence_before();
@@ -449,13 +477,26 @@ __global__ void tc_images_kernel(const double *X64, int64_t N, int n, int NK, in
 
 }  // namespace
 
+#define CR_TC_NK_LIST(X) X(8) X(16) X(24) X(32) X(40) X(48) X(56) X(64) X(72) X(80)
+
 cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const TcParams &p, cudaStream_t s) {
-    pass_tc_kernel<<<p.G, NTHR, p.smem_bytes, s>>>(tmB1, tmB2, p);
+    switch (p.NK) {
+#define CR_CASE(V) case V: pass_tc_kernel<V><<<p.G, NTHR, p.smem_bytes, s>>>(tmB1, tmB2, p); break;
+        CR_TC_NK_LIST(CR_CASE)
+#undef CR_CASE
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
-cudaError_t pass_tc_prepare(int smem_bytes) {
-    return cudaFuncSetAttribute(pass_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+cudaError_t pass_tc_prepare(int NK, int smem_bytes) {
+    switch (NK) {
+#define CR_CASE(V) \
+    case V: return cudaFuncSetAttribute(pass_tc_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+        CR_TC_NK_LIST(CR_CASE)
+#undef CR_CASE
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 size_t tc_barrier_bytes() { return sizeof(TcBarriers) + 8 + 2 * 2 * 4 * 32 * 4; }
