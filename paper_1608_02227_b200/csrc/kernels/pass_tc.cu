@@ -159,18 +159,19 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             }
         }
     } else if (warp == 1) {
-        // ============================================================ MMA issuer
-        if (lane == 0) {
+        // ============================================================ MMA issuer (whole warp, convergent;
+        // elect.sync inside the tcgen05 wrappers picks the issuing lane)
+        {
             const uint32_t id1 = idesc_tf32(TBM, TBN, 0, 0);   // A K-major (TMEM), B K-major
             const uint32_t id2 = idesc_tf32(TBM, NP2, 0, 0);
             int run = 0, flushes = 0;
             bool window_start = true;
             auto gemm1 = [&](const Cursor &c) {
                 const int b = c.u & 1;
-                TC_TRACE(1, c.u, 0);
+                if (lane == 0) TC_TRACE(1, c.u, 0);
                 mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
                 mbar_wait(&bar->d1_empty[b], (uint32_t)(((c.u >> 1) & 1) ^ 1));
-                TC_TRACE(1, c.u, 1);
+                if (lane == 0) TC_TRACE(1, c.u, 1);
                 tc_fence_after();
                 const uint8_t *xh = stage_ptr(c.s) + o_g1;
                 const uint32_t d = tmem + c_d1 + (uint32_t)b * TBN;
@@ -182,11 +183,11 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     for (int kk = 0; kk < NK / 8; ++kk) {
                         // K-major interleave: 4-k chunks LBO = 512 B apart, 8-row j groups SBO = 128 B
                         const uint64_t bd = smem_desc(xb + kk * 1024, 512, 128, 0);
-                        mma_tf32_ts(d, tmem + a_col + (uint32_t)kk * 8, bd, id1, (pass | kk) != 0);
+                        mma_tf32_ts_warp(d, tmem + a_col + (uint32_t)kk * 8, bd, id1, (pass | kk) != 0);
                     }
                 }
-                mma_commit(&bar->d1_full[b]);
-                TC_TRACE(1, c.u, 2);
+                mma_commit_warp(&bar->d1_full[b]);
+                if (lane == 0) TC_TRACE(1, c.u, 2);
             };
             mbar_wait(&bar->xi_full, 0);
             tc_fence_after();
@@ -198,10 +199,10 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 const bool next_same_run = (n.u < U) && n.cb != 0;
                 if (next_same_run) gemm1(n);
                 const int a = c.u & 1;
-                TC_TRACE(1, c.u, 3);
+                if (lane == 0) TC_TRACE(1, c.u, 3);
                 mbar_wait(&bar->at_full[a], (uint32_t)((c.u >> 1) & 1));
                 if (window_start && flushes > 0) mbar_wait(&bar->d2_empty, (uint32_t)((flushes - 1) & 1));
-                TC_TRACE(1, c.u, 4);
+                if (lane == 0) TC_TRACE(1, c.u, 4);
                 tc_fence_after();
                 const uint8_t *xh = stage_ptr(c.s) + o_g2;
 #pragma unroll
@@ -212,16 +213,16 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     for (int jj = 0; jj < TBN / 8; ++jj) {
                         // X^T image, K-major interleave: 4-j chunks lbo2 apart, 8-row d groups 128 B
                         const uint64_t bd = smem_desc(xb + jj * 2 * lbo2, lbo2, 128, 0);
-                        mma_tf32_ts(tmem + c_d2, tmem + a_col + (uint32_t)jj * 8, bd, id2,
-                                    !(window_start && pass == 0 && jj == 0));
+                        mma_tf32_ts_warp(tmem + c_d2, tmem + a_col + (uint32_t)jj * 8, bd, id2,
+                                         !(window_start && pass == 0 && jj == 0));
                     }
                 }
-                mma_commit(&bar->at_empty[a]);
-                mma_commit(&bar->empty[c.s]);
-                TC_TRACE(1, c.u, 5);
+                mma_commit_warp(&bar->at_empty[a]);
+                mma_commit_warp(&bar->empty[c.s]);
+                if (lane == 0) TC_TRACE(1, c.u, 5);
                 window_start = false;
                 if (flush_after(c)) {
-                    mma_commit(&bar->d2_full);
+                    mma_commit_warp(&bar->d2_full);
                     ++flushes;
                     window_start = true;
                 }
