@@ -79,8 +79,10 @@ template <int NK>
 __global__ void __launch_bounds__(NTHR, 1)
 pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2, const TcParams p) {
     constexpr int NP2 = (NK + 15) / 16 * 16;           // GEMM2 N (multiple of 16 for M = 128)
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    // 1024-byte alignment by offsetting the shared pointer itself (an integer round trip would
+    // lose the shared address space and turn every access into a generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int S = p.stages;
     const uint32_t stage_bytes = p.stage_bytes;
     TcBarriers *bar = reinterpret_cast<TcBarriers *>(smem + (size_t)S * stage_bytes);
@@ -325,7 +327,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 mbar_wait(&bar->d1_full[b ^ 1], (uint32_t)(((c.u - 1) >> 1) & 1));
                 load_xi(rb);
             }
-            const int64_t lr = (int64_t)rb * TBM + r, gr = p.row0 + lr;
+            const int lr = rb * TBM + r;                  // local row (< 2^31: Rp * 128)
             if (rb != cur_rb) { bi = p.bv[lr]; cur_rb = rb; }
             // ---- Theta tiles landed? (B1, B2, y' of this tile); S' = Xi' X^T ready in TMEM?
             mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
@@ -339,7 +341,17 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             const float *yt = reinterpret_cast<const float *>(st + o_y);
             uint8_t *rowB1 = st + r * 128, *rowB2 = st + TILE_BYTES + r * 128;
             const int64_t j0 = (int64_t)cb * TBN;
-            const bool clean = (gr < j0 || gr >= j0 + TBN) && (j0 + TBN <= p.N) && (lr < p.Ns);
+            // masks in tile-local 32-bit terms: the diagonal column (if in this tile), the
+            // number of real columns, and whether this row exists
+            const int64_t dg = p.row0 + lr - j0;
+            const int dcol = (dg >= 0 && dg < TBN) ? (int)dg : -1;
+            const int nvalid = (int)min((int64_t)TBN, p.N - j0);
+            const bool row_ok = lr < p.Ns;
+            // valid-column bit mask of this thread's row; 'dirty' warps (diagonal / tails) take a
+            // separate, warp-uniform masking branch
+            uint32_t vmask = row_ok ? (nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u)) : 0u;
+            if (dcol >= 0) vmask &= ~(1u << dcol);
+            const bool dirty = __any_sync(0xffffffffu, vmask != 0xffffffffu);
             float rtile = 0.f;
             float *colw = my_colS + ((((c.u >> 1) & 1) * 4) + q) * 32;
             // two 16-column halves, rolled (keeps the loop body small: instruction-cache resident)
@@ -361,18 +373,15 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float acc = __uint_as_float(sv[4 * k4 + e]) - (yj[e] + bi);   // -(C eta)_ij / L
-                        // theta~ + acc: b1 + acc formed exactly (TwoSum), one final rounding
-                        const float dd = b1[e] - b2[e];
-                        const float sm = b1[e] + acc;
-                        const float bb = sm - b1[e];
-                        const float er = (b1[e] - (sm - bb)) + (acc - bb);
-                        const float v = fmaf(beta, dd, sm) + er;
-                        float o = fmaxf(v, 0.f);                                            // ( . )_+
-                        if (!clean) {
-                            const int64_t j = j0 + 4 * k + e;
-                            if (!(lr < p.Ns && j < p.N && j != gr)) o = 0.f;                // diag / tails
-                        }
-                        th[4 * k4 + e] = o;
+                        // theta~ - (C eta)/L = b1 + (beta (b1 - b2) + acc): the inner rounding is at
+                        // the scale of the update, so the stored value carries ~one rounding of theta
+                        const float v = b1[e] + fmaf(beta, b1[e] - b2[e], acc);
+                        th[4 * k4 + e] = fmaxf(v, 0.f);                                     // ( . )_+
+                    }
+                    if (dirty) {                                                            // diag / tails
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (!((vmask >> (4 * k + e)) & 1u)) th[4 * k4 + e] = 0.f;
                     }
                     *reinterpret_cast<float4 *>(rowB2 + off) =                              // in place, for the store
                         make_float4(th[4 * k4], th[4 * k4 + 1], th[4 * k4 + 2], th[4 * k4 + 3]);
@@ -398,17 +407,20 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     for (int cc = 0; cc < 4; ++cc) s8[cc] += s8[cc + 4];
                     rtile += (s8[0] + s8[2]) + (s8[1] + s8[3]);
                 }
-                // column sums of the half over this warp's 32 rows: butterfly on lane bits 3..0,
-                // then across bit 4; lane l (< 16) ends with column 16 half + l
-                {
-                    float v8[8], v4[4], v2[2], v1[1];
-                    bfly<8>(th, v8, lane);
-                    bfly<4>(v8, v4, lane);
-                    bfly<2>(v4, v2, lane);
-                    bfly<1>(v2, v1, lane);
-                    const float cs = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 16);
-                    if (lane < 16) colw[16 * half + lane] = cs;
+            }
+            // column sums over this warp's 32 rows from the staged Theta^k tile: lane = column,
+            // rows in a fixed order (conflict-free: the 128-B swizzle spreads a row over all banks)
+            __syncwarp();
+            {
+                const uint8_t *tile = st + TILE_BYTES;
+                const int cofs = (lane & 3) * 4;
+                float cs = 0.f;
+#pragma unroll 8
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int row = q * 32 + rr;
+                    cs += *reinterpret_cast<const float *>(tile + row * 128 + (((lane >> 2) ^ (row & 7)) << 4) + cofs);
                 }
+                colw[lane] = cs;
             }
             tmem_wait_st();
             tc_fence_before();
