@@ -109,7 +109,7 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     L->rb_slots = take((size_t)(L->nRB + kGMax) * 4);
     L->cfull = take((size_t)WS * 8);
     L->ts = take(sizeof(DevScalars));
-    L->statpro = take((size_t)(L->Rp / 256 + 2) * 8 * 8);
+    L->statpro = take((size_t)kStatBlocks * 8 * 8);
     L->statres = take((size_t)kStatBlocks * 8 * 8);
     if (L->tc) {
         L->g1h = take((size_t)L->nCBtc * L->NK * 128);
@@ -318,7 +318,7 @@ SmallParams small_params(cr_ctx *ctx, int sa, int sb, int use_beta, double scale
     p.a64 = ctx->at<double>(Ly.a64);
     p.yv = ctx->ws + Ly.yv;
     p.bv = ctx->ws + Ly.bv;
-    p.XiT = ctx->ws + Ly.XiT;
+    p.XiT = Ly.tc ? nullptr : ctx->ws + Ly.XiT;          // the SIMT pass operand only
     p.statpart = stats ? ctx->at<double>(Ly.statpro) : nullptr;
     p.ts = ctx->at<DevScalars>(Ly.ts);
     p.use_beta = use_beta;

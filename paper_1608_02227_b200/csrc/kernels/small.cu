@@ -18,13 +18,17 @@
 namespace cr {
 namespace {
 
+// One warp per row (grid-stride), lanes over the n features: coalesced fp64 reads of the
+// sums, coalesced writes of xi; a_i by a fixed-order warp reduction.  Per-block partials of
+// |u|^2, u.ybar, |xi|^2 and a nonfinite flag go to statpart (fixed order: deterministic).
 template <typename T>
-__global__ void prologue_kernel(const SmallParams p) {
-    __shared__ double red[4][256];
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
+    __shared__ double red[4][8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double beta = p.use_beta ? (p.ts->t_prev - 1.0) / p.ts->t_cur : 0.0;
     double u2 = 0.0, uy = 0.0, xi2 = 0.0, bad = 0.0;
-    if (i < p.Ns) {
-        const double beta = p.use_beta ? (p.ts->t_prev - 1.0) / p.ts->t_cur : 0.0;
+    T *XiT = static_cast<T *>(p.XiT);
+    for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < p.Ns; i += (int64_t)gridDim.x * 8) {
         const double r1 = p.r1[i], r2 = p.r2[i], c1 = p.c1[i], c2 = p.c2[i];
         const double rt = r1 + beta * (r1 - r2);
         const double ct = c1 + beta * (c1 - c2);
@@ -32,71 +36,97 @@ __global__ void prologue_kernel(const SmallParams p) {
         const double u = ct - rt;                       // (A1^T theta~)_i
         const double y = p.ybar[gi] + u;
         const double *x = p.X64 + gi * p.n;
-        double a = 0.0;
-        T *XiT = static_cast<T *>(p.XiT);
-        for (int d = 0; d < p.n; ++d) {
+        double a = 0.0, q2 = 0.0;
+        for (int d = lane; d < p.n; d += 32) {
             const double P1 = p.P1[i * p.n + d], P2 = p.P2[i * p.n + d];
             const double Pt = P1 + beta * (P1 - P2);
             const double xi = (rt * x[d] - Pt) / p.gamma;   // (A2^T theta~)_i / gamma
             p.Xi64[i * p.n + d] = xi;
-            XiT[(int64_t)d * p.Rp + i] = T(xi * p.scale);
+            if (XiT) XiT[(int64_t)d * p.Rp + i] = T(xi * p.scale);
             if (p.XiR) p.XiR[i * p.NK + d] = (float)(xi * p.scale);
             a += xi * x[d];
-            xi2 += xi * xi;
+            q2 += xi * xi;
         }
-        p.y64[gi] = y;
-        p.a64[i] = a;
-        static_cast<T *>(p.yv)[gi] = T(y * p.scale);
-        static_cast<T *>(p.bv)[i] = T((a - y) * p.scale);
-        u2 = u * u;
-        uy = u * p.ybar[gi];
-        bad = (isfinite(y) && isfinite(a)) ? 0.0 : 1.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+        }
+        if (lane == 0) {
+            p.y64[gi] = y;
+            p.a64[i] = a;
+            static_cast<T *>(p.yv)[gi] = T(y * p.scale);
+            static_cast<T *>(p.bv)[i] = T((a - y) * p.scale);
+            u2 += u * u;
+            uy += u * p.ybar[gi];
+            xi2 += q2;
+            bad += (isfinite(y) && isfinite(a)) ? 0.0 : 1.0;
+        }
     }
-    red[0][threadIdx.x] = u2; red[1][threadIdx.x] = uy; red[2][threadIdx.x] = xi2; red[3][threadIdx.x] = bad;
+    if (lane == 0) { red[0][warp] = u2; red[1][warp] = uy; red[2][warp] = xi2; red[3][warp] = bad; }
     __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if ((int)threadIdx.x < s)
-            for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + s];
-        __syncthreads();
+    if (threadIdx.x < 4 && p.statpart) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+        p.statpart[blockIdx.x * 8 + threadIdx.x] = t;
     }
-    if (threadIdx.x == 0 && p.statpart)
-        for (int q = 0; q < 4; ++q) p.statpart[blockIdx.x * 8 + q] = red[q][0];
 }
 
+// Blocks [0, ncolb): column sums, 32 columns per block, 8 warps splitting the row-block range
+// (fixed chunks, combined in order).  Remaining blocks: one thread per (row, d <= n) summing
+// that row's run slots in a fixed order and resetting each consumed partial to 0.
 template <typename Tc>
-__global__ void reduce_kernel(const ReduceParams p) {
-    const int64_t nrow = p.Ns * (p.n + 1);
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < nrow) {
-        const int64_t i = g / (p.n + 1);
-        const int d = (int)(g % (p.n + 1));
-        const int rb = (int)(i / p.rbm), ii = (int)(i % p.rbm);
-        double s = 0.0;
-        // fixed slot order; each consumed partial is reset to 0 (passes may rely on zeroed slots)
-        for (int e = p.rb_ptr[rb]; e < p.rb_ptr[rb + 1]; ++e) {
-            double *row = const_cast<double *>(p.rowpart) + ((int64_t)p.rb_slots[e] * p.rbm + ii) * p.NBP;
-            if (d < p.n) {
-                s += row[d];
-                row[d] = 0.0;
-            } else {
-                s += row[p.rcol0];
-                row[p.rcol0] = 0.0;
-                if (p.rcol1 >= 0) {
-                    s += row[p.rcol1];
-                    row[p.rcol1] = 0.0;
+__global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int ncolb) {
+    if ((int)blockIdx.x < ncolb) {
+        __shared__ double cs[8][32];
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+        const Tc *cp = static_cast<const Tc *>(p.colpart);
+        const int rb0 = (int)((int64_t)p.nRB * warp / 8), rb1 = (int)((int64_t)p.nRB * (warp + 1) / 8);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (j < p.N) {
+            int rb = rb0;
+            for (; rb + 4 <= rb1; rb += 4) {
+                s0 += (double)cp[(int64_t)rb * p.ldT + j];
+                s1 += (double)cp[(int64_t)(rb + 1) * p.ldT + j];
+                s2 += (double)cp[(int64_t)(rb + 2) * p.ldT + j];
+                s3 += (double)cp[(int64_t)(rb + 3) * p.ldT + j];
+            }
+            for (; rb < rb1; ++rb) s0 += (double)cp[(int64_t)rb * p.ldT + j];
+        }
+        cs[warp][lane] = (s0 + s1) + (s2 + s3);
+        __syncthreads();
+        if (warp == 0 && j < p.N) {
+            double s = 0.0;
+            for (int w = 0; w < 8; ++w) s += cs[w][lane];
+            p.c_out[j] = s;
+        }
+    } else {
+        const int64_t g = (int64_t)(blockIdx.x - ncolb) * blockDim.x + threadIdx.x;
+        if (g < p.Ns * (p.n + 1)) {
+            const int64_t i = g / (p.n + 1);
+            const int d = (int)(g % (p.n + 1));
+            const int rb = (int)(i / p.rbm), ii = (int)(i % p.rbm);
+            double s = 0.0;
+            for (int e = p.rb_ptr[rb]; e < p.rb_ptr[rb + 1]; ++e) {
+                double *row = const_cast<double *>(p.rowpart) + ((int64_t)p.rb_slots[e] * p.rbm + ii) * p.NBP;
+                if (d < p.n) {
+                    s += row[d];
+                    row[d] = 0.0;
+                } else {
+                    s += row[p.rcol0];
+                    row[p.rcol0] = 0.0;
+                    if (p.rcol1 >= 0) {
+                        s += row[p.rcol1];
+                        row[p.rcol1] = 0.0;
+                    }
                 }
             }
+            if (d < p.n) p.P[i * p.n + d] = s;
+            else p.r[i] = s;
         }
-        if (d < p.n) p.P[i * p.n + d] = s;
-        else p.r[i] = s;
-    } else if (g < nrow + p.N) {
-        const int64_t j = g - nrow;
-        const Tc *cp = static_cast<const Tc *>(p.colpart);
-        double s = 0.0;
-        for (int rb = 0; rb < p.nRB; ++rb) s += (double)cp[(int64_t)rb * p.ldT + j];
-        p.c_out[j] = s;
     }
-    if (p.advance_t && g == 0) {
+    if (p.advance_t && blockIdx.x == 0 && threadIdx.x == 0) {
         const double t = p.ts->t_cur;
         p.ts->t_prev = t;
         p.ts->t_cur = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;   // Step 3
@@ -212,22 +242,21 @@ inline unsigned nblk(int64_t work, int bs) { return (unsigned)((work + bs - 1) /
 }  // namespace
 
 cudaError_t launch_prologue(const SmallParams &p, int fp64, cudaStream_t s, int *nb_out) {
-    const unsigned nb = p.Ns > 0 ? nblk(p.Ns, 256) : 1;
-    if (nb > (unsigned)kStatBlocks && p.statpart) {
-        // statpart capacity: fall back to no per-block stats (caller passes statpart only
-        // when Ns <= 256 * kStatBlocks)
-    }
-    if (fp64) prologue_kernel<double><<<nb, 256, 0, s>>>(p);
-    else prologue_kernel<float><<<nb, 256, 0, s>>>(p);
+    int64_t nb = (p.Ns + 7) / 8;
+    if (nb < 1) nb = 1;
+    if (nb > kStatBlocks) nb = kStatBlocks;
+    if (fp64) prologue_kernel<double><<<(unsigned)nb, 256, 0, s>>>(p);
+    else prologue_kernel<float><<<(unsigned)nb, 256, 0, s>>>(p);
     if (nb_out) *nb_out = (int)nb;
     return cudaGetLastError();
 }
 
 cudaError_t launch_reduce(const ReduceParams &p, int fp64, cudaStream_t s) {
-    const int64_t work = p.Ns * (p.n + 1) + p.N;
-    const unsigned nb = work > 0 ? nblk(work, 256) : 1;
-    if (fp64) reduce_kernel<double><<<nb, 256, 0, s>>>(p);
-    else reduce_kernel<float><<<nb, 256, 0, s>>>(p);
+    const int ncolb = (int)((p.N + 31) / 32);
+    const int64_t nrowb = (p.Ns * (p.n + 1) + 255) / 256;
+    const unsigned nb = (unsigned)(ncolb + nrowb);
+    if (fp64) reduce_kernel<double><<<nb, 256, 0, s>>>(p, ncolb);
+    else reduce_kernel<float><<<nb, 256, 0, s>>>(p, ncolb);
     return cudaGetLastError();
 }
 
