@@ -16,7 +16,7 @@
 // Theta^{k-1}, Theta^{k-2} tiles arrive by TMA (128B-swizzled 128x32 boxes); Theta^k leaves by
 // TMA store from the same smem slot.  The Theta X accumulator lives in TMEM and is flushed to
 // fp64 (global, per CTA run slot) every `window` tiles.
-// Warp roles: 0 = TMA producer, 1 = MMA issuer (+ TMEM owner), 2 = TMA storer, 3 = spare,
+// Warp roles: 0 = TMA producer, 1 = GEMM1 issuer (+ TMEM owner), 2 = TMA storer, 3 = GEMM2 issuer,
 // 4..7 / 8..11 = two epilogue warpgroups that take alternate tiles (ping-pong).
 // Persistent: CTA g owns tiles [g T / G, (g+1) T / G) of the row-major (row block, column
 // tile) order, like the SIMT pass.
@@ -160,66 +160,71 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 bulk_load(st + o_y, p.yv + c.cb * TBN, TBN * 4, fb, pol_keep);
             }
         }
-    } else if (warp == 1) {
-        // ============================================================ MMA issuer (whole warp, convergent;
-        // elect.sync inside the tcgen05 wrappers picks the issuing lane)
-        {
+    } else if (warp == 1 || warp == 3) {
+        // ============================================================ MMA issuers (whole warp, convergent;
+        // elect.sync inside the tcgen05 wrappers picks the issuing lane).  Warp 1 issues GEMM1
+        // (S' into D1), warp 3 issues GEMM2 (Theta X into D2): the two accumulators are
+        // independent, so the issue streams run in parallel.
+        const uint32_t tmu = __shfl_sync(0xffffffffu, tmem, 0);   // warp-uniform copies
+        const uint32_t sbase = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+        if (warp == 1) {
             const uint32_t id1 = idesc_tf32(TBM, TBN, 0, 0);   // A K-major (TMEM), B K-major
-            const uint32_t id2 = idesc_tf32(TBM, NP2, 0, 0);
-            int run = 0, flushes = 0;
-            bool window_start = true;
-            auto gemm1 = [&](const Cursor &c) {
+            int run = 0;
+            for (Cursor c = start(); c.u < U; adv(c, 1)) {
                 const int b = c.u & 1;
                 if (lane == 0) TC_TRACE(1, c.u, 0);
+                if (run_start(c)) {                          // Xi' of this run loaded into TMEM
+                    mbar_wait(&bar->xi_full, (uint32_t)(run & 1));
+                    ++run;
+                }
                 mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
                 mbar_wait(&bar->d1_empty[b], (uint32_t)(((c.u >> 1) & 1) ^ 1));
                 if (lane == 0) TC_TRACE(1, c.u, 1);
                 tc_fence_after();
-                const uint8_t *xh = stage_ptr(c.s) + o_g1;
-                const uint32_t d = tmem + c_d1 + (uint32_t)b * TBN;
+                const uint32_t xh = sbase + (uint32_t)c.s * stage_bytes + o_g1;
+                const uint32_t d = tmu + c_d1 + (uint32_t)b * TBN;
+                // K-major interleave: 4-k chunks LBO = 512 B apart, 8-row j groups SBO = 128 B;
+                // K-step kk advances the start address by 1024 B (= 64 in the >>4 address field)
+                const uint64_t bh = smem_desc_u32(xh, 512, 128, 0), bl = smem_desc_u32(xh + g1_bytes, 512, 128, 0);
 #pragma unroll
                 for (int pass = 0; pass < 3; ++pass) {
-                    const uint8_t *xb = pass == 1 ? xh + g1_bytes : xh;
-                    const uint32_t a_col = c_xi + (pass == 2 ? (uint32_t)NK : 0u);
+                    const uint64_t bd0 = pass == 1 ? bl : bh;
+                    const uint32_t a0 = tmu + c_xi + (pass == 2 ? (uint32_t)NK : 0u);
 #pragma unroll
-                    for (int kk = 0; kk < NK / 8; ++kk) {
-                        // K-major interleave: 4-k chunks LBO = 512 B apart, 8-row j groups SBO = 128 B
-                        const uint64_t bd = smem_desc(xb + kk * 1024, 512, 128, 0);
-                        mma_tf32_ts_warp(d, tmem + a_col + (uint32_t)kk * 8, bd, id1, (pass | kk) != 0);
-                    }
+                    for (int kk = 0; kk < NK / 8; ++kk)
+                        mma_tf32_ts_warp(d, a0 + (uint32_t)kk * 8, bd0 + (uint64_t)(kk * 64), id1, (pass | kk) != 0);
                 }
                 mma_commit_warp(&bar->d1_full[b]);
                 if (lane == 0) TC_TRACE(1, c.u, 2);
-            };
-            mbar_wait(&bar->xi_full, 0);
-            tc_fence_after();
-            Cursor c = start();
-            gemm1(c);
-            for (; c.u < U; adv(c, 1)) {
-                Cursor n = c;
-                adv(n, 1);
-                const bool next_same_run = (n.u < U) && n.cb != 0;
-                if (next_same_run) gemm1(n);
+            }
+        } else {
+            const uint32_t id2 = idesc_tf32(TBM, NP2, 0, 0);
+            int flushes = 0;
+            bool window_start = true;
+            for (Cursor c = start(); c.u < U; adv(c, 1)) {
                 const int a = c.u & 1;
                 if (lane == 0) TC_TRACE(1, c.u, 3);
                 mbar_wait(&bar->at_full[a], (uint32_t)((c.u >> 1) & 1));
                 if (window_start && flushes > 0) mbar_wait(&bar->d2_empty, (uint32_t)((flushes - 1) & 1));
                 if (lane == 0) TC_TRACE(1, c.u, 4);
                 tc_fence_after();
-                const uint8_t *xh = stage_ptr(c.s) + o_g2;
+                const uint32_t xh = sbase + (uint32_t)c.s * stage_bytes + o_g2;
+                // X^T image, K-major interleave: 4-j chunks lbo2 apart, 8-row d groups 128 B;
+                // K-step jj (8 j) advances the start address by 2 lbo2 bytes
+                const uint64_t bh = smem_desc_u32(xh, lbo2, 128, 0), bl = smem_desc_u32(xh + g2_bytes, lbo2, 128, 0);
+                const uint32_t ws = window_start ? 1u : 0u;
 #pragma unroll
                 for (int pass = 0; pass < 3; ++pass) {
-                    const uint8_t *xb = pass == 1 ? xh + g2_bytes : xh;
-                    const uint32_t a_col = c_at + (uint32_t)a * 64 + (pass == 2 ? 32u : 0u);
+                    const uint64_t bd0 = pass == 1 ? bl : bh;
+                    const uint32_t a0 = tmu + c_at + (uint32_t)a * 64 + (pass == 2 ? 32u : 0u);
 #pragma unroll
-                    for (int jj = 0; jj < TBN / 8; ++jj) {
-                        // X^T image, K-major interleave: 4-j chunks lbo2 apart, 8-row d groups 128 B
-                        const uint64_t bd = smem_desc(xb + jj * 2 * lbo2, lbo2, 128, 0);
-                        mma_tf32_ts_warp(tmem + c_d2, tmem + a_col + (uint32_t)jj * 8, bd, id2,
-                                         !(window_start && pass == 0 && jj == 0));
-                    }
+                    for (int jj = 0; jj < TBN / 8; ++jj)
+                        mma_tf32_ts_warp(tmu + c_d2, a0 + (uint32_t)jj * 8, bd0 + (uint64_t)(jj * 2 * lbo2 / 16), id2,
+                                         (pass | jj) != 0 ? 1u : (ws ^ 1u));
                 }
                 mma_commit_warp(&bar->at_empty[a]);
+                // GEMM1 of this tile completed before the epilogue released at_full, so the
+                // stage's X images are no longer read once GEMM2 is done
                 mma_commit_warp(&bar->empty[c.s]);
                 if (lane == 0) TC_TRACE(1, c.u, 5);
                 window_start = false;
@@ -227,12 +232,6 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     mma_commit_warp(&bar->d2_full);
                     ++flushes;
                     window_start = true;
-                }
-                if (n.u < U && !next_same_run) {
-                    ++run;
-                    mbar_wait(&bar->xi_full, (uint32_t)(run & 1));
-                    tc_fence_after();
-                    gemm1(n);
                 }
             }
         }

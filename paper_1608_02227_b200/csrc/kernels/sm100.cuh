@@ -193,6 +193,15 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn_major, 
 
 // Shared-memory matrix descriptor (cute::UMMA::SmemDescriptor layout), version 1 (sm100).
 // layout: 2 = SWIZZLE_128B.  lbo/sbo in bytes.
+__device__ __forceinline__ uint64_t smem_desc_u32(uint32_t a, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
+    uint64_t d = 0;
+    d |= (uint64_t)((a >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1u << 46;                   // version
+    d |= (uint64_t)(layout & 7u) << 61;
+    return d;
+}
 __device__ __forceinline__ uint64_t smem_desc(const void *smem, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
     const uint32_t a = smem_u32(smem);
     uint64_t d = 0;

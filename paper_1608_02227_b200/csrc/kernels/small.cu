@@ -102,28 +102,27 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
             p.c_out[j] = s;
         }
     } else {
-        const int64_t g = (int64_t)(blockIdx.x - ncolb) * blockDim.x + threadIdx.x;
-        if (g < p.Ns * (p.n + 1)) {
-            const int64_t i = g / (p.n + 1);
-            const int d = (int)(g % (p.n + 1));
-            const int rb = (int)(i / p.rbm), ii = (int)(i % p.rbm);
-            double s = 0.0;
-            for (int e = p.rb_ptr[rb]; e < p.rb_ptr[rb + 1]; ++e) {
-                double *row = const_cast<double *>(p.rowpart) + ((int64_t)p.rb_slots[e] * p.rbm + ii) * p.NBP;
-                if (d < p.n) {
-                    s += row[d];
-                    row[d] = 0.0;
-                } else {
-                    s += row[p.rcol0];
-                    row[p.rcol0] = 0.0;
-                    if (p.rcol1 >= 0) {
+        // one warp per row, lanes over d <= n (32-bit index math: Ns < 2^31)
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int i = (int)(blockIdx.x - ncolb) * 8 + warp;
+        if (i < p.Ns) {
+            const int rb = i / p.rbm, ii = i - rb * p.rbm;
+            const int e0 = p.rb_ptr[rb], e1 = p.rb_ptr[rb + 1];
+            for (int d = lane; d <= p.n; d += 32) {
+                const int col = d < p.n ? d : p.rcol0;
+                double s = 0.0;
+                for (int e = e0; e < e1; ++e) {
+                    double *row = const_cast<double *>(p.rowpart) + ((int64_t)p.rb_slots[e] * p.rbm + ii) * p.NBP;
+                    s += row[col];
+                    row[col] = 0.0;
+                    if (d == p.n && p.rcol1 >= 0) {
                         s += row[p.rcol1];
                         row[p.rcol1] = 0.0;
                     }
                 }
+                if (d < p.n) p.P[(int64_t)i * p.n + d] = s;
+                else p.r[i] = s;
             }
-            if (d < p.n) p.P[i * p.n + d] = s;
-            else p.r[i] = s;
         }
     }
     if (p.advance_t && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -253,7 +252,7 @@ cudaError_t launch_prologue(const SmallParams &p, int fp64, cudaStream_t s, int 
 
 cudaError_t launch_reduce(const ReduceParams &p, int fp64, cudaStream_t s) {
     const int ncolb = (int)((p.N + 31) / 32);
-    const int64_t nrowb = (p.Ns * (p.n + 1) + 255) / 256;
+    const int64_t nrowb = (p.Ns + 7) / 8;
     const unsigned nb = (unsigned)(ncolb + nrowb);
     if (fp64) reduce_kernel<double><<<nb, 256, 0, s>>>(p, ncolb);
     else reduce_kernel<float><<<nb, 256, 0, s>>>(p, ncolb);
