@@ -38,7 +38,10 @@ constexpr uint32_t TILE_BYTES = TBM * TBN * 4;     // 16 KB
 
 struct __align__(8) TcBarriers {
     uint64_t full[kTcMaxStages], empty[kTcMaxStages];
-    uint64_t d1_full[2], d1_empty[2], at_full[2], at_empty[2], st_full[2];
+    // st_full is per stage (not per warpgroup): a stage is refilled only after the storer
+    // released it, so no arrival can run two phases ahead of the storer's parity wait
+    uint64_t st_full[kTcMaxStages];
+    uint64_t d1_full[2], d1_empty[2], at_full[2], at_empty[2];
     uint64_t d2_full, d2_empty, xi_full;
     uint32_t tmem_base;
 };
@@ -120,11 +123,14 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) { mbar_init(&bar->full[s], 1); mbar_init(&bar->empty[s], 2); }
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&bar->full[s], 1);
+            mbar_init(&bar->empty[s], 2);
+            mbar_init(&bar->st_full[s], 4);
+        }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&bar->d1_full[b], 1); mbar_init(&bar->d1_empty[b], 4);
             mbar_init(&bar->at_full[b], 4); mbar_init(&bar->at_empty[b], 1);
-            mbar_init(&bar->st_full[b], 4);
         }
         mbar_init(&bar->d2_full, 1);
         mbar_init(&bar->d2_empty, 4);
@@ -241,7 +247,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             const uint64_t pol_stream = policy_evict_first();
             for (Cursor c = start(); c.u < U; adv(c, 1)) {
                 TC_TRACE(2, c.u, 0);
-                mbar_wait(&bar->st_full[c.u & 1], (uint32_t)((c.u >> 1) & 1));
+                mbar_wait(&bar->st_full[c.s], (uint32_t)c.ph);
                 TC_TRACE(2, c.u, 1);
                 tma_store_2d(&tmB2, c.cb * TBN, c.rb * TBM, stage_ptr(c.s) + TILE_BYTES, pol_stream);
                 bulk_commit();
@@ -431,7 +437,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             }
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar->st_full[wg]);
+            if (lane == 0) mbar_arrive(&bar->st_full[c.s]);
             rrun += (double)rtile;
             named_barrier(1 + wg, 128);
             if (tr) TC_TRACE(3 + wg, c.u, 5);
