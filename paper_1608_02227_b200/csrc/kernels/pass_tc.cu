@@ -65,10 +65,11 @@ __device__ __forceinline__ void bfly(const float *v, float *o, int lane) {
     }
 }
 
-// Position of tile u within a CTA's contiguous tile range: row block, column tile, and the
-// stage slot / phase parity of the smem ring (all maintained incrementally: no divisions).
+// Position of the u-th tile a CTA processes: segment k of its schedule (a row block rb and a
+// column-tile range [cbb, cbe)), column tile cb, and the stage slot / phase parity of the smem
+// ring (all maintained incrementally: no divisions).
 struct Cursor {
-    int u, rb, cb, s, ph;
+    int u, k, rb, cb, cbb, cbe, s, ph;
 };
 
 // debug timeline (p.trace != nullptr): clock64 of role events for the first 256 tiles of CTA 0
@@ -102,25 +103,42 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     constexpr uint32_t g1_bytes = (uint32_t)NK * 128, g2_bytes = (uint32_t)NP2 * 128;
     constexpr uint32_t o_g1 = 2 * TILE_BYTES, o_g2 = o_g1 + 2 * g1_bytes, o_y = o_g2 + 2 * g2_bytes;
     constexpr uint32_t lbo2 = (uint32_t)NP2 * 16;      // X^T image: K-chunk (4 j) stride
-    const int rb0 = t0 / nCB, cb0 = t0 - rb0 * nCB;
     const int slot0 = p.cta_slot0[blockIdx.x];
+    // Schedule.  The CTA owns the contiguous tiles [t0, t1) of the row-major (row block, column
+    // tile) order: possibly a partial head row block, full row blocks, a partial tail row block.
+    // It processes the FULL row blocks first (each swept from column tile 0), then the tail, then
+    // the head: all CTAs then sweep the column tiles in near lockstep, so the per-column-tile X
+    // operand images they stream are shared through L2 instead of being re-read from HBM.
+    const int rbA = t0 / nCB, cbA = t0 - rbA * nCB;
+    const int rbZ = (t1 - 1) / nCB, cbZ = (t1 - 1) - rbZ * nCB + 1;
+    const bool single = rbA == rbZ;
+    const bool hp = !single && cbA > 0, tp = !single && cbZ < nCB;
+    const int full0 = hp ? rbA + 1 : rbA, nfull = single ? 0 : (tp ? rbZ - 1 : rbZ) - full0 + 1;
+    const int nseg = single ? 1 : nfull + (tp ? 1 : 0) + (hp ? 1 : 0);
+    auto seg = [&](Cursor &c) {             // load segment c.k into the cursor
+        if (single) { c.rb = rbA; c.cbb = cbA; c.cbe = cbZ; }
+        else if (c.k < nfull) { c.rb = full0 + c.k; c.cbb = 0; c.cbe = nCB; }
+        else if (c.k == nfull && tp) { c.rb = rbZ; c.cbb = 0; c.cbe = cbZ; }
+        else { c.rb = rbA; c.cbb = cbA; c.cbe = nCB; }
+        c.cb = c.cbb;
+    };
 
     auto stage_ptr = [&](int s) { return smem + (size_t)s * stage_bytes; };
     auto adv = [&](Cursor &c, int k) {
-        c.u += k;
-        c.cb += k;
-        while (c.cb >= nCB) { c.cb -= nCB; ++c.rb; }
-        c.s += k;
-        while (c.s >= S) { c.s -= S; c.ph ^= 1; }
+        for (int i = 0; i < k; ++i) {
+            ++c.u;
+            if (++c.cb == c.cbe && ++c.k < nseg) seg(c);
+            if (++c.s == S) { c.s = 0; c.ph ^= 1; }
+        }
     };
-    auto start = [&]() { return Cursor{0, rb0, cb0, 0, 0}; };
-    auto run_start = [&](const Cursor &c) { return c.u == 0 || c.cb == 0; };
-    auto run_end = [&](const Cursor &c) { return c.u + 1 == U || c.cb + 1 == nCB; };
-    auto flush_after = [&](const Cursor &c) {
-        if (run_end(c)) return true;
-        const int rs = c.rb * nCB > t0 ? c.rb * nCB : t0;          // first tile of this run
-        return ((t0 + c.u - rs + 1) & wmask) == 0;
+    auto start = [&]() {
+        Cursor c{0, 0, 0, 0, 0, 0, 0, 0};
+        seg(c);
+        return c;
     };
+    auto run_start = [&](const Cursor &c) { return c.cb == c.cbb; };
+    auto run_end = [&](const Cursor &c) { return c.cb + 1 == c.cbe; };
+    auto flush_after = [&](const Cursor &c) { return run_end(c) || ((c.cb - c.cbb + 1) & wmask) == 0; };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -297,7 +315,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         auto flush = [&](const Cursor &c) {
             mbar_wait(&bar->d2_full, (uint32_t)(flushes & 1));
             tc_fence_after();
-            const int sl = slot0 + (c.rb - rb0);
+            const int sl = slot0 + (c.rb - rbA);
             const bool first = sl != last_flush_slot;
             last_flush_slot = sl;
             double *dst = p.rowpart + ((int64_t)sl * TBM + r) * W;
@@ -321,7 +339,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
 
         Cursor c = start();
         if (wg == 1) adv(c, 1);
-        if (wg == 0) load_xi(rb0);
+        if (wg == 0) load_xi(c.rb);
         const bool tr = (q == 0 && lane == 0);
         for (; c.u < U; adv(c, 2)) {
             const int b = c.u & 1;
@@ -450,7 +468,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             Cursor n2 = c;
             adv(n2, 2);
             if (n2.u >= U || n2.rb != rb) {
-                p.rowpart[((int64_t)(slot0 + rb - rb0) * TBM + r) * W + NP2 + wg] = rrun;
+                p.rowpart[((int64_t)(slot0 + rb - rbA) * TBM + r) * W + NP2 + wg] = rrun;
                 rrun = 0.0;
             }
             // ---- Theta X flushes (warpgroup 0 handles those after tiles u and u+1)
