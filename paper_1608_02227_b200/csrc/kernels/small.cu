@@ -107,21 +107,41 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
         const int i = (int)(blockIdx.x - ncolb) * 8 + warp;
         if (i < p.Ns) {
             const int rb = i / p.rbm, ii = i - rb * p.rbm;
-            const int e0 = p.rb_ptr[rb], e1 = p.rb_ptr[rb + 1];
-            for (int d = lane; d <= p.n; d += 32) {
-                const int col = d < p.n ? d : p.rcol0;
-                double s = 0.0;
-                for (int e = e0; e < e1; ++e) {
-                    double *row = const_cast<double *>(p.rowpart) + ((int64_t)p.rb_slots[e] * p.rbm + ii) * p.NBP;
-                    s += row[col];
-                    row[col] = 0.0;
-                    if (d == p.n && p.rcol1 >= 0) {
-                        s += row[p.rcol1];
-                        row[p.rcol1] = 0.0;
+            const int e0 = p.rb_ptr[rb], ns = p.rb_ptr[rb + 1] - e0;
+            double *rp = const_cast<double *>(p.rowpart);
+            // slot ids loaded cooperatively (one per lane), then broadcast; all of a row's partial
+            // loads are issued before the fixed-order sum (latency: one round trip, not ns)
+            for (int base = 0; base < ns; base += 32) {
+                const int m = min(32, ns - base);
+                const int my = lane < m ? p.rb_slots[e0 + base + lane] : 0;
+                for (int d = lane; d <= p.n; d += 32) {
+                    const int col = d < p.n ? d : p.rcol0;
+                    const bool two = d == p.n && p.rcol1 >= 0;
+                    double s = base == 0 ? 0.0 : (d < p.n ? p.P[(int64_t)i * p.n + d] : p.r[i]);
+                    for (int q0 = 0; q0 < m; q0 += 4) {
+                        double v[4], w[4];
+                        double *rows[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {           // 4 independent loads in flight
+                            const int sl = __shfl_sync(0xffffffffu, my, (q0 + k) & 31);
+                            rows[k] = rp + ((int64_t)sl * p.rbm + ii) * p.NBP;
+                            const bool ok = q0 + k < m;
+                            v[k] = ok ? rows[k][col] : 0.0;
+                            w[k] = (ok && two) ? rows[k][p.rcol1] : 0.0;
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (q0 + k < m) {
+                                s += v[k];
+                                if (two) s += w[k];
+                                rows[k][col] = 0.0;
+                                if (two) rows[k][p.rcol1] = 0.0;
+                            }
+                        }
                     }
+                    if (d < p.n) p.P[(int64_t)i * p.n + d] = s;
+                    else p.r[i] = s;
                 }
-                if (d < p.n) p.P[(int64_t)i * p.n + d] = s;
-                else p.r[i] = s;
             }
         }
     }
