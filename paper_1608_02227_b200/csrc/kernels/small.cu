@@ -109,11 +109,11 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
             const int rb = i / p.rbm, ii = i - rb * p.rbm;
             const int e0 = p.rb_ptr[rb], ns = p.rb_ptr[rb + 1] - e0;
             double *rp = const_cast<double *>(p.rowpart);
-            // slot ids loaded cooperatively (one per lane), then broadcast; all of a row's partial
-            // loads are issued before the fixed-order sum (latency: one round trip, not ns)
+            // the row's partial loads are issued 4 at a time before the fixed-order sum
+            // (slot ids are broadcast loads: every lane reads the same address)
             for (int base = 0; base < ns; base += 32) {
                 const int m = min(32, ns - base);
-                const int my = lane < m ? p.rb_slots[e0 + base + lane] : 0;
+                const int *ids = p.rb_slots + e0 + base;
                 for (int d = lane; d <= p.n; d += 32) {
                     const int col = d < p.n ? d : p.rcol0;
                     const bool two = d == p.n && p.rcol1 >= 0;
@@ -123,9 +123,9 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
                         double *rows[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {           // 4 independent loads in flight
-                            const int sl = __shfl_sync(0xffffffffu, my, (q0 + k) & 31);
-                            rows[k] = rp + ((int64_t)sl * p.rbm + ii) * p.NBP;
                             const bool ok = q0 + k < m;
+                            const int sl = ok ? ids[q0 + k] : 0;
+                            rows[k] = rp + ((int64_t)sl * p.rbm + ii) * p.NBP;
                             v[k] = ok ? rows[k][col] : 0.0;
                             w[k] = (ok && two) ? rows[k][p.rcol1] : 0.0;
                         }
