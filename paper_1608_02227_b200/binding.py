@@ -131,6 +131,26 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def shard_range(N: int, rank: int, world: int):
+    """Rows [row0, row0 + rows) of Theta owned by `rank` (include/cr.h: S = ceil(N/world))."""
+    S = -(-int(N) // int(world))
+    row0 = min(int(N), int(rank) * S)
+    return row0, min(int(N), row0 + S) - row0
+
+
+def broadcast_unique_id(group, device=None) -> bytes:
+    """Rank 0 of `group` draws a 128-byte ncclUniqueId (cr_nccl_get_unique_id) and broadcasts it
+    over torch.distributed (CPU tensor for gloo, `device` tensor for nccl)."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    raw = nccl_unique_id() if rank == 0 else bytes(128)
+    bdev = device if (device is not None and dist.get_backend(group) == "nccl") else torch.device("cpu")
+    t = torch.tensor(list(raw), dtype=torch.uint8, device=bdev)
+    dist.broadcast(t, src=dist.get_global_rank(group, 0), group=group)
+    return bytes(t.cpu().tolist())
+
+
 class Solver:
     """One rank's share of the smoothed-dual P-APG solve (Fig. 2).
 
@@ -159,15 +179,9 @@ class Solver:
             self.world = dist.get_world_size(group)
             self.rank = dist.get_rank(group)
             if self.world > 1:
-                raw = nccl_unique_id() if self.rank == 0 else bytes(128)
-                bdev = dev if dist.get_backend(group) == "nccl" else torch.device("cpu")
-                t = torch.tensor(list(raw), dtype=torch.uint8, device=bdev)
-                dist.broadcast(t, src=dist.get_global_rank(group, 0), group=group)
-                uid = (C.c_char * 128).from_buffer_copy(bytes(t.cpu().tolist()))
+                uid = (C.c_char * 128).from_buffer_copy(broadcast_unique_id(group, dev))
         self._uid = uid
-        S = -(-self.N // self.world)
-        self.row0 = min(self.N, self.rank * S)
-        self.rows = min(self.N, self.row0 + S) - self.row0
+        self.row0, self.rows = shard_range(self.N, self.rank, self.world)
         nbytes = workspace_size(self.N, self.n, prec, kernel, self.rank, self.world)
         if nbytes == 0:
             raise CrError(f"unsupported shape/precision: N={self.N} n={self.n} prec={prec} kernel={kernel}")
