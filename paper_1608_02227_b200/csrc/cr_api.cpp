@@ -204,8 +204,7 @@ struct cr_ctx {
     cudaStream_t cap_stream = nullptr;   // private stream used only to record graphs
     // tensor-core pass
     CUtensorMap tm[2];
-    int G_tc = 0, stages = 0, window = 64, smem_tc = 0;
-    uint32_t stage_bytes = 0;
+    int G_tc = 0, stages = 0, g1stages = 0, g2stages = 0, window = 64, smem_tc = 0;
     int64_t T_tc = 0;
     unsigned long long *trace = nullptr;   // debug timeline buffer (CR_TC_TRACE=<file>)
     ncclComm_t comm = nullptr;
@@ -341,7 +340,8 @@ TcParams tc_params(cr_ctx *ctx) {
     p.NP2 = Ly.NP2;
     p.stages = ctx->stages;
     p.window = ctx->window;
-    p.stage_bytes = ctx->stage_bytes;
+    p.g1stages = ctx->g1stages;
+    p.g2stages = ctx->g2stages;
     p.smem_bytes = ctx->smem_tc;
     p.g1_hi = ctx->at<float>(Ly.g1h);
     p.g1_lo = ctx->at<float>(Ly.g1l);
@@ -656,12 +656,33 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         // tcgen05 pass: one persistent CTA per SM (512 TMEM columns, ~200 KB smem each)
         ctx->T_tc = (int64_t)Ly.nRBtc * Ly.nCBtc;
         ctx->G_tc = (int)std::min<int64_t>({ctx->T_tc, (int64_t)nsm, (int64_t)kGMax});
-        ctx->stage_bytes = (uint32_t)((2 * kTcBM * kTcBN * 4 + 2 * Ly.NK * 128 + 2 * Ly.NP2 * 128 + kTcBN * 4 + 1023) / 1024 * 1024);
+        // Theta ring: 32 KB slots (B1, B2 tiles, 1024-B aligned for the 128-B swizzle); X_J and
+        // X_J^T image rings (hi + lo per slot).  Defaults: 4 Theta slots and 3 + 3 image slots,
+        // reduced (images first, not below 2) until they fit.  CR_TC_STAGES / CR_TC_G1STAGES /
+        // CR_TC_G2STAGES override.
+        const size_t tb = 2 * (size_t)kTcBM * kTcBN * 4, b1 = 2 * (size_t)Ly.NK * 128, b2 = 2 * (size_t)Ly.NP2 * 128;
         const size_t fixed = tc_barrier_bytes() + 1024 + 64;
-        const size_t budget = 227 * 1024;
-        ctx->stages = (int)std::min<size_t>(kTcMaxStages, (budget - fixed) / ctx->stage_bytes);
-        if (ctx->stages < 2) { fail(ctx, CR_ERR_UNSUPPORTED, "tc pass: smem"); return bail(CR_ERR_UNSUPPORTED); }
-        ctx->smem_tc = (int)(ctx->stages * (size_t)ctx->stage_bytes + fixed);
+        const size_t budget = 227 * 1024 - fixed;
+        auto env_int = [](const char *k, int d) {
+            const char *e = std::getenv(k);
+            return e ? std::max(2, std::min(kTcMaxStages, std::atoi(e))) : d;
+        };
+        int st = env_int("CR_TC_STAGES", 4), s1 = env_int("CR_TC_G1STAGES", 3), s2 = env_int("CR_TC_G2STAGES", 3);
+        auto bytes = [&]() { return st * tb + s1 * b1 + s2 * b2; };
+        while (bytes() > budget && (s1 > 2 || s2 > 2)) {
+            if (s1 * b1 >= s2 * b2 && s1 > 2) --s1;
+            else if (s2 > 2) --s2;
+            else --s1;
+        }
+        while (bytes() > budget && st > 2) --st;
+        if (bytes() > budget) {
+            fail(ctx, CR_ERR_UNSUPPORTED, "tc pass: smem");
+            return bail(CR_ERR_UNSUPPORTED);
+        }
+        ctx->stages = st;
+        ctx->g1stages = s1;
+        ctx->g2stages = s2;
+        ctx->smem_tc = (int)(bytes() + fixed);
         IK(pass_tc_prepare(Ly.NK, ctx->smem_tc));
         slot_tables(ctx->G_tc, ctx->T_tc, Ly.nRBtc, Ly.nCBtc, slot0t, rb_ptrt, slotst);
         IK(cudaMemcpyAsync(ctx->ws + Ly.slot0_tc, slot0t.data(), slot0t.size() * 4, cudaMemcpyHostToDevice, ctx->stream));

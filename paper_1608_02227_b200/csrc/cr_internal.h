@@ -111,7 +111,7 @@ cudaError_t launch_stats_finalize(const double *pro, int nb_pro, const double *r
 struct TcParams {
     int64_t N, Ns, row0, ldT, T;
     int G, nCB, NK, NP2, stages, window;
-    uint32_t stage_bytes;
+    int g1stages, g2stages;          // X_J / X_J^T image ring slots
     int smem_bytes;
     const float *g1_hi, *g1_lo;      // [nCB][NK * 32]  X_J  tiles (K-major interleave), tf32 hi / lo
     const float *g2_hi, *g2_lo;      // [nCB][NP2 * 32] X_J^T tiles (K-major interleave), tf32 hi / lo

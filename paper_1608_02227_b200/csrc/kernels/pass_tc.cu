@@ -37,7 +37,9 @@ constexpr int NTHR = 384;       // 12 warps
 constexpr uint32_t TILE_BYTES = TBM * TBN * 4;     // 16 KB
 
 struct __align__(8) TcBarriers {
-    uint64_t full[kTcMaxStages], empty[kTcMaxStages];
+    uint64_t full[kTcMaxStages], empty[kTcMaxStages];      // Theta ring (B1, B2 tiles, y'_J)
+    uint64_t g1full[kTcMaxStages], g1empty[kTcMaxStages];  // X_J image ring (GEMM1 B operand)
+    uint64_t g2full[kTcMaxStages], g2empty[kTcMaxStages];  // X_J^T image ring (GEMM2 B operand)
     // st_full is per stage (not per warpgroup): a stage is refilled only after the storer
     // released it, so no arrival can run two phases ahead of the storer's parity wait
     uint64_t st_full[kTcMaxStages];
@@ -66,10 +68,10 @@ __device__ __forceinline__ void bfly(const float *v, float *o, int lane) {
 }
 
 // Position of the u-th tile a CTA processes: segment k of its schedule (a row block rb and a
-// column-tile range [cbb, cbe)), column tile cb, and the stage slot / phase parity of the smem
-// ring (all maintained incrementally: no divisions).
+// column-tile range [cbb, cbe)), column tile cb, and the slot / phase parity of the Theta ring
+// (s, ph), the X_J ring (x, xph) and the X_J^T ring (z, zph) (all incremental: no divisions).
 struct Cursor {
-    int u, k, rb, cb, cbb, cbe, s, ph;
+    int u, k, rb, cb, cbb, cbe, s, ph, x, xph, z, zph;
 };
 
 // debug timeline (p.trace != nullptr): clock64 of role events for the first 256 tiles of CTA 0
@@ -87,9 +89,20 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     // 1024-byte alignment by offsetting the shared pointer itself (an integer round trip would
     // lose the shared address space and turn every access into a generic LD/ST)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int S = p.stages;
-    const uint32_t stage_bytes = p.stage_bytes;
-    TcBarriers *bar = reinterpret_cast<TcBarriers *>(smem + (size_t)S * stage_bytes);
+    // Three rings, each with its own depth and release point:
+    //   Theta ring, S slots  [B1 16K][B2 16K] (+ y'_J, 128 B, in a side array): HBM stream;
+    //                        released by the storer once Theta^k has left the slot
+    //   X_J ring,   S1 slots [X hi][X lo] (GEMM1 B operand): released when GEMM1 completes
+    //   X_J^T ring, S2 slots [X^T hi][X^T lo] (GEMM2 B operand): released when GEMM2 completes
+    // so the L2-resident operand images never wait on the epilogue of an older tile.
+    const int S = p.stages, S1 = p.g1stages, S2 = p.g2stages;
+    constexpr uint32_t stage_bytes = 2 * TILE_BYTES;
+    // X slot images (hi, lo)
+    constexpr uint32_t g1_bytes = (uint32_t)NK * 128, g2_bytes = (uint32_t)NP2 * 128;
+    uint8_t *g1ring = smem + (size_t)S * stage_bytes;
+    uint8_t *g2ring = g1ring + (size_t)S1 * 2 * g1_bytes;
+    uint8_t *yring = g2ring + (size_t)S2 * 2 * g2_bytes;
+    TcBarriers *bar = reinterpret_cast<TcBarriers *>(yring + (size_t)kTcMaxStages * 128);
     float *colS = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + sizeof(TcBarriers) + 8);  // [2 wg][2][4][32]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -99,9 +112,6 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     const int nCB = p.nCB;
     constexpr int W = NP2 + 2;
     const int wmask = p.window - 1;                    // flush window (power of two)
-    // stage image: [B1 16K][B2 16K][X hi][X lo][X^T hi][X^T lo][y' 128 B]
-    constexpr uint32_t g1_bytes = (uint32_t)NK * 128, g2_bytes = (uint32_t)NP2 * 128;
-    constexpr uint32_t o_g1 = 2 * TILE_BYTES, o_g2 = o_g1 + 2 * g1_bytes, o_y = o_g2 + 2 * g2_bytes;
     constexpr uint32_t lbo2 = (uint32_t)NP2 * 16;      // X^T image: K-chunk (4 j) stride
     const int slot0 = p.cta_slot0[blockIdx.x];
     // Schedule.  The CTA owns the contiguous tiles [t0, t1) of the row-major (row block, column
@@ -129,10 +139,12 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             ++c.u;
             if (++c.cb == c.cbe && ++c.k < nseg) seg(c);
             if (++c.s == S) { c.s = 0; c.ph ^= 1; }
+            if (++c.x == S1) { c.x = 0; c.xph ^= 1; }
+            if (++c.z == S2) { c.z = 0; c.zph ^= 1; }
         }
     };
     auto start = [&]() {
-        Cursor c{0, 0, 0, 0, 0, 0, 0, 0};
+        Cursor c{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         seg(c);
         return c;
     };
@@ -143,8 +155,16 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&bar->full[s], 1);
-            mbar_init(&bar->empty[s], 2);
+            mbar_init(&bar->empty[s], 1);           // storer: Theta^k left the slot
             mbar_init(&bar->st_full[s], 4);
+        }
+        for (int x = 0; x < S1; ++x) {
+            mbar_init(&bar->g1full[x], 1);
+            mbar_init(&bar->g1empty[x], 1);         // GEMM1 commit
+        }
+        for (int z = 0; z < S2; ++z) {
+            mbar_init(&bar->g2full[z], 1);
+            mbar_init(&bar->g2empty[z], 1);         // GEMM2 commit
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&bar->d1_full[b], 1); mbar_init(&bar->d1_empty[b], 4);
@@ -166,22 +186,40 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
 
     if (warp == 0) {
         // ============================================================ TMA producer
+        // One thread feeds the three rings, polling their free-slot barriers without blocking:
+        // each ring's loads go out as soon as its next slot is released.
         if (lane == 0) {
             const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-            for (Cursor c = start(); c.u < U; adv(c, 1)) {
-                TC_TRACE(0, c.u, 0);
-                mbar_wait(&bar->empty[c.s], (uint32_t)(c.ph ^ 1));
-                TC_TRACE(0, c.u, 1);
-                uint8_t *st = stage_ptr(c.s);
-                uint64_t *fb = &bar->full[c.s];
-                mbar_arrive_expect_tx(fb, 2 * TILE_BYTES + 2 * g1_bytes + 2 * g2_bytes + TBN * 4);
-                tma_load_2d(st, &tmB1, c.cb * TBN, c.rb * TBM, fb, pol_stream);
-                tma_load_2d(st + TILE_BYTES, &tmB2, c.cb * TBN, c.rb * TBM, fb, pol_stream);
-                bulk_load(st + o_g1, p.g1_hi + (size_t)c.cb * NK * 32, g1_bytes, fb, pol_keep);
-                bulk_load(st + o_g1 + g1_bytes, p.g1_lo + (size_t)c.cb * NK * 32, g1_bytes, fb, pol_keep);
-                bulk_load(st + o_g2, p.g2_hi + (size_t)c.cb * NP2 * 32, g2_bytes, fb, pol_keep);
-                bulk_load(st + o_g2 + g2_bytes, p.g2_lo + (size_t)c.cb * NP2 * 32, g2_bytes, fb, pol_keep);
-                bulk_load(st + o_y, p.yv + c.cb * TBN, TBN * 4, fb, pol_keep);
+            Cursor c = start(), c1 = start(), c2 = start();
+            while (c.u < U || c1.u < U || c2.u < U) {
+                if (c.u < U && mbar_test(&bar->empty[c.s], (uint32_t)(c.ph ^ 1))) {
+                    TC_TRACE(0, c.u, 1);
+                    uint8_t *st = stage_ptr(c.s);
+                    uint64_t *fb = &bar->full[c.s];
+                    mbar_arrive_expect_tx(fb, 2 * TILE_BYTES + TBN * 4);
+                    tma_load_2d(st, &tmB1, c.cb * TBN, c.rb * TBM, fb, pol_stream);
+                    tma_load_2d(st + TILE_BYTES, &tmB2, c.cb * TBN, c.rb * TBM, fb, pol_stream);
+                    bulk_load(yring + c.s * 128, p.yv + c.cb * TBN, TBN * 4, fb, pol_keep);
+                    adv(c, 1);
+                }
+                if (c1.u < U && mbar_test(&bar->g1empty[c1.x], (uint32_t)(c1.xph ^ 1))) {
+                    TC_TRACE(0, c1.u, 2);
+                    uint8_t *xs = g1ring + (size_t)c1.x * 2 * g1_bytes;
+                    uint64_t *fb = &bar->g1full[c1.x];
+                    mbar_arrive_expect_tx(fb, 2 * g1_bytes);
+                    bulk_load(xs, p.g1_hi + (size_t)c1.cb * NK * 32, g1_bytes, fb, pol_keep);
+                    bulk_load(xs + g1_bytes, p.g1_lo + (size_t)c1.cb * NK * 32, g1_bytes, fb, pol_keep);
+                    adv(c1, 1);
+                }
+                if (c2.u < U && mbar_test(&bar->g2empty[c2.z], (uint32_t)(c2.zph ^ 1))) {
+                    TC_TRACE(0, c2.u, 3);
+                    uint8_t *xs = g2ring + (size_t)c2.z * 2 * g2_bytes;
+                    uint64_t *fb = &bar->g2full[c2.z];
+                    mbar_arrive_expect_tx(fb, 2 * g2_bytes);
+                    bulk_load(xs, p.g2_hi + (size_t)c2.cb * NP2 * 32, g2_bytes, fb, pol_keep);
+                    bulk_load(xs + g2_bytes, p.g2_lo + (size_t)c2.cb * NP2 * 32, g2_bytes, fb, pol_keep);
+                    adv(c2, 1);
+                }
             }
         }
     } else if (warp == 1 || warp == 3) {
@@ -190,7 +228,8 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         // (S' into D1), warp 3 issues GEMM2 (Theta X into D2): the two accumulators are
         // independent, so the issue streams run in parallel.
         const uint32_t tmu = __shfl_sync(0xffffffffu, tmem, 0);   // warp-uniform copies
-        const uint32_t sbase = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+        const uint32_t g1base = __shfl_sync(0xffffffffu, smem_u32(g1ring), 0);
+        const uint32_t g2base = __shfl_sync(0xffffffffu, smem_u32(g2ring), 0);
         if (warp == 1) {
             const uint32_t id1 = idesc_tf32(TBM, TBN, 0, 0);   // A K-major (TMEM), B K-major
             int run = 0;
@@ -201,11 +240,16 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     mbar_wait(&bar->xi_full, (uint32_t)(run & 1));
                     ++run;
                 }
+                mbar_wait(&bar->g1full[c.x], (uint32_t)c.xph);
+                // GEMM1 also waits for the tile's Theta: letting it run ahead of the Theta stream
+                // (it needs only X_J and Xi') faulted the kernel with a 3-slot Theta ring at C4/C5
+                // (cudaErrorLaunchFailure within ~100-500 launches; 4 and 5 slots ran clean) and
+                // buys nothing, since Theta is prefetched S tiles ahead anyway.
                 mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
                 mbar_wait(&bar->d1_empty[b], (uint32_t)(((c.u >> 1) & 1) ^ 1));
                 if (lane == 0) TC_TRACE(1, c.u, 1);
                 tc_fence_after();
-                const uint32_t xh = sbase + (uint32_t)c.s * stage_bytes + o_g1;
+                const uint32_t xh = g1base + (uint32_t)c.x * 2 * g1_bytes;
                 const uint32_t d = tmu + c_d1 + (uint32_t)b * TBN;
                 // K-major interleave: 4-k chunks LBO = 512 B apart, 8-row j groups SBO = 128 B;
                 // K-step kk advances the start address by 1024 B (= 64 in the >>4 address field)
@@ -219,6 +263,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                         mma_tf32_ts_warp(d, a0 + (uint32_t)kk * 8, bd0 + (uint64_t)(kk * 64), id1, (pass | kk) != 0);
                 }
                 mma_commit_warp(&bar->d1_full[b]);
+                mma_commit_warp(&bar->g1empty[c.x]);
                 if (lane == 0) TC_TRACE(1, c.u, 2);
             }
         } else {
@@ -229,10 +274,11 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 const int a = c.u & 1;
                 if (lane == 0) TC_TRACE(1, c.u, 3);
                 mbar_wait(&bar->at_full[a], (uint32_t)((c.u >> 1) & 1));
+                mbar_wait(&bar->g2full[c.z], (uint32_t)c.zph);
                 if (window_start && flushes > 0) mbar_wait(&bar->d2_empty, (uint32_t)((flushes - 1) & 1));
                 if (lane == 0) TC_TRACE(1, c.u, 4);
                 tc_fence_after();
-                const uint32_t xh = sbase + (uint32_t)c.s * stage_bytes + o_g2;
+                const uint32_t xh = g2base + (uint32_t)c.z * 2 * g2_bytes;
                 // X^T image, K-major interleave: 4-j chunks lbo2 apart, 8-row d groups 128 B;
                 // K-step jj (8 j) advances the start address by 2 lbo2 bytes
                 const uint64_t bh = smem_desc_u32(xh, lbo2, 128, 0), bl = smem_desc_u32(xh + g2_bytes, lbo2, 128, 0);
@@ -247,9 +293,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                                          (pass | jj) != 0 ? 1u : (ws ^ 1u));
                 }
                 mma_commit_warp(&bar->at_empty[a]);
-                // GEMM1 of this tile completed before the epilogue released at_full, so the
-                // stage's X images are no longer read once GEMM2 is done
-                mma_commit_warp(&bar->empty[c.s]);
+                mma_commit_warp(&bar->g2empty[c.z]);
                 if (lane == 0) TC_TRACE(1, c.u, 5);
                 window_start = false;
                 if (flush_after(c)) {
@@ -361,7 +405,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             if (tr) TC_TRACE(3 + wg, c.u, 3);
             tc_fence_after();
             uint8_t *st = stage_ptr(c.s);
-            const float *yt = reinterpret_cast<const float *>(st + o_y);
+            const float *yt = reinterpret_cast<const float *>(yring + c.s * 128);
             uint8_t *rowB1 = st + r * 128, *rowB2 = st + TILE_BYTES + r * 128;
             const int64_t j0 = (int64_t)cb * TBN;
             // masks in tile-local 32-bit terms: the diagonal column (if in this tile), the
@@ -535,7 +579,7 @@ cudaError_t pass_tc_prepare(int NK, int smem_bytes) {
     }
 }
 
-size_t tc_barrier_bytes() { return sizeof(TcBarriers) + 8 + 2 * 2 * 4 * 32 * 4; }
+size_t tc_barrier_bytes() { return (size_t)kTcMaxStages * 128 + sizeof(TcBarriers) + 8 + 2 * 2 * 4 * 32 * 4; }
 
 cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,
                              float *g2h, float *g2l, cudaStream_t s) {
