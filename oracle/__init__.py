@@ -9,7 +9,8 @@ arithmetic).
 Contents
 --------
 ``papg_oracle.c`` (loaded here via ctypes)
-    fp64 Fig. 2 iteration with K = N, plain loops + OpenMP over rows.
+    fp64 Fig. 2 iteration (P:377-397) with K = N, plain loops + OpenMP over rows;
+    the adaptive-step variant (Eq. (adaptive-check)) written out literally.
 ``ref.py``
     dense A1/A2/C (Def. A1A2), the exact regularized optimum via the
     NNLS form of the dual, the univariate sorted-slope convex fit
@@ -17,10 +18,10 @@ Contents
     (lischitz)), closed-form dual value.
 
 Parity status per function:
-    oracle_papg, oracle_eta, oracle_stats, oracle_project_rows -- pinned
+    oracle_papg, oracle_eta, oracle_stats, oracle_project_rows, oracle_papg_adaptive -- pinned
     (tests/test_oracle_pins.py); lipschitz(structured) -- pinned against the
     definition form and Lemma 4 closed forms.
 """
 from .core import (  # noqa: F401
-    build_oracle, lib, papg, eta, stats, project_rows, momentum_next, max_threads, extrapolate, state_after,
+    build_oracle, lib, papg, papg_adaptive, eta, stats, project_rows, momentum_next, max_threads, extrapolate, state_after,
 )

@@ -36,7 +36,9 @@ def lib():
         L.oracle_eta.argtypes = [i64, i32, _dp, _dp, d, _dp, _dp, _dp, i32]
         L.oracle_stats.argtypes = [i64, i32, _dp, _dp, d, dpn, _dp, _dp, _dp, i32]
         L.oracle_project_rows.argtypes = [i64, i32, _dp, _dp, _dp, d, _ip, i64, _dp, _dp, i32]
-        for f in (L.oracle_papg, L.oracle_eta, L.oracle_stats, L.oracle_project_rows):
+        L.oracle_papg_adaptive.argtypes = [i64, i32, _dp, _dp, d, d, i64, _dp, _dp, C.POINTER(d), C.POINTER(d),
+                                           _ip, _dp, dpn, dpn, i32, i32]
+        for f in (L.oracle_papg, L.oracle_eta, L.oracle_stats, L.oracle_project_rows, L.oracle_papg_adaptive):
             f.restype = C.c_int
         L.oracle_max_threads.restype = C.c_int
         _lib = L
@@ -76,6 +78,31 @@ def papg(X, ybar, gamma, L, K, Tprev=None, Tt=None, t=1.0, nthreads=0):
     if rc:
         raise MemoryError("oracle_papg allocation failed")
     return dict(Tprev=Tprev, Tt=Tt, t=tt.value, y=y, xi=xi)
+
+
+def papg_adaptive(X, ybar, gamma, s, K, ups=2.0, Tprev=None, Tt=None, t=1.0, max_trials=200, nthreads=0):
+    """K iterations of P-APG with the adaptive step rule of P:400-407 from state
+    (theta^{k-1}, theta~^k, t_k, s_{k-1}); the paper's start is theta^0 = 0, t_1 = 1, s_0 = L.
+
+    Returns dict(Tprev, Tt, t, s, trials (l_k + 1 per iteration), s_hist (s_k), y, xi)."""
+    X = _c64(X)
+    ybar = _c64(ybar)
+    N, n = X.shape
+    Tprev = np.zeros((N, N)) if Tprev is None else _c64(Tprev).copy()
+    Tt = Tprev.copy() if Tt is None else _c64(Tt).copy()
+    y = np.zeros(N)
+    xi = np.zeros((N, n))
+    trials = np.zeros(max(int(K), 1), dtype=np.int64)
+    s_hist = np.zeros(max(int(K), 1))
+    tt, ss = C.c_double(float(t)), C.c_double(float(s))
+    rc = lib().oracle_papg_adaptive(N, n, X, ybar, float(gamma), float(ups), int(K), Tprev, Tt, C.byref(tt),
+                                    C.byref(ss), trials, s_hist, y.ctypes.data, xi.ctypes.data, int(max_trials),
+                                    int(nthreads))
+    if rc == 1:
+        raise MemoryError("oracle_papg_adaptive allocation failed")
+    if rc == 2:
+        raise RuntimeError("adaptive step: no l_k <= max_trials passed Eq. (adaptive-check)")
+    return dict(Tprev=Tprev, Tt=Tt, t=tt.value, s=ss.value, trials=trials[:K], s_hist=s_hist[:K], y=y, xi=xi)
 
 
 def eta(X, ybar, gamma, T, nthreads=0):

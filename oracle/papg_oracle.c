@@ -238,3 +238,121 @@ int oracle_project_rows(int64_t N, int n, const double *X, const double *y, cons
     }
     return 0;
 }
+
+/*
+ * g_gamma(theta) at its Step-1 minimizer (Eq. (g_gamma)):
+ *     g(theta) = 1/2 ||y - ybar||^2 + gamma/2 ||xi||^2 - <theta, C eta(theta)>,
+ * with eta(theta) = (y, xi) from step1().  Pair terms summed in row-block order.
+ */
+static int dual_value(int64_t N, int n, const double *X, const double *ybar, double gamma,
+                      const double *T, const double *y, const double *xi, double *g_out)
+{
+    int64_t nb = (N + ORACLE_RB - 1) / ORACLE_RB;
+    double *gp = (double *)calloc((size_t)nb, sizeof(double));
+    if (!gp) return 1;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; ++b) {
+        int64_t i1 = (b + 1) * ORACLE_RB < N ? (b + 1) * ORACLE_RB : N;
+        double s = 0.0;
+        for (int64_t i = b * ORACLE_RB; i < i1; ++i)
+            for (int64_t j = 0; j < N; ++j)
+                if (j != i) s += T[i * N + j] * pair_residual(n, X, y, xi, i, j);
+        gp[b] = s;
+    }
+    double tc = 0.0, ry = 0.0, rx = 0.0;
+    for (int64_t b = 0; b < nb; ++b) tc += gp[b];
+    for (int64_t i = 0; i < N; ++i) { double u = y[i] - ybar[i]; ry += u * u; }
+    for (int64_t i = 0; i < N * n; ++i) rx += xi[i] * xi[i];
+    *g_out = 0.5 * ry + 0.5 * gamma * rx - tc;
+    free(gp);
+    return 0;
+}
+
+/*
+ * K iterations of P-APG with the paper's adaptive step rule ("PAPG_A"):
+ * Step 2 uses 1/s_k instead of 1/L_gamma, where s_k = s_{k-1} * ups^(l_k - 1) and l_k >= 0
+ * is the smallest integer for which Eq. (adaptive-check) holds:
+ *     g(theta^k) >= g(theta~^k) + <grad g(theta~^k), theta^k - theta~^k>
+ *                   - (s_k/2) ||theta^k - theta~^k||^2,
+ * grad g(theta~^k) = -C eta^k (Eq. (dual gradient) P:370), theta^k = (theta~^k - C eta^k / s_k)_+.
+ * Steps 1, 3, 4 as in oracle_papg.  s_0 = L_gamma is the caller's initial *s.
+ * State in/out as oracle_papg plus *s = s_{k-1} (in) / s_{k+K-1} (out).
+ * trials[k] (nullable) = l_k + 1 (number of Step-2 evaluations), s_hist[k] (nullable) = s_k.
+ * max_trials bounds l_k + 1 (returns 2 if exceeded).
+ */
+int oracle_papg_adaptive(int64_t N, int n, const double *X, const double *ybar, double gamma, double ups,
+                         int64_t K, double *Tprev, double *Tt, double *t, double *s, int64_t *trials,
+                         double *s_hist, double *y_out, double *xi_out, int max_trials, int nthreads)
+{
+    set_threads(nthreads);
+    double *y = (double *)malloc((size_t)N * sizeof(double));
+    double *xi = (double *)malloc((size_t)(N * n) * sizeof(double));
+    double *y2 = (double *)malloc((size_t)N * sizeof(double));
+    double *xi2 = (double *)malloc((size_t)(N * n) * sizeof(double));
+    double *Tn = (double *)malloc((size_t)(N * N) * sizeof(double));
+    int64_t nb = (N + ORACLE_RB - 1) / ORACLE_RB;
+    double *lp = (double *)calloc((size_t)nb, sizeof(double));
+    double *qp = (double *)calloc((size_t)nb, sizeof(double));
+    int rc = 0;
+    if (!y || !xi || !y2 || !xi2 || !Tn || !lp || !qp) { rc = 1; goto done; }
+    for (int64_t k = 0; k < K; ++k) {
+        /* Step 1 at theta~^k and g(theta~^k). */
+        double g_t;
+        if (step1(N, n, X, ybar, gamma, Tt, y, xi) || dual_value(N, n, X, ybar, gamma, Tt, y, xi, &g_t)) {
+            rc = 1; goto done;
+        }
+        const double s_prev = *s;
+        double s_k = 0.0;
+        int l;
+        for (l = 0; l < max_trials; ++l) {
+            s_k = s_prev * pow(ups, (double)l - 1.0);
+            /* Step 2 with step 1/s_k; <grad g(theta~), D> = -sum R D, ||D||^2. */
+            #pragma omp parallel for schedule(dynamic, 1)
+            for (int64_t b = 0; b < nb; ++b) {
+                int64_t i1 = (b + 1) * ORACLE_RB < N ? (b + 1) * ORACLE_RB : N;
+                double lin = 0.0, sq = 0.0;
+                for (int64_t i = b * ORACLE_RB; i < i1; ++i)
+                    for (int64_t j = 0; j < N; ++j) {
+                        double tnew = 0.0, R = 0.0;
+                        if (j != i) {
+                            R = pair_residual(n, X, y, xi, i, j);
+                            double v = Tt[i * N + j] - R / s_k;
+                            tnew = v > 0.0 ? v : 0.0;
+                        }
+                        Tn[i * N + j] = tnew;
+                        double D = tnew - Tt[i * N + j];
+                        lin += -R * D;
+                        sq += D * D;
+                    }
+                lp[b] = lin;
+                qp[b] = sq;
+            }
+            double lin = 0.0, sq = 0.0;
+            for (int64_t b = 0; b < nb; ++b) { lin += lp[b]; sq += qp[b]; }
+            double g_new;
+            if (step1(N, n, X, ybar, gamma, Tn, y2, xi2) ||
+                dual_value(N, n, X, ybar, gamma, Tn, y2, xi2, &g_new)) { rc = 1; goto done; }
+            if (g_new >= g_t + lin - 0.5 * s_k * sq) break;      /* Eq. (adaptive-check) */
+        }
+        if (l == max_trials) { rc = 2; goto done; }
+        if (trials) trials[k] = l + 1;
+        if (s_hist) s_hist[k] = s_k;
+        *s = s_k;
+        /* Steps 3-4. */
+        double tk = *t;
+        double tn = (1.0 + sqrt(1.0 + 4.0 * tk * tk)) / 2.0;
+        double beta = (tk - 1.0) / tn;
+        #pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < N * N; ++e) {
+            double tnew = Tn[e];
+            Tt[e] = tnew + beta * (tnew - Tprev[e]);
+            Tprev[e] = tnew;
+        }
+        *t = tn;
+    }
+    if (y_out) memcpy(y_out, y, (size_t)N * sizeof(double));
+    if (xi_out) memcpy(xi_out, xi, (size_t)(N * n) * sizeof(double));
+done:
+    free(y); free(xi); free(y2); free(xi2); free(Tn); free(lp); free(qp);
+    return rc;
+}

@@ -342,3 +342,96 @@ def test_config_generators_are_seeded_and_fp32_rounded():
     assert np.all(X1.astype(np.float32).astype(np.float64) == X1)
     Xc, yc = crdata.make_problem("C1")
     assert Xc.shape == (50, 2) and np.abs(Xc).max() <= 1
+
+
+# ---------------------------------------------------------------- adaptive step
+def _adaptive_check_dense(theta_t, theta_k, s, X, ybar, gamma):
+    """Eq. (adaptive-check) evaluated with the dense Def. A1A2 operators:
+    g(theta^k) - [g(theta~) + <grad g(theta~), theta^k - theta~> - s/2 ||theta^k - theta~||^2]."""
+    tt, tk = ref.theta_vec(theta_t), ref.theta_vec(theta_k)
+    D = tk - tt
+    lhs = ref.dual_value_dense(tk, X, ybar, gamma)
+    rhs = ref.dual_value_dense(tt, X, ybar, gamma) + ref.dual_grad_dense(tt, X, ybar, gamma) @ D - 0.5 * s * (D @ D)
+    return lhs - rhs
+
+
+def _dense_step(theta_t, s, X, ybar, gamma):
+    """Step 2 with step 1/s: (theta~ - C eta(theta~) / s)_+, dense."""
+    tt = ref.theta_vec(theta_t)
+    return ref.theta_mat(np.maximum(tt + ref.dual_grad_dense(tt, X, ybar, gamma) / s, 0.0), X.shape[0])
+
+
+@pytest.mark.parametrize("N,n,seed,ups", [(6, 2, 0, 2.0), (8, 3, 1, 2.0), (7, 1, 2, 3.0)])
+def test_adaptive_rule_accepts_minimal_l(N, n, seed, ups):
+    """PAPG_A: every accepted s_k = s_{k-1} ups^(l_k - 1) satisfies Eq. (adaptive-check)
+    and l_k is minimal (the trial at s_k / ups fails), both re-evaluated with dense operators."""
+    X, ybar = _tiny(N, n, seed)
+    gamma = 0.05
+    L = ref.lipschitz(X, gamma)
+    st = dict(Tprev=None, Tt=None, t=1.0, s=L)
+    for k in range(25):
+        Tt = np.zeros((N, N)) if st["Tt"] is None else st["Tt"]
+        nxt = oracle.papg_adaptive(X, ybar, gamma, st["s"], 1, ups=ups, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"])
+        s_k, l_k = nxt["s_hist"][0], int(nxt["trials"][0]) - 1
+        assert math.isclose(s_k, st["s"] * ups ** (l_k - 1), rel_tol=1e-15)
+        Tk = nxt["Tprev"]
+        np.testing.assert_allclose(Tk, _dense_step(Tt, s_k, X, ybar, gamma), rtol=1e-10, atol=1e-14)
+        scale = 1.0 + abs(ref.dual_value_dense(ref.theta_vec(Tt), X, ybar, gamma))
+        assert _adaptive_check_dense(Tt, Tk, s_k, X, ybar, gamma) >= -1e-12 * scale
+        if l_k >= 1:
+            Tr = _dense_step(Tt, s_k / ups, X, ybar, gamma)
+            assert _adaptive_check_dense(Tt, Tr, s_k / ups, X, ybar, gamma) < 0
+        st = dict(Tprev=nxt["Tprev"], Tt=nxt["Tt"], t=nxt["t"], s=nxt["s"])
+
+
+def test_adaptive_with_huge_ups_is_constant_step():
+    """With ups = 1e30 the l = 0 trial (step 1e30/s) always fails and l = 1 (s_k = s_{k-1} = L)
+    always passes (descent lemma: L bounds the gradient's Lipschitz constant, Eq. (lischitz)
+    P:375), so PAPG_A reproduces the constant-step Fig. 2 iterates with 2 trials per iteration."""
+    X, ybar = _tiny(12, 2, seed=4)
+    gamma = 0.02
+    L = ref.lipschitz(X, gamma)
+    a = oracle.papg_adaptive(X, ybar, gamma, L, 30, ups=1e30)
+    c = oracle.papg(X, ybar, gamma, L, 30)
+    assert np.all(a["trials"] == 2)
+    assert np.all(a["s_hist"] == L)
+    np.testing.assert_allclose(a["Tprev"], c["Tprev"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(a["y"], c["y"], rtol=0, atol=1e-13)
+
+
+def test_adaptive_quadratic_identity():
+    """g is quadratic at K = N (Step 1 is unconstrained), so for any theta, D:
+    g(theta+D) - g(theta) - <grad g(theta), D> = -1/2 (||A1^T D||^2 + ||A2^T D||^2 / gamma).
+    This is the form the GPU evaluates Eq. (adaptive-check) in (reading R15)."""
+    X, ybar = _tiny(7, 2, seed=5)
+    gamma = 0.03
+    rng = np.random.default_rng(0)
+    M = 7 * 6
+    for _ in range(5):
+        th, D = rng.random(M), rng.standard_normal(M)
+        lhs = (ref.dual_value_dense(th + D, X, ybar, gamma) - ref.dual_value_dense(th, X, ybar, gamma)
+               - ref.dual_grad_dense(th, X, ybar, gamma) @ D)
+        A1D, A2D = ref.dense_A1(7).T @ D, ref.dense_A2(X).T @ D
+        assert math.isclose(lhs, -0.5 * (A1D @ A1D + A2D @ A2D / gamma), rel_tol=1e-9)
+
+
+def test_adaptive_converges_to_nnls_optimum_within_backtracking_rate():
+    """PAPG_A reaches the exact regularized optimum (P3) and obeys the backtracking-APG rate
+    p* - g(theta^k) <= 2 max_k(s_k) ||theta^0 - theta*||^2 / (k+1)^2 (P:341 with L -> max s_k)."""
+    X, ybar = _tiny(8, 2, seed=6)
+    gamma = 0.05
+    opt = ref.regularized_optimum(X, ybar, gamma)
+    L = ref.lipschitz(X, gamma)
+    st = dict(Tprev=None, Tt=None, t=1.0, s=L)
+    smax = 0.0
+    th2 = opt["theta"] @ opt["theta"]
+    for k in range(1, 401):
+        nxt = oracle.papg_adaptive(X, ybar, gamma, st["s"], 1, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"])
+        smax = max(smax, nxt["s_hist"][0])
+        g = ref.dual_value_dense(ref.theta_vec(nxt["Tprev"]), X, ybar, gamma)
+        assert opt["p"] - g <= 2 * smax * th2 / (k + 1) ** 2 + 1e-10
+        st = dict(Tprev=nxt["Tprev"], Tt=nxt["Tt"], t=nxt["t"], s=nxt["s"])
+    y, _ = oracle.eta(X, ybar, gamma, st["Tprev"])
+    # (near the optimum the literal check's rounding -- g values of O(||ybar||^2) differenced to
+    # O(||D||^2) -- rejects steps spuriously and s_k grows; 400 iterations stay clear of that)
+    np.testing.assert_allclose(y, opt["y"], atol=5e-6)
