@@ -75,6 +75,18 @@ typedef enum {
     CR_KERNEL_TC = 2     /* tcgen05 (3xTF32) fused pass, fp32 only                         */
 } cr_kernel;
 
+/* Step rule of Step 2 (P:387 / P:400-407). */
+typedef enum {
+    CR_STEP_CONSTANT = 0,  /* step 1/L_gamma, Fig. 2 as printed                                  */
+    CR_STEP_ADAPTIVE = 1   /* step 1/s_k, s_k = s_{k-1} ups^(l_k - 1), l_k >= 0 the smallest
+                              integer passing Eq. (adaptive-check); s_0 = L_gamma */
+} cr_step_rule;
+
+/* cr_config.flags */
+#define CR_FLAG_ADAPTIVE 1  /* reserve a third Theta buffer + sums slot so cr_set_step_rule can
+                               select CR_STEP_ADAPTIVE (a rejected trial must not overwrite
+                               Theta^{k-2}); +1 Theta matrix of workspace                       */
+
 typedef struct cr_ctx cr_ctx;
 
 typedef struct {
@@ -93,6 +105,7 @@ typedef struct {
     void *stream;               /* cudaStream_t to enqueue on (NULL = legacy default stream)   */
     void *workspace;            /* DEVICE memory, >= cr_workspace_size(...) bytes, caller-owned */
     size_t workspace_bytes;
+    int32_t flags;              /* CR_FLAG_* (0: constant step only)                           */
 } cr_config;
 
 /* Diagnostics of eta(Theta^k) (Theorem 1 semantics) reported per P:951 / P:1106. */
@@ -119,9 +132,9 @@ typedef struct {
     cr_step_stats last;    /* stats at exit (only when stop != NULL)                           */
 } cr_report;
 
-/* Bytes of device workspace cr_init needs for this shape / rank (0 if unsupported). */
+/* Bytes of device workspace cr_init needs for this shape / rank / flags (0 if unsupported). */
 size_t cr_workspace_size(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel,
-                         int32_t rank, int32_t world);
+                         int32_t rank, int32_t world, int32_t flags);
 
 /* Largest n this library was built for. */
 int32_t cr_max_dim(void);
@@ -175,6 +188,24 @@ cr_status cr_get_eta(cr_ctx *ctx, double *y, double *xi);
  * r (HOST, this rank's rows), c (HOST, this rank's rows; column sums over ALL rows of all
  * ranks), P (HOST, rows x n, Theta X).  Any pointer may be NULL.  Synchronizes. */
 cr_status cr_get_sums(cr_ctx *ctx, int32_t which, double *r, double *c, double *P);
+
+/* Select the step rule for subsequent cr_dual_step / cr_solve calls.
+ *   CR_STEP_CONSTANT: 1/L (upsilon, s_prev ignored).
+ *   CR_STEP_ADAPTIVE (needs CR_FLAG_ADAPTIVE at cr_init, else CR_ERR_STATE): growth factor
+ *     upsilon > 1 (the paper leaves it open; 2 is the usual choice), s_prev = s_{k-1} the
+ *     next iteration starts from (0 -> L_gamma, the paper's s_0).  Each iteration
+ *     evaluates trials l = 0, 1, ... : a prologue + fused pass + reduce writing the trial
+ *     Theta^k into the spare buffer, and the check of Eq. (adaptive-check) evaluated as
+ *         ||A1^T D||^2 + ||A2^T D||^2 / gamma <= s ||D||^2,   D = Theta^k - theta~^k,
+ *     which is the same inequality because g_gamma is quadratic at K = N (R15);
+ *     one host synchronisation per trial (a trial whose Theta^k overflows the storage
+ *     precision counts as failing).  More than 64 trials: CR_ERR_STATE.
+ * Errors: CR_ERR_INVALID_ARG for a bad rule / upsilon / s_prev (context unchanged). */
+cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, double s_prev);
+
+/* s_k of the last accepted step (L for the constant rule), trials l_k + 1 of the last
+ * adaptive iteration and the total number of adaptive trials; any pointer may be NULL. */
+cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *trials_total);
 
 /* Step constant in use. */
 double cr_lipschitz(const cr_ctx *ctx);

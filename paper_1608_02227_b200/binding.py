@@ -19,13 +19,15 @@ CR_OK, CR_ERR_INVALID_ARG, CR_ERR_CUDA, CR_ERR_NCCL, CR_ERR_OOM, CR_ERR_STATE, C
 PREC = {"fp32": 0, "fp64": 1}
 KERNEL = {"auto": 0, "simt": 1, "tc": 2}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
+STEP_RULE = {"constant": 0, "adaptive": 1}
+CR_FLAG_ADAPTIVE = 1
 
 # Symbols include/cr.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "cr_workspace_size", "cr_max_dim", "cr_nccl_get_unique_id", "cr_init", "cr_set_theta", "cr_get_theta",
     "cr_get_theta_rows", "cr_get_sums", "cr_dual_step", "cr_solve", "cr_primal", "cr_get_eta", "cr_lipschitz",
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
-    "cr_last_error", "cr_status_string", "cr_destroy",
+    "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info",
 )
 
 
@@ -34,7 +36,7 @@ class CrConfig(C.Structure):
                 ("gamma", C.c_double), ("L", C.c_double), ("prec", C.c_int), ("kernel", C.c_int),
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t)]
+                ("workspace_bytes", C.c_size_t), ("flags", C.c_int32)]
 
 
 class CrStepStats(C.Structure):
@@ -72,7 +74,7 @@ def load(path: str = LIB_PATH):
     L = C.CDLL(path)
     vp, i64, i32, d = C.c_void_p, C.c_int64, C.c_int32, C.c_double
     sig = {
-        "cr_workspace_size": (C.c_size_t, [i64, i32, C.c_int, C.c_int, i32, i32]),
+        "cr_workspace_size": (C.c_size_t, [i64, i32, C.c_int, C.c_int, i32, i32, i32]),
         "cr_max_dim": (i32, []),
         "cr_nccl_get_unique_id": (C.c_int, [vp]),
         "cr_init": (C.c_int, [C.POINTER(CrConfig), C.POINTER(vp)]),
@@ -93,6 +95,8 @@ def load(path: str = LIB_PATH):
         "cr_last_error": (C.c_char_p, [vp]),
         "cr_status_string": (C.c_char_p, [C.c_int]),
         "cr_destroy": (None, [vp]),
+        "cr_set_step_rule": (C.c_int, [vp, C.c_int, d, d]),
+        "cr_step_info": (C.c_int, [vp, C.POINTER(d), C.POINTER(i64), C.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -109,8 +113,9 @@ def _f64(a, shape=None):
     return a
 
 
-def workspace_size(N, n, prec="fp32", kernel="auto", rank=0, world=1) -> int:
-    return int(load().cr_workspace_size(int(N), int(n), PREC[prec], KERNEL[kernel], int(rank), int(world)))
+def workspace_size(N, n, prec="fp32", kernel="auto", rank=0, world=1, flags=0) -> int:
+    return int(load().cr_workspace_size(int(N), int(n), PREC[prec], KERNEL[kernel], int(rank), int(world),
+                                        int(flags)))
 
 
 def lipschitz_host(X, gamma) -> float:
@@ -160,7 +165,7 @@ class Solver:
     """
 
     def __init__(self, X, ybar, gamma, L=0.0, prec="fp32", kernel="auto", device=None, stream=None,
-                 group=None):
+                 group=None, adaptive=False):
         import torch
         if not torch.cuda.is_available():
             raise CrError("libcr needs a CUDA device (no CPU fallback)")
@@ -182,7 +187,8 @@ class Solver:
                 uid = (C.c_char * 128).from_buffer_copy(broadcast_unique_id(group, dev))
         self._uid = uid
         self.row0, self.rows = shard_range(self.N, self.rank, self.world)
-        nbytes = workspace_size(self.N, self.n, prec, kernel, self.rank, self.world)
+        flags = CR_FLAG_ADAPTIVE if adaptive else 0
+        nbytes = workspace_size(self.N, self.n, prec, kernel, self.rank, self.world, flags)
         if nbytes == 0:
             raise CrError(f"unsupported shape/precision: N={self.N} n={self.n} prec={prec} kernel={kernel}")
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
@@ -191,7 +197,7 @@ class Solver:
                        L=float(L), prec=PREC[prec], kernel=KERNEL[kernel], rank=self.rank, world=self.world,
                        nccl_unique_id=C.cast(uid, C.c_void_p) if uid is not None else None,
                        device=dev.index, stream=self.stream.cuda_stream,
-                       workspace=self.workspace.data_ptr(), workspace_bytes=nbytes)
+                       workspace=self.workspace.data_ptr(), workspace_bytes=nbytes, flags=flags)
         h = C.c_void_p()
         st = self.lib.cr_init(C.byref(cfg), C.byref(h))
         if st != CR_OK:
@@ -272,6 +278,17 @@ class Solver:
         self._check(self.lib.cr_get_sums(self.h, int(which), r.ctypes.data, c.ctypes.data, P.ctypes.data),
                     "cr_get_sums")
         return r, c, P
+
+    def set_step_rule(self, rule: str = "constant", upsilon: float = 2.0, s_prev: float = 0.0):
+        """Step rule of Step 2: "constant" (1/L) or "adaptive" (needs adaptive=True)."""
+        self._check(self.lib.cr_set_step_rule(self.h, STEP_RULE[rule], float(upsilon), float(s_prev)),
+                    "cr_set_step_rule")
+
+    def step_info(self):
+        """dict(s = s_k of the last accepted step, trials_last = l_k + 1, trials_total)."""
+        sk, tl, tt = C.c_double(), C.c_int64(), C.c_int64()
+        self._check(self.lib.cr_step_info(self.h, C.byref(sk), C.byref(tl), C.byref(tt)), "cr_step_info")
+        return dict(s=sk.value, trials_last=tl.value, trials_total=tt.value)
 
     def set_pass_timing(self, on: bool):
         self._check(self.lib.cr_set_pass_timing(self.h, 1 if on else 0), "cr_set_pass_timing")

@@ -6,7 +6,10 @@
 //   fused pass (Steps 2 + 4 for every owned pair, sums of Theta^k)
 //   reduce    (fixed-order fp64 sums -> S^k; Step 3 momentum update on device)
 //   [world > 1: ncclReduceScatter of the column sums]
-// cr_solve replays the iteration as a CUDA graph (two graphs: buffer parities 0/1).
+// cr_solve replays the iteration as a CUDA graph (one graph per (Theta^{k-1}, Theta^{k-2})
+// buffer assignment).  With CR_FLAG_ADAPTIVE a third Theta buffer (and sums slot) receives the
+// trial Theta^k of the adaptive step rule, so a rejected trial leaves both state
+// matrices intact; the host accepts or retries from two device scalars per trial.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -36,12 +39,13 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Layout {
     int64_t N = 0, S = 0, Ns = 0, row0 = 0, Rp = 0, ldT = 0;
     int n = 0, NB = 0, NBP = 0, nRB = 0, world = 1, fp64 = 0;
+    int nbuf = 2;                  // Theta buffers / sums slots (3 with CR_FLAG_ADAPTIVE)
     size_t es = 4;
     // tensor-core pass
     bool tc = false;
     int NK = 0, NP2 = 0, nCBtc = 0, nRBtc = 0;
     // byte offsets
-    size_t th[2], XT, Xh, X64, ybar, r[2], c[2], P[2], y64, yv, bv, XiT, Xi64, a64, colpart, rowpart,
+    size_t th[3] = {0, 0, 0}, XT, Xh, X64, ybar, r[3] = {0, 0, 0}, c[3] = {0, 0, 0}, P[3] = {0, 0, 0}, dsq = 0, y64, yv, bv, XiT, Xi64, a64, colpart, rowpart,
         slot0, rb_ptr, rb_slots, cfull, ts, statpro, statres, g1h, g1l, g2h, g2l, XiR, slot0_tc, rb_ptr_tc, rb_slots_tc,
         total;
 };
@@ -55,8 +59,11 @@ bool use_tc(int n, cr_precision prec, cr_kernel kernel) {
     return n >= 16;
 }
 
-bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank, int world, Layout *L) {
+bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank, int world, int flags,
+                 Layout *L) {
     if (N < 2 || n < 1 || world < 1 || rank < 0 || rank >= world) return false;
+    if (flags & ~CR_FLAG_ADAPTIVE) return false;
+    L->nbuf = (flags & CR_FLAG_ADAPTIVE) ? 3 : 2;
     if (kernel == CR_KERNEL_TC && prec != CR_FP32) return false;
     L->tc = use_tc(n, prec, kernel);
     L->N = N;
@@ -77,16 +84,17 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     const int64_t WS = (int64_t)world * L->S;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + std::max<size_t>(bytes, 1), A); return r; };
-    for (int b = 0; b < 2; ++b) L->th[b] = take((size_t)L->Rp * L->ldT * es);
+    for (int b = 0; b < L->nbuf; ++b) L->th[b] = take((size_t)L->Rp * L->ldT * es);
     L->XT = take((size_t)L->NB * L->ldT * es);
     L->Xh = take((size_t)L->ldT * L->NBP * es);
     L->X64 = take((size_t)N * n * 8);
     L->ybar = take((size_t)N * 8);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < L->nbuf; ++s) {
         L->r[s] = take((size_t)L->Rp * 8);
         L->c[s] = take((size_t)L->Rp * 8);
         L->P[s] = take((size_t)L->Rp * n * 8);
     }
+    L->dsq = take((size_t)L->Rp * 8);
     L->y64 = take((size_t)std::max(WS, N) * 8);
     L->yv = take((size_t)std::max(WS, L->ldT) * es);
     L->bv = take((size_t)L->Rp * es);
@@ -101,7 +109,7 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
         L->nCBtc = (int)((N + kTcBN - 1) / kTcBN);
         L->nRBtc = (int)(L->Rp / kTcBM);
         if (192 + L->NP2 + 2 * L->NK > 512) return false;     // TMEM columns
-        rp_simt = std::max(rp_simt, (size_t)(L->nRBtc + kGMax) * kTcBM * (L->NP2 + 2) * 8);
+        rp_simt = std::max(rp_simt, (size_t)(L->nRBtc + kGMax) * kTcBM * (L->NP2 + 4) * 8);
     }
     L->rowpart = take(rp_simt);
     L->slot0 = take((size_t)kGMax * 4);
@@ -185,10 +193,16 @@ struct cr_ctx {
     cudaStream_t stream = nullptr;
     char *ws = nullptr;
     // device views
-    void *th[2];
-    double *r[2], *c[2], *P[2];
-    int b1 = 0;          // buffer holding Theta^{k-1} at the start of the next iteration
-    int s1 = 0;          // sums slot of Theta^{k-1}
+    void *th[3] = {nullptr, nullptr, nullptr};
+    double *r[3], *c[3], *P[3];      // sums slot b holds the sums of Theta buffer b
+    int bA = 0;          // buffer holding Theta^k (= Theta^{k-1} of the next iteration)
+    int bB = 1;          // buffer holding Theta^{k-1} (= Theta^{k-2} of the next iteration)
+    // step rule: constant 1/L, or adaptive 1/s_k
+    cr_step_rule rule = CR_STEP_CONSTANT;
+    double ups = 2.0;    // growth factor upsilon > 1
+    double s_cur = 0.0;  // s_{k-1} (adaptive)
+    int max_trials = 64;
+    int64_t trials_last = 0, trials_total = 0;
     int64_t k = 0;
     int G = 0, nCB = 0;
     int64_t T = 0;
@@ -199,11 +213,11 @@ struct cr_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> ev;
     size_t ev_used = 0;
-    // graphs per parity
-    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    // constant-step graphs per (bA, bB) assignment
+    cudaGraphExec_t graph[9] = {};
     cudaStream_t cap_stream = nullptr;   // private stream used only to record graphs
     // tensor-core pass
-    CUtensorMap tm[2];
+    CUtensorMap tm[3];
     int G_tc = 0, stages = 0, g1stages = 0, g2stages = 0, window = 64, smem_tc = 0;
     int64_t T_tc = 0;
     unsigned long long *trace = nullptr;   // debug timeline buffer (CR_TC_TRACE=<file>)
@@ -244,11 +258,14 @@ cr_status fail(cr_ctx *c, cr_status s, const char *fmt, ...) {
 
 ncclDataType_t nccl_t(const cr_ctx *ctx) { return ctx->lay.fp64 ? ncclFloat64 : ncclFloat32; }
 
-PassParams pass_params(cr_ctx *ctx, int b_read, int b_write) {
+PassParams pass_params(cr_ctx *ctx, int b_read, int b_read2, int b_out = -1, bool adapt = false) {
     const Layout &Ly = ctx->lay;
     PassParams p{};
     p.B1 = ctx->th[b_read];
-    p.B2 = ctx->th[b_write];
+    p.B2 = ctx->th[b_read2];
+    p.Bout = ctx->th[b_out < 0 ? b_read2 : b_out];
+    p.adapt = adapt ? 1 : 0;
+    p.dcol = Ly.n + 1;
     p.ldT = Ly.ldT;
     p.N = Ly.N;
     p.Ns = Ly.Ns;
@@ -270,7 +287,7 @@ PassParams pass_params(cr_ctx *ctx, int b_read, int b_write) {
     return p;
 }
 
-ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance, bool tc = false) {
+ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance, bool tc = false, bool adapt = false) {
     const Layout &Ly = ctx->lay;
     ReduceParams q{};
     q.N = Ly.N;
@@ -278,9 +295,12 @@ ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance, bool tc = false) 
     q.Rp = Ly.Rp;
     q.ldT = Ly.ldT;
     q.n = Ly.n;
-    q.NBP = tc ? Ly.NP2 + 2 : Ly.NBP;
+    q.NBP = tc ? Ly.NP2 + 4 : Ly.NBP;
     q.rcol0 = tc ? Ly.NP2 : Ly.n;
     q.rcol1 = tc ? Ly.NP2 + 1 : -1;
+    q.dcol0 = adapt ? (tc ? Ly.NP2 + 2 : Ly.n + 1) : -1;
+    q.dcol1 = (adapt && tc) ? Ly.NP2 + 3 : -1;
+    q.dsq = ctx->at<double>(Ly.dsq);
     q.nRB = tc ? Ly.nRBtc : Ly.nRB;
     q.rbm = tc ? kTcBM : kBM;
     q.colpart = ctx->ws + Ly.colpart;
@@ -326,7 +346,7 @@ SmallParams small_params(cr_ctx *ctx, int sa, int sb, int use_beta, double scale
     return p;
 }
 
-TcParams tc_params(cr_ctx *ctx) {
+TcParams tc_params(cr_ctx *ctx, bool adapt = false) {
     const Layout &Ly = ctx->lay;
     TcParams p{};
     p.N = Ly.N;
@@ -342,6 +362,7 @@ TcParams tc_params(cr_ctx *ctx) {
     p.window = ctx->window;
     p.g1stages = ctx->g1stages;
     p.g2stages = ctx->g2stages;
+    p.adapt = adapt ? 1 : 0;
     p.smem_bytes = ctx->smem_tc;
     p.g1_hi = ctx->at<float>(Ly.g1h);
     p.g1_lo = ctx->at<float>(Ly.g1l);
@@ -381,11 +402,14 @@ cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
     return CR_OK;
 }
 
-// One P-APG iteration for the current parity (no host sync).
-cr_status enqueue_step(cr_ctx *ctx, bool allow_timing) {
+// One P-APG iteration (no host sync): Step 1 at theta~^k from the sums of Theta^{k-1} (bA) and
+// Theta^{k-2} (bB) with step 1/s (scale), then the fused pass writing Theta^k into buffer bo
+// (bB in place for the constant step; the spare buffer for an adaptive trial) and its sums
+// into slot bo.  advance_t: Step 3 on the device (constant step); adapt: also ||D||^2 per row.
+cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, bool advance_t, bool adapt) {
     const Layout &Ly = ctx->lay;
-    const int b1 = ctx->b1, b2 = 1 - b1, s1 = ctx->s1, s2 = 1 - s1;
-    SmallParams sp = small_params(ctx, s1, s2, 1, 1.0 / ctx->L, false);
+    const int bA = ctx->bA, bB = ctx->bB;
+    SmallParams sp = small_params(ctx, bA, bB, 1, scale, false);
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
     if (ctx->world > 1) {
         char *yv = ctx->ws + Ly.yv;
@@ -400,32 +424,90 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing) {
         CK(cudaEventRecord(e0, ctx->stream));
     }
     if (Ly.tc) {
-        TcParams tp = tc_params(ctx);
-        CK(launch_pass_tc(ctx->tm[b1], ctx->tm[b2], tp, ctx->stream));
+        TcParams tp = tc_params(ctx, adapt);
+        CK(launch_pass_tc(ctx->tm[bA], ctx->tm[bB], ctx->tm[bo], tp, ctx->stream));
     } else {
-        PassParams p = pass_params(ctx, b1, b2);
+        PassParams p = pass_params(ctx, bA, bB, bo, adapt);
         CK(launch_pass_simt(p, Ly.fp64, Ly.NB, MODE_STEP, ctx->stream));
     }
     if (e1) CK(cudaEventRecord(e1, ctx->stream));
-    ReduceParams q = reduce_params(ctx, s2, 1, Ly.tc);
+    ReduceParams q = reduce_params(ctx, bo, advance_t ? 1 : 0, Ly.tc, adapt);
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
     if (ctx->world > 1)
-        NK(ncclReduceScatter(ctx->at<double>(Ly.cfull), ctx->c[s2], (size_t)Ly.S, ncclFloat64, ncclSum,
+        NK(ncclReduceScatter(ctx->at<double>(Ly.cfull), ctx->c[bo], (size_t)Ly.S, ncclFloat64, ncclSum,
                              ctx->comm, ctx->stream));
     ctx->launches += 3;
     return CR_OK;
 }
 
-void advance_host(cr_ctx *ctx) {
-    ctx->b1 = 1 - ctx->b1;
-    ctx->s1 = 1 - ctx->s1;
+// Theta^k now in buffer bo: it becomes Theta^{k-1} of the next iteration, the old Theta^{k-1}
+// becomes Theta^{k-2}.
+void advance_host(cr_ctx *ctx, int bo) {
+    ctx->bB = ctx->bA;
+    ctx->bA = bo;
     ctx->k += 1;
+}
+
+// One adaptive P-APG iteration: trial s = s_{k-1} ups^(l-1), l = 0, 1, ...;
+// Theta^k(s) into the spare buffer; accept when Q <= s ||D||^2 (Eq. (adaptive-check) in
+// quadratic form, R15).  Synchronizes once per trial.
+cr_status adaptive_step(cr_ctx *ctx) {
+    const Layout &Ly = ctx->lay;
+    const int bo = 3 - ctx->bA - ctx->bB;
+    DevScalars *ts = ctx->at<DevScalars>(Ly.ts);
+    double h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, ts, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const double t_prev = h[0], t_cur = h[1];
+    const double s_prev = ctx->s_cur;
+    int l = 0;
+    double s_try = 0.0;
+    for (;; ++l) {
+        if (l >= ctx->max_trials)
+            return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check)", ctx->max_trials);
+        s_try = s_prev * std::pow(ctx->ups, (double)l - 1.0);
+        cr_status st = enqueue_step(ctx, true, bo, 1.0 / s_try, false, true);
+        if (st != CR_OK) return st;
+        AdaptParams ap{};
+        ap.Ns = Ly.Ns;
+        ap.row0 = Ly.row0;
+        ap.n = Ly.n;
+        ap.gamma = ctx->gamma;
+        ap.X64 = ctx->at<double>(Ly.X64);
+        ap.rA = ctx->r[ctx->bA]; ap.cA = ctx->c[ctx->bA]; ap.PA = ctx->P[ctx->bA];
+        ap.rB = ctx->r[ctx->bB]; ap.cB = ctx->c[ctx->bB]; ap.PB = ctx->P[ctx->bB];
+        ap.rO = ctx->r[bo]; ap.cO = ctx->c[bo]; ap.PO = ctx->P[bo];
+        ap.dsq = ctx->at<double>(Ly.dsq);
+        ap.statpart = ctx->at<double>(Ly.statres);
+        ap.ts = ts;
+        CK(launch_adapt_check(ap, ctx->stream));
+        ctx->launches += 2;
+        if (ctx->world > 1) NK(ncclAllReduce(ts->stats + 8, ts->stats + 8, 2, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+        double qd[2];
+        CK(cudaMemcpyAsync(qd, ts->stats + 8, sizeof qd, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        // g(Theta^k) - [g(theta~) + <grad g(theta~), D> - s/2 ||D||^2] = (s ||D||^2 - Q) / 2 >= 0.
+        // A trial whose Theta^k overflowed the storage precision (a step far too long) cannot
+        // pass: it is rejected like any failing trial.
+        if (std::isfinite(qd[0]) && std::isfinite(qd[1]) && qd[0] <= s_try * qd[1]) break;
+    }
+    // Step 3 and the role change of Step 4
+    h[0] = t_cur;
+    h[1] = (1.0 + std::sqrt(1.0 + 4.0 * t_cur * t_cur)) / 2.0;
+    (void)t_prev;
+    CK(cudaMemcpyAsync(ts, h, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->s_cur = s_try;
+    ctx->trials_last = l + 1;
+    ctx->trials_total += l + 1;
+    advance_host(ctx, bo);
+    return CR_OK;
 }
 
 // eta(Theta^k) and diagnostics (Theorem 1 semantics); synchronizes.
 cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     const Layout &Ly = ctx->lay;
-    const int s = ctx->s1, b = ctx->b1;
+    const int s = ctx->bA, b = ctx->bA;
     int nb_pro = 0, nb_res = 0;
     SmallParams sp = small_params(ctx, s, s, 0, 1.0, true);
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, &nb_pro));
@@ -491,10 +573,10 @@ void drop_graphs(cr_ctx *ctx) {
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
 }
 
-cr_status build_graph(cr_ctx *ctx, int parity) {
-    // parity = ctx->b1 at capture time; capture one iteration, then restore host state
+cr_status build_graph(cr_ctx *ctx, int key) {
+    // key = 3 bA + bB at capture time; capture one constant-step iteration, restore host state
     cudaGraph_t g = nullptr;
-    const int b1 = ctx->b1, s1 = ctx->s1;
+    const int bA = ctx->bA, bB = ctx->bB;
     const int64_t k = ctx->k, launches = ctx->launches;
     // The caller's stream may be the legacy default stream, which cannot be captured: record
     // on a private stream, replay on the caller's stream (cudaGraphLaunch(..., ctx->stream)).
@@ -506,13 +588,13 @@ cr_status build_graph(cr_ctx *ctx, int parity) {
         ctx->stream = user;
         return fail(ctx, CR_ERR_CUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(e));
     }
-    cr_status st = enqueue_step(ctx, false);
+    cr_status st = enqueue_step(ctx, false, bB, 1.0 / ctx->L, true, false);
     e = cudaStreamEndCapture(ctx->stream, &g);
     ctx->stream = user;
-    ctx->b1 = b1; ctx->s1 = s1; ctx->k = k; ctx->launches = launches;
+    ctx->bA = bA; ctx->bB = bB; ctx->k = k; ctx->launches = launches;
     if (st != CR_OK) { if (g) cudaGraphDestroy(g); return st; }
     if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&ctx->graph[parity], g, 0);
+    e = cudaGraphInstantiate(&ctx->graph[key], g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
     return CR_OK;
@@ -549,9 +631,9 @@ cr_status cr_nccl_get_unique_id(void *out) {
 }
 
 size_t cr_workspace_size(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel, int32_t rank,
-                         int32_t world) {
+                         int32_t world, int32_t flags) {
     Layout L;
-    if (!make_layout(N, n, prec, kernel, rank, world, &L)) return 0;
+    if (!make_layout(N, n, prec, kernel, rank, world, flags, &L)) return 0;
     return L.total;
 }
 
@@ -591,7 +673,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     ctx->world = cfg->world;
     ctx->device = cfg->device;
     ctx->stream = static_cast<cudaStream_t>(cfg->stream);
-    if (!make_layout(N, n, cfg->prec, cfg->kernel, cfg->rank, cfg->world, &ctx->lay)) {
+    if (!make_layout(N, n, cfg->prec, cfg->kernel, cfg->rank, cfg->world, cfg->flags, &ctx->lay)) {
         delete ctx;
         return CR_ERR_UNSUPPORTED;
     }
@@ -612,8 +694,8 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         ctx->L = L;
     }
 
-    for (int b = 0; b < 2; ++b) ctx->th[b] = ctx->ws + Ly.th[b];
-    for (int s = 0; s < 2; ++s) {
+    for (int b = 0; b < Ly.nbuf; ++b) ctx->th[b] = ctx->ws + Ly.th[b];
+    for (int s = 0; s < Ly.nbuf; ++s) {
         ctx->r[s] = ctx->at<double>(Ly.r[s]);
         ctx->c[s] = ctx->at<double>(Ly.c[s]);
         ctx->P[s] = ctx->at<double>(Ly.P[s]);
@@ -697,7 +779,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
             IK(cudaMalloc(&ctx->trace, 5 * 256 * 8 * 8));
             IK(cudaMemsetAsync(ctx->trace, 0, 5 * 256 * 8 * 8, ctx->stream));
         }
-        for (int b = 0; b < 2; ++b)
+        for (int b = 0; b < Ly.nbuf; ++b)
             if (!make_theta_tmap(&ctx->tm[b], ctx->th[b], Ly.Rp, Ly.ldT)) {
                 fail(ctx, CR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                 return bail(CR_ERR_CUDA);
@@ -752,8 +834,8 @@ cr_status cr_set_theta(cr_ctx *ctx, const double *tk1, const double *tk2, double
             }
         }
     }
-    ctx->b1 = 0;
-    ctx->s1 = 0;
+    ctx->bA = 0;
+    ctx->bB = 1;
     st = enqueue_sums(ctx, 0, 0);
     if (st != CR_OK) return st;
     st = enqueue_sums(ctx, 1, 1);
@@ -788,8 +870,8 @@ cr_status cr_get_theta(cr_ctx *ctx, double *theta_k, double *theta_km1, double *
     cr_status st = check_ctx(ctx);
     if (st != CR_OK) return st;
     const Layout &Ly = ctx->lay;
-    if (theta_k && (st = read_buffer(ctx, ctx->b1, 0, Ly.Ns, theta_k)) != CR_OK) return st;
-    if (theta_km1 && (st = read_buffer(ctx, 1 - ctx->b1, 0, Ly.Ns, theta_km1)) != CR_OK) return st;
+    if (theta_k && (st = read_buffer(ctx, ctx->bA, 0, Ly.Ns, theta_k)) != CR_OK) return st;
+    if (theta_km1 && (st = read_buffer(ctx, ctx->bB, 0, Ly.Ns, theta_km1)) != CR_OK) return st;
     double t[2];
     CK(cudaMemcpyAsync(t, ctx->ws + Ly.ts, sizeof t, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -804,13 +886,19 @@ cr_status cr_get_theta_rows(cr_ctx *ctx, int32_t which, int64_t row0, int64_t nr
     const Layout &Ly = ctx->lay;
     if ((which != 0 && which != 1) || row0 < 0 || nrows < 0 || row0 + nrows > Ly.Ns || (!out && nrows))
         return fail(ctx, CR_ERR_INVALID_ARG, "cr_get_theta_rows: bad range");
-    return read_buffer(ctx, which == 0 ? ctx->b1 : 1 - ctx->b1, row0, nrows, out);
+    return read_buffer(ctx, which == 0 ? ctx->bA : ctx->bB, row0, nrows, out);
 }
 
 cr_status cr_dual_step(cr_ctx *ctx, cr_step_stats *out) {
     cr_status st = check_ctx(ctx);
     if (st != CR_OK) return st;
-    if ((st = enqueue_step(ctx, true)) != CR_OK) return st;
+    if (ctx->rule == CR_STEP_ADAPTIVE) {
+        if ((st = adaptive_step(ctx)) != CR_OK) return st;
+        if (out) return eval_stats(ctx, out);
+        return CR_OK;
+    }
+    const int bo = ctx->bB;
+    if ((st = enqueue_step(ctx, true, bo, 1.0 / ctx->L, true, false)) != CR_OK) return st;
     if (ctx->trace) {   // debug: dump the tensor-core pass timeline of CTA 0
         std::vector<unsigned long long> h(5 * 256 * 8);
         CK(cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -820,7 +908,7 @@ cr_status cr_dual_step(cr_ctx *ctx, cr_step_stats *out) {
             std::fclose(f);
         }
     }
-    advance_host(ctx);
+    advance_host(ctx, bo);
     if (out) return eval_stats(ctx, out);
     return CR_OK;
 }
@@ -835,15 +923,20 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
     const double Nd = (double)ctx->lay.N;
     int64_t it = 0;
     while (it < max_iters) {
-        if (use_graph) {
-            const int par = ctx->b1;
-            if (!ctx->graph[par] && (st = build_graph(ctx, par)) != CR_OK) return st;
-            CK(cudaGraphLaunch(ctx->graph[par], ctx->stream));
-            ctx->launches += 3;
-        } else if ((st = enqueue_step(ctx, true)) != CR_OK) {
-            return st;
+        if (ctx->rule == CR_STEP_ADAPTIVE) {
+            if ((st = adaptive_step(ctx)) != CR_OK) return st;
+        } else {
+            const int bo = ctx->bB;
+            if (use_graph) {
+                const int key = 3 * ctx->bA + ctx->bB;
+                if (!ctx->graph[key] && (st = build_graph(ctx, key)) != CR_OK) return st;
+                CK(cudaGraphLaunch(ctx->graph[key], ctx->stream));
+                ctx->launches += 3;
+            } else if ((st = enqueue_step(ctx, true, bo, 1.0 / ctx->L, true, false)) != CR_OK) {
+                return st;
+            }
+            advance_host(ctx, bo);
         }
-        advance_host(ctx);
         ++it;
         if (stop && (it % stop->report_every == 0 || it == max_iters)) {
             cr_step_stats s{};
@@ -889,13 +982,39 @@ cr_status cr_get_sums(cr_ctx *ctx, int32_t which, double *r, double *c, double *
     if (st != CR_OK) return st;
     if (which != 0 && which != 1) return fail(ctx, CR_ERR_INVALID_ARG, "cr_get_sums: which");
     const Layout &Ly = ctx->lay;
-    const int s = which == 0 ? ctx->s1 : 1 - ctx->s1;
+    const int s = which == 0 ? ctx->bA : ctx->bB;
     if (Ly.Ns > 0) {
         if (r) CK(cudaMemcpyAsync(r, ctx->r[s], (size_t)Ly.Ns * 8, cudaMemcpyDeviceToHost, ctx->stream));
         if (c) CK(cudaMemcpyAsync(c, ctx->c[s], (size_t)Ly.Ns * 8, cudaMemcpyDeviceToHost, ctx->stream));
         if (P) CK(cudaMemcpyAsync(P, ctx->P[s], (size_t)Ly.Ns * Ly.n * 8, cudaMemcpyDeviceToHost, ctx->stream));
     }
     CK(cudaStreamSynchronize(ctx->stream));
+    return CR_OK;
+}
+
+cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, double s_prev) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    if (rule != CR_STEP_CONSTANT && rule != CR_STEP_ADAPTIVE)
+        return fail(ctx, CR_ERR_INVALID_ARG, "cr_set_step_rule: unknown rule");
+    if (rule == CR_STEP_ADAPTIVE) {
+        if (ctx->lay.nbuf < 3)
+            return fail(ctx, CR_ERR_STATE, "adaptive step needs the third Theta buffer (cr_config.flags CR_FLAG_ADAPTIVE)");
+        if (!(upsilon > 1.0) || !std::isfinite(upsilon))
+            return fail(ctx, CR_ERR_INVALID_ARG, "upsilon must be finite and > 1");
+        if (s_prev < 0.0 || !std::isfinite(s_prev)) return fail(ctx, CR_ERR_INVALID_ARG, "s_prev must be >= 0");
+        ctx->ups = upsilon;
+        ctx->s_cur = s_prev > 0.0 ? s_prev : ctx->L;     // s_0 = L_gamma
+    }
+    ctx->rule = rule;
+    return CR_OK;
+}
+
+cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *trials_total) {
+    if (!ctx) return CR_ERR_INVALID_ARG;
+    if (s_k) *s_k = ctx->rule == CR_STEP_ADAPTIVE ? ctx->s_cur : ctx->L;
+    if (trials_last) *trials_last = ctx->rule == CR_STEP_ADAPTIVE ? ctx->trials_last : 1;
+    if (trials_total) *trials_total = ctx->trials_total;
     return CR_OK;
 }
 

@@ -31,7 +31,10 @@ struct DevScalars {
 
 struct PassParams {
     const void *B1;        // Theta^{k-1} (read)
-    void *B2;              // Theta^{k-2} (read), overwritten with Theta^k (MODE_STEP)
+    void *B2;              // Theta^{k-2} (read)
+    void *Bout;            // Theta^k (MODE_STEP): B2 (in place) or a third buffer (adaptive step)
+    int adapt;             // 1: row partial column n+1 receives sum_j (Theta^k - theta~)^2
+    int dcol;              // that column (n + 1 < NBP)
     int64_t ldT;           // row pitch of Theta, XT, colpart (elements)
     int64_t N, Ns, row0;   // global size, shard rows, first global row of the shard
     int nRB, nCB;          // tile grid (row blocks of kBM, column tiles of kBN)
@@ -84,6 +87,8 @@ struct ReduceParams {
     const double *rowpart; // [slots][kBM][NBP]
     const int *rb_ptr;     // [nRB + 1]
     const int *rb_slots;   // row-partial slot list per row block (CTA order)
+    int dcol0, dcol1;      // slot-row columns holding ||Theta^k - theta~||^2 partials (-1: none)
+    double *dsq;           // [Rp] per-row ||Theta^k - theta~||^2 (when dcol0 >= 0)
     double *r, *P;         // this shard's rows
     double *c_out;         // column sums for all N columns (shard partial)
     DevScalars *ts;
@@ -91,6 +96,21 @@ struct ReduceParams {
 };
 
 cudaError_t launch_reduce(const ReduceParams &p, int prec_fp64, cudaStream_t s);
+
+// Adaptive step: Eq. (adaptive-check) in its quadratic form (R15),
+//   Q = ||A1^T D||^2 + ||A2^T D||^2 / gamma   vs   s ||D||^2,   D = Theta^k - theta~^k,
+// from the sums of Theta^{k-1} (A), Theta^{k-2} (B), Theta^k (O) and the per-row ||D||^2.
+struct AdaptParams {
+    int64_t Ns, row0;
+    int n;
+    double gamma;
+    const double *X64;
+    const double *rA, *cA, *PA, *rB, *cB, *PB, *rO, *cO, *PO;
+    const double *dsq;
+    double *statpart;      // [kStatBlocks][8]: Q at 0, ||D||^2 at 1
+    DevScalars *ts;        // beta from (t_prev, t_cur); results to stats[8], stats[9]
+};
+cudaError_t launch_adapt_check(const AdaptParams &p, cudaStream_t s);
 
 struct ResidualParams {
     const void *Theta;     // [Rp][ldT] storage precision
@@ -112,6 +132,7 @@ struct TcParams {
     int64_t N, Ns, row0, ldT, T;
     int G, nCB, NK, NP2, stages, window;
     int g1stages, g2stages;          // X_J / X_J^T image ring slots
+    int adapt;                       // 1: also accumulate ||Theta^k - theta~||^2 per row (adaptive step)
     int smem_bytes;
     const float *g1_hi, *g1_lo;      // [nCB][NK * 32]  X_J  tiles (K-major interleave), tf32 hi / lo
     const float *g2_hi, *g2_lo;      // [nCB][NP2 * 32] X_J^T tiles (K-major interleave), tf32 hi / lo
@@ -119,14 +140,15 @@ struct TcParams {
     const float *XiR;                // [Rp][NK] xi * scale
     const float *bv;                 // [Rp] (a - y) * scale
     float *colpart;                  // [nRB128][ldT]
-    double *rowpart;                 // [slots][128][NP2]
+    double *rowpart;                 // [slots][128][NP2 + 4]: Theta X | r (wg 0, 1) | ||D||^2 (wg 0, 1)
     const int *cta_slot0;
     unsigned long long *trace;       // debug: clock64 timeline of CTA 0 (nullptr = off)
     const double *ts;
 };
 
 // tcgen05 fused pass (kernels/pass_tc.cu).
-cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const TcParams &p, cudaStream_t s);
+cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const CUtensorMap &tmOut, const TcParams &p,
+                           cudaStream_t s);
 cudaError_t pass_tc_prepare(int NK, int smem_bytes);
 size_t tc_barrier_bytes();
 cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,

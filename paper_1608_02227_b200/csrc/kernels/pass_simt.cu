@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
     if (t0 >= t1) return;
 
     const T *B1 = static_cast<const T *>(p.B1);
-    T *B2 = static_cast<T *>(p.B2);
+    const T *B2 = static_cast<const T *>(p.B2);
+    T *Bout = static_cast<T *>(p.Bout);
     const T *XT = static_cast<const T *>(p.XT);
     const T *Xh = static_cast<const T *>(p.Xh);
     const T *XiT = static_cast<const T *>(p.XiT);
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
     T pacc[PB][16];
     (void)pacc_f;
     int slot = p.cta_slot0[blockIdx.x];
+    double dacc[4] = {0.0, 0.0, 0.0, 0.0};     // adaptive step: sum_j (Theta^k - theta~)^2 of the 4 rows
     int64_t cur_rb = -1;
     int since_flush = 0;
 
@@ -190,6 +192,17 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) s += Pd[(ks * NOB + ob) * 16 + e];
             dst[o] = s;
+        }
+        if (MODE == MODE_STEP && p.adapt) {
+            __syncthreads();                     // column dcol of the slot rows written above
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double v = dacc[r];
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);   // over tx
+                if (tx == 0) dst[(ty * 4 + r) * NBP + p.dcol] = v;
+                dacc[r] = 0.0;
+            }
         }
         ++slot;
         (void)rb;
@@ -269,8 +282,12 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
                     const double b1 = (double)cb1[r][c];
                     const double v = fma(beta64, b1 - (double)cb2[r][c], b1) + (double)acc[r][c];
                     th[r][c] = ok ? T(fmax(v, 0.0)) : T(0);           // ( . )_+  (Step 2)
+                    if (p.adapt) {                                     // D = Theta^k - theta~
+                        const double d = ((double)th[r][c] - b1) - beta64 * (b1 - (double)cb2[r][c]);
+                        dacc[r] = fma(d, d, dacc[r]);
+                    }
                 }
-                st4cs(B2 + lr * ldT + gj0, th[r]);
+                st4cs(Bout + lr * ldT + gj0, th[r]);
             }
         } else {
 #pragma unroll

@@ -83,7 +83,8 @@ struct Cursor {
 
 template <int NK>
 __global__ void __launch_bounds__(NTHR, 1)
-pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2, const TcParams p) {
+pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
+               const __grid_constant__ CUtensorMap tmOut, const TcParams p) {
     constexpr int NP2 = (NK + 15) / 16 * 16;           // GEMM2 N (multiple of 16 for M = 128)
     extern __shared__ __align__(16) uint8_t smem_raw[];
     // 1024-byte alignment by offsetting the shared pointer itself (an integer round trip would
@@ -110,7 +111,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
     if (t0 >= t1) return;
     const int U = t1 - t0;
     const int nCB = p.nCB;
-    constexpr int W = NP2 + 2;
+    constexpr int W = NP2 + 4;                         // rowpart row: Theta X | r (2 wg) | ||D||^2 (2 wg)
     const int wmask = p.window - 1;                    // flush window (power of two)
     constexpr uint32_t lbo2 = (uint32_t)NP2 * 16;      // X^T image: K-chunk (4 j) stride
     const int slot0 = p.cta_slot0[blockIdx.x];
@@ -176,7 +177,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(&bar->tmem_base, 512);
-    if (warp == 0 && lane == 0) { prefetch_tmap(&tmB1); prefetch_tmap(&tmB2); }
+    if (warp == 0 && lane == 0) { prefetch_tmap(&tmB1); prefetch_tmap(&tmB2); prefetch_tmap(&tmOut); }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -311,7 +312,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 TC_TRACE(2, c.u, 0);
                 mbar_wait(&bar->st_full[c.s], (uint32_t)c.ph);
                 TC_TRACE(2, c.u, 1);
-                tma_store_2d(&tmB2, c.cb * TBN, c.rb * TBM, stage_ptr(c.s) + TILE_BYTES, pol_stream);
+                tma_store_2d(&tmOut, c.cb * TBN, c.rb * TBM, stage_ptr(c.s) + TILE_BYTES, pol_stream);
                 bulk_commit();
                 bulk_wait_read<0>();                      // slot read by the store engine
                 TC_TRACE(2, c.u, 2);
@@ -329,6 +330,8 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         int flushes = 0;
         int last_flush_slot = -1;
         double rrun = 0.0;                            // this warpgroup's row sum over the current run
+        double drun = 0.0;                            // ... and sum of (Theta^k - theta~)^2 (adaptive step)
+        const bool adapt = p.adapt != 0;
         float bi = 0.f;
         int cur_rb = -1;
         float *my_colS = colS + wg * 2 * 4 * 32;
@@ -419,7 +422,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             uint32_t vmask = row_ok ? (nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u)) : 0u;
             if (dcol >= 0) vmask &= ~(1u << dcol);
             const bool dirty = __any_sync(0xffffffffu, vmask != 0xffffffffu);
-            float rtile = 0.f;
+            float rtile = 0.f, dtile = 0.f;
             float *colw = my_colS + ((((c.u >> 1) & 1) * 4) + q) * 32;
             // two 16-column halves, rolled (keeps the loop body small: instruction-cache resident)
 #pragma unroll 1
@@ -449,6 +452,13 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
                             if (!((vmask >> (4 * k + e)) & 1u)) th[4 * k4 + e] = 0.f;
+                    }
+                    if (adapt) {           // D = Theta^k - theta~ = (Theta^k - b1) - beta (b1 - b2)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float d = (th[4 * k4 + e] - b1[e]) - beta * (b1[e] - b2[e]);
+                            dtile = fmaf(d, d, dtile);
+                        }
                     }
                     *reinterpret_cast<float4 *>(rowB2 + off) =                              // in place, for the store
                         make_float4(th[4 * k4], th[4 * k4 + 1], th[4 * k4 + 2], th[4 * k4 + 3]);
@@ -501,6 +511,7 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->st_full[c.s]);
             rrun += (double)rtile;
+            drun += (double)dtile;
             named_barrier(1 + wg, 128);
             if (tr) TC_TRACE(3 + wg, c.u, 5);
             if (q == 0) {
@@ -512,8 +523,11 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
             Cursor n2 = c;
             adv(n2, 2);
             if (n2.u >= U || n2.rb != rb) {
-                p.rowpart[((int64_t)(slot0 + rb - rbA) * TBM + r) * W + NP2 + wg] = rrun;
+                double *rp = p.rowpart + ((int64_t)(slot0 + rb - rbA) * TBM + r) * W;
+                rp[NP2 + wg] = rrun;
+                if (adapt) rp[NP2 + 2 + wg] = drun;
                 rrun = 0.0;
+                drun = 0.0;
             }
             // ---- Theta X flushes (warpgroup 0 handles those after tiles u and u+1)
             if (wg == 0) {
@@ -559,9 +573,10 @@ __global__ void tc_images_kernel(const double *X64, int64_t N, int n, int NK, in
 
 #define CR_TC_NK_LIST(X) X(8) X(16) X(24) X(32) X(40) X(48) X(56) X(64) X(72) X(80)
 
-cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const TcParams &p, cudaStream_t s) {
+cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const CUtensorMap &tmOut, const TcParams &p,
+                           cudaStream_t s) {
     switch (p.NK) {
-#define CR_CASE(V) case V: pass_tc_kernel<V><<<p.G, NTHR, p.smem_bytes, s>>>(tmB1, tmB2, p); break;
+#define CR_CASE(V) case V: pass_tc_kernel<V><<<p.G, NTHR, p.smem_bytes, s>>>(tmB1, tmB2, tmOut, p); break;
         CR_TC_NK_LIST(CR_CASE)
 #undef CR_CASE
         default: return cudaErrorInvalidValue;

@@ -114,10 +114,14 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
             for (int base = 0; base < ns; base += 32) {
                 const int m = min(32, ns - base);
                 const int *ids = p.rb_slots + e0 + base;
-                for (int d = lane; d <= p.n; d += 32) {
-                    const int col = d < p.n ? d : p.rcol0;
-                    const bool two = d == p.n && p.rcol1 >= 0;
-                    double s = base == 0 ? 0.0 : (d < p.n ? p.P[(int64_t)i * p.n + d] : p.r[i]);
+                // virtual columns: d < n -> Theta X, d = n -> r, d = n + 1 -> ||D||^2 (adaptive)
+                const int dmax = p.n + (p.dcol0 >= 0 ? 1 : 0);
+                for (int d = lane; d <= dmax; d += 32) {
+                    const int col = d < p.n ? d : (d == p.n ? p.rcol0 : p.dcol0);
+                    const int col2 = d < p.n ? -1 : (d == p.n ? p.rcol1 : p.dcol1);
+                    const bool two = col2 >= 0;
+                    double *out = d < p.n ? p.P + (int64_t)i * p.n + d : (d == p.n ? p.r + i : p.dsq + i);
+                    double s = base == 0 ? 0.0 : *out;
                     for (int q0 = 0; q0 < m; q0 += 4) {
                         double v[4], w[4];
                         double *rows[4];
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
                             const int sl = ok ? ids[q0 + k] : 0;
                             rows[k] = rp + ((int64_t)sl * p.rbm + ii) * p.NBP;
                             v[k] = ok ? rows[k][col] : 0.0;
-                            w[k] = (ok && two) ? rows[k][p.rcol1] : 0.0;
+                            w[k] = (ok && two) ? rows[k][col2] : 0.0;
                         }
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
@@ -135,12 +139,11 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
                                 s += v[k];
                                 if (two) s += w[k];
                                 rows[k][col] = 0.0;
-                                if (two) rows[k][p.rcol1] = 0.0;
+                                if (two) rows[k][col2] = 0.0;
                             }
                         }
                     }
-                    if (d < p.n) p.P[(int64_t)i * p.n + d] = s;
-                    else p.r[i] = s;
+                    *out = s;
                 }
             }
         }
@@ -150,6 +153,51 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
         p.ts->t_prev = t;
         p.ts->t_cur = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;   // Step 3
     }
+}
+
+// Adaptive step check in quadratic form: one warp per row, lanes over d.
+//   Dr = r_O - (r_A + beta (r_A - r_B)), Dc likewise, DP_d likewise  (sums of D = Theta^k - theta~)
+//   q_i = (Dc_i - Dr_i)^2 + sum_d (Dr_i x_id - DP_id)^2 / gamma       ((A1^T D)_i^2 + |(A2^T D)_i|^2/gamma)
+// Per-block partials of Q = sum q_i and ||D||^2 = sum dsq_i to statpart (fixed order).
+__global__ void __launch_bounds__(256) adapt_check_kernel(const AdaptParams p) {
+    __shared__ double red[2][8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double beta = (p.ts->t_prev - 1.0) / p.ts->t_cur;
+    double Q = 0.0, D2 = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < p.Ns; i += (int64_t)gridDim.x * 8) {
+        const double dr = p.rO[i] - (p.rA[i] + beta * (p.rA[i] - p.rB[i]));
+        const double dc = p.cO[i] - (p.cA[i] + beta * (p.cA[i] - p.cB[i]));
+        const double *x = p.X64 + (p.row0 + i) * p.n;
+        double q = 0.0;
+        for (int d = lane; d < p.n; d += 32) {
+            const int64_t e = i * p.n + d;
+            const double dP = p.PO[e] - (p.PA[e] + beta * (p.PA[e] - p.PB[e]));
+            const double a2 = dr * x[d] - dP;
+            q += a2 * a2;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if (lane == 0) {
+            const double a1 = dc - dr;
+            Q += a1 * a1 + q / p.gamma;
+            D2 += p.dsq[i];
+        }
+    }
+    if (lane == 0) { red[0][warp] = Q; red[1][warp] = D2; }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+        p.statpart[blockIdx.x * 8 + threadIdx.x] = t;
+    }
+}
+
+__global__ void adapt_finalize_kernel(const double *part, int nb, DevScalars *ts) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double q = 0.0, d = 0.0;
+    for (int b = 0; b < nb; ++b) { q += part[b * 8]; d += part[b * 8 + 1]; }
+    ts->stats[8] = q;
+    ts->stats[9] = d;
 }
 
 // Residual pass: 128 columns x 32 rows per tile, thread = (column, 16-row half).
@@ -276,6 +324,15 @@ cudaError_t launch_reduce(const ReduceParams &p, int fp64, cudaStream_t s) {
     const unsigned nb = (unsigned)(ncolb + nrowb);
     if (fp64) reduce_kernel<double><<<nb, 256, 0, s>>>(p, ncolb);
     else reduce_kernel<float><<<nb, 256, 0, s>>>(p, ncolb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adapt_check(const AdaptParams &p, cudaStream_t s) {
+    int64_t nb = (p.Ns + 7) / 8;
+    if (nb < 1) nb = 1;
+    if (nb > kStatBlocks) nb = kStatBlocks;
+    adapt_check_kernel<<<(unsigned)nb, 256, 0, s>>>(p);
+    adapt_finalize_kernel<<<1, 32, 0, s>>>(p.statpart, (int)nb, p.ts);
     return cudaGetLastError();
 }
 

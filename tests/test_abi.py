@@ -41,6 +41,10 @@ def test_workspace_sizes_and_unsupported(lib):
     assert n4 >= 2 * 16384 * 16384 * 4
     assert crp.workspace_size(16384, 40, "fp32", rank=1, world=8) < n4 / 4
     assert crp.workspace_size(1, 2) == 0                  # N < 2
+    # CR_FLAG_ADAPTIVE reserves one more Theta matrix (+ sums slot); unknown flags are rejected
+    extra = crp.workspace_size(16384, 40, "fp32", flags=1) - n4
+    assert 16384 * 16384 * 4 <= extra < 16384 * 16384 * 4 * 1.1
+    assert crp.workspace_size(16384, 40, "fp32", flags=2) == 0
     assert crp.workspace_size(100, 0) == 0                # n < 1
     assert crp.workspace_size(100, 500) == 0              # n beyond the compiled buckets
     assert crp.workspace_size(100, 4, rank=3, world=2) == 0
