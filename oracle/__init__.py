@@ -10,7 +10,8 @@ Contents
 --------
 ``papg_oracle.c`` (loaded here via ctypes)
     fp64 Fig. 2 iteration (P:377-397) with K = N, plain loops + OpenMP over rows;
-    the adaptive-step variant (Eq. (adaptive-check)) written out literally.
+    the adaptive-step variant (P:400-407, Eq. (adaptive-check)) written out literally;
+    the continuation over gamma_t (Section 2.4.1) in core.py on top of it.
 ``ref.py``
     dense A1/A2/C (Def. A1A2), the exact regularized optimum via the
     NNLS form of the dual, the univariate sorted-slope convex fit
@@ -23,5 +24,5 @@ Parity status per function:
     definition form and Lemma 4 closed forms.
 """
 from .core import (  # noqa: F401
-    build_oracle, lib, papg, papg_adaptive, eta, stats, project_rows, momentum_next, max_threads, extrapolate, state_after,
+    build_oracle, lib, papg, papg_adaptive, continuation, eta, stats, project_rows, momentum_next, max_threads, extrapolate, state_after,
 )

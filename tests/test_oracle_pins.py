@@ -435,3 +435,49 @@ def test_adaptive_converges_to_nnls_optimum_within_backtracking_rate():
     # (near the optimum the literal check's rounding -- g values of O(||ybar||^2) differenced to
     # O(||D||^2) -- rejects steps spuriously and s_k grows; 400 iterations stay clear of that)
     np.testing.assert_allclose(y, opt["y"], atol=5e-6)
+
+
+# ---------------------------------------------------------------- continuation (Section 2.4.1)
+def test_continuation_approaches_unregularized_estimator_1d():
+    """Continuation on a univariate problem: as gamma_t = kappa eps0 / beta^t -> 0 the
+    stage estimators y^(t) approach the exact unregularized convex LS fit y* (sorted-slope fit, a
+    textbook routine) within ||xi*|| sqrt(gamma_t) + sqrt(2 delta_t), delta_t the dual
+    suboptimality of stage t measured against the exact regularized optimum (NNLS, P3)."""
+    N = 20
+    rng = np.random.default_rng(7)
+    x = np.sort(rng.uniform(-1, 1, N))
+    ybar = x ** 2 + 0.1 * rng.standard_normal(N)
+    X = x[:, None]
+    ystar = ref.convex_fit_1d(x, ybar)
+    slopes = np.diff(ystar) / np.diff(x)
+    xi_star = np.clip(0.0, np.concatenate([[-np.inf], slopes]), np.concatenate([slopes, [np.inf]]))
+    sigma2 = ref.sigma_max_sq(X)
+    stages = oracle.continuation(X, ybar, sigma2, eps0=1e-1, beta=4.0, kappa_gamma=1.0, iters=[3000] * 5)
+    prev = np.inf
+    for st in stages:
+        opt = ref.regularized_optimum(X, ybar, st["gamma"])
+        delta = opt["p"] - ref.dual_value_dense(ref.theta_vec(st["Theta"]), X, ybar, st["gamma"])
+        assert delta >= -1e-10
+        dist = np.linalg.norm(st["y"] - ystar)
+        bound = np.linalg.norm(xi_star) * math.sqrt(st["gamma"]) + math.sqrt(2 * max(delta, 0.0))
+        assert dist <= bound * (1 + 1e-6) + 1e-9, (st["gamma"], dist, bound)
+        prev = min(prev, dist)
+    assert np.linalg.norm(stages[-1]["y"] - ystar) < np.linalg.norm(stages[0]["y"] - ystar)
+
+
+def test_continuation_stage_is_warm_started_papg():
+    """Stage t is Fig. 2 restarted at theta^(t-1) (theta~^1 = theta^0, t_1 = 1) with
+    L_t = sigma_max(C)^2 / gamma_t (Eq. (lischitz)): a 1-stage continuation from Theta0
+    equals oracle.papg from (Theta0, Theta0, 1) -- and its first step from 0 is Theta^1 of P1."""
+    X, ybar = _tiny(10, 2, seed=8)
+    sigma2 = ref.sigma_max_sq(X)
+    st = oracle.continuation(X, ybar, sigma2, eps0=0.5, beta=2.0, kappa_gamma=0.1, iters=[1])[0]
+    assert math.isclose(st["gamma"], 0.1 * 0.5 / 2.0)
+    want = np.maximum(ybar[:, None] - ybar[None, :], 0.0) / (sigma2 / st["gamma"])
+    np.fill_diagonal(want, 0.0)
+    np.testing.assert_allclose(st["Theta"], want, rtol=1e-14, atol=0)
+    T0 = crdata.random_theta(10, seed=3)
+    a = oracle.continuation(X, ybar, sigma2, eps0=0.5, beta=2.0, kappa_gamma=0.1, iters=[7, 5], Theta0=T0)
+    b1 = oracle.papg(X, ybar, a[0]["gamma"], a[0]["L"], 7, Tprev=T0, Tt=T0, t=1.0)
+    b2 = oracle.papg(X, ybar, a[1]["gamma"], a[1]["L"], 5, Tprev=b1["Tprev"], Tt=b1["Tprev"], t=1.0)
+    np.testing.assert_array_equal(a[1]["Theta"], b2["Tprev"])
