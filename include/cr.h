@@ -207,7 +207,41 @@ cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, doubl
  * adaptive iteration and the total number of adaptive trials; any pointer may be NULL. */
 cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *trials_total);
 
-/* Step constant in use. */
+/* Change the Tikhonov weight (Eq. (regularize)) of the problem being solved and restart
+ * Fig. 2 at the current iterate: theta^0 := Theta^k, theta~^1 = theta^0, t_1 = 1.
+ * L > 0 is used as given; L == 0 uses sigma_max(C)^2 / gamma with the sigma_max(C)^2 this
+ * context holds (= L * gamma of cr_init; Eq. (lischitz), valid for gamma <= 1).  Under
+ * the adaptive rule s is reset to the new L.  Errors: CR_ERR_INVALID_ARG. */
+cr_status cr_set_gamma(cr_ctx *ctx, double gamma, double L);
+
+/* Continuation over gamma (Section 2.4.1).  Outer stages t = 1..stages:
+ *   eps_t = eps0 / beta^t,  gamma_t = kappa_gamma * eps_t  (must lie in (0, 1]),
+ *   theta^(t) = P-APG on the gamma_t problem started from theta^(t-1) (cr_set_gamma(gamma_t, 0)
+ *   then cr_solve), theta^(0) = the context's current Theta^k (0 after cr_init),
+ * each stage running iters[t-1] iterations (HOST array of `stages` budgets, the K_t of P:580,
+ * which the paper bounds a priori but leaves to the user), or iters_per_stage when iters is
+ * NULL, ending early when `stop` (nullable) holds -- the stopping pair of P:1106, as in cr_solve.
+ * The step rule in force (cr_set_step_rule) is used inside the stages. */
+typedef struct {
+    double eps0;              /* eps_0 > 0                                   */
+    double beta;              /* beta > 1                                    */
+    double kappa_gamma;       /* kappa_gamma > 0                             */
+    int32_t stages;           /* T >= 1                                      */
+    const int64_t *iters;     /* HOST [stages] or NULL                       */
+    int64_t iters_per_stage;  /* used when iters == NULL (>= 0)              */
+    const cr_stop *stop;      /* nullable                                    */
+} cr_cont;
+
+typedef struct {
+    int32_t stages_run;
+    int64_t iters_total;
+    double gamma_last, L_last;
+    cr_step_stats last;       /* diagnostics of eta(Theta) on the gamma_last problem */
+} cr_cont_report;
+
+cr_status cr_continuation(cr_ctx *ctx, const cr_cont *params, cr_cont_report *out);
+
+/* Step constant in use (L_gamma of the current gamma). */
 double cr_lipschitz(const cr_ctx *ctx);
 
 /* Host-only: L = sigma_max(C)^2 / gamma by fp64 Lanczos on the structured C^T C

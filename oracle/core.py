@@ -105,14 +105,15 @@ def papg_adaptive(X, ybar, gamma, s, K, ups=2.0, Tprev=None, Tt=None, t=1.0, max
     return dict(Tprev=Tprev, Tt=Tt, t=tt.value, s=ss.value, trials=trials[:K], s_hist=s_hist[:K], y=y, xi=xi)
 
 
-def continuation(X, ybar, sigma2, eps0, beta, kappa_gamma, iters, Theta0=None, stop=None, nthreads=0):
+def continuation(X, ybar, sigma2, eps0, beta, kappa_gamma, iters, Theta0=None, stop=None, ups=None, nthreads=0):
     """Continuation over gamma (Section 2.4.1): for outer t = 1..T,
         eps_t = eps0 / beta^t,  gamma_t = kappa_gamma eps_t,  L_t = sigma2 / gamma_t  (Eq. (lischitz)),
     theta^(t) = P-APG (Fig. 2) on the gamma_t problem started from theta^(t-1) (theta~^1 = theta^0
     = theta^(t-1), t_1 = 1), theta^(0) = Theta0 (default 0), run for iters[t-1] iterations
     (the a-priori budget K_t of P:580 is the caller's), or fewer when ``stop`` = (m, infeas_tol,
     gap_tol) holds at a multiple of m: normalized infeasibility <= infeas_tol and |gap| / (N^2 - N)
-    <= gap_tol at eta(theta^k) (the stopping pair of P:1106).
+    <= gap_tol at eta(theta^k) (the stopping pair of P:1106).  ups: use the adaptive step rule
+     inside the stages with growth factor ups, s_0 = L_t at each stage start.
 
     Returns a list with one dict per stage: gamma, L, iters, Theta, y, xi (= eta(theta^(t)))."""
     X = _c64(X)
@@ -123,11 +124,15 @@ def continuation(X, ybar, sigma2, eps0, beta, kappa_gamma, iters, Theta0=None, s
     for t, K in enumerate(iters, start=1):
         gamma = kappa_gamma * eps0 / beta ** t
         L = sigma2 / gamma
-        st = dict(Tprev=Th, Tt=Th, t=1.0)
+        st = dict(Tprev=Th, Tt=Th, t=1.0, s=L)
         done = 0
         while done < K:
             m = K - done if stop is None else min(stop[0], K - done)
-            st = papg(X, ybar, gamma, L, m, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"], nthreads=nthreads)
+            if ups is None:
+                st = papg(X, ybar, gamma, L, m, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"], nthreads=nthreads)
+            else:
+                st = papg_adaptive(X, ybar, gamma, st["s"], m, ups=ups, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"],
+                                   nthreads=nthreads)
             done += m
             if stop is not None:
                 y, xi = eta(X, ybar, gamma, st["Tprev"], nthreads)

@@ -27,7 +27,8 @@ EXPORTS = (
     "cr_workspace_size", "cr_max_dim", "cr_nccl_get_unique_id", "cr_init", "cr_set_theta", "cr_get_theta",
     "cr_get_theta_rows", "cr_get_sums", "cr_dual_step", "cr_solve", "cr_primal", "cr_get_eta", "cr_lipschitz",
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
-    "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info",
+    "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info", "cr_set_gamma",
+    "cr_continuation",
 )
 
 
@@ -54,6 +55,16 @@ class CrStop(C.Structure):
 
 class CrReport(C.Structure):
     _fields_ = [("iters", C.c_int64), ("converged", C.c_int32), ("last", CrStepStats)]
+
+
+class CrCont(C.Structure):
+    _fields_ = [("eps0", C.c_double), ("beta", C.c_double), ("kappa_gamma", C.c_double), ("stages", C.c_int32),
+                ("iters", C.c_void_p), ("iters_per_stage", C.c_int64), ("stop", C.c_void_p)]
+
+
+class CrContReport(C.Structure):
+    _fields_ = [("stages_run", C.c_int32), ("iters_total", C.c_int64), ("gamma_last", C.c_double),
+                ("L_last", C.c_double), ("last", CrStepStats)]
 
 
 class CrError(RuntimeError):
@@ -97,6 +108,8 @@ def load(path: str = LIB_PATH):
         "cr_destroy": (None, [vp]),
         "cr_set_step_rule": (C.c_int, [vp, C.c_int, d, d]),
         "cr_step_info": (C.c_int, [vp, C.POINTER(d), C.POINTER(i64), C.POINTER(i64)]),
+        "cr_set_gamma": (C.c_int, [vp, d, d]),
+        "cr_continuation": (C.c_int, [vp, C.POINTER(CrCont), C.POINTER(CrContReport)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -289,6 +302,26 @@ class Solver:
         sk, tl, tt = C.c_double(), C.c_int64(), C.c_int64()
         self._check(self.lib.cr_step_info(self.h, C.byref(sk), C.byref(tl), C.byref(tt)), "cr_step_info")
         return dict(s=sk.value, trials_last=tl.value, trials_total=tt.value)
+
+    def set_gamma(self, gamma: float, L: float = 0.0):
+        """New Tikhonov weight; restarts Fig. 2 at the current iterate (cr_set_gamma)."""
+        self._check(self.lib.cr_set_gamma(self.h, float(gamma), float(L)), "cr_set_gamma")
+        self.gamma = float(gamma)
+
+    def continuation(self, eps0: float, beta: float, kappa_gamma: float, iters, report_every: int = 0,
+                     infeas_tol: float = 1e-1, gap_tol: float = 5e-7):
+        """Continuation over gamma_t = kappa_gamma eps0 / beta^t (Section 2.4.1); ``iters`` is a list of
+        per-stage budgets (one stage each)."""
+        its = np.ascontiguousarray(iters, dtype=np.int64)
+        stop = CrStop(report_every, infeas_tol, gap_tol) if report_every > 0 else None
+        p = CrCont(eps0=float(eps0), beta=float(beta), kappa_gamma=float(kappa_gamma), stages=len(its),
+                   iters=its.ctypes.data, iters_per_stage=0,
+                   stop=C.cast(C.pointer(stop), C.c_void_p) if stop is not None else None)
+        rep = CrContReport()
+        self._check(self.lib.cr_continuation(self.h, C.byref(p), C.byref(rep)), "cr_continuation")
+        self.gamma = rep.gamma_last
+        return dict(stages_run=rep.stages_run, iters_total=rep.iters_total, gamma_last=rep.gamma_last,
+                    L_last=rep.L_last, last=rep.last.as_dict())
 
     def set_pass_timing(self, on: bool):
         self._check(self.lib.cr_set_pass_timing(self.h, 1 if on else 0), "cr_set_pass_timing")

@@ -189,6 +189,7 @@ struct cr_ctx {
     cr_precision prec = CR_FP32;
     cr_kernel kernel = CR_KERNEL_SIMT;
     double gamma = 0, L = 0;
+    double sigma2 = 0;   // sigma_max(C)^2 = L gamma (Eq. (lischitz)), for cr_set_gamma
     int rank = 0, world = 1, device = 0;
     cudaStream_t stream = nullptr;
     char *ws = nullptr;
@@ -693,6 +694,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         if (s != CR_OK) return bail(s);
         ctx->L = L;
     }
+    ctx->sigma2 = ctx->L * cfg->gamma;
 
     for (int b = 0; b < Ly.nbuf; ++b) ctx->th[b] = ctx->ws + Ly.th[b];
     for (int s = 0; s < Ly.nbuf; ++s) {
@@ -1015,6 +1017,56 @@ cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *
     if (s_k) *s_k = ctx->rule == CR_STEP_ADAPTIVE ? ctx->s_cur : ctx->L;
     if (trials_last) *trials_last = ctx->rule == CR_STEP_ADAPTIVE ? ctx->trials_last : 1;
     if (trials_total) *trials_total = ctx->trials_total;
+    return CR_OK;
+}
+
+cr_status cr_set_gamma(cr_ctx *ctx, double gamma, double L) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    if (!(gamma > 0.0) || !std::isfinite(gamma) || L < 0.0 || !std::isfinite(L))
+        return fail(ctx, CR_ERR_INVALID_ARG, "cr_set_gamma: gamma must be > 0, L >= 0");
+    if (L == 0.0 && gamma > 1.0)
+        return fail(ctx, CR_ERR_INVALID_ARG, "cr_set_gamma: sigma_max(C)^2/gamma bounds the gradient only for gamma <= 1");
+    drop_graphs(ctx);                       // gamma and 1/L are baked into the captured launches
+    ctx->gamma = gamma;
+    ctx->L = L > 0.0 ? L : ctx->sigma2 / gamma;
+    if (ctx->rule == CR_STEP_ADAPTIVE) ctx->s_cur = ctx->L;     // s_0 = L_gamma
+    // restart Fig. 2 at the current iterate: theta~^1 = theta^0 := Theta^k, t_1 = 1;
+    // (t_prev, t_cur) = (1, 1) makes beta_0 = 0, so Theta^{k-1}'s buffer is not read
+    DevScalars h{};
+    h.t_prev = 1.0;
+    h.t_cur = 1.0;
+    CK(cudaMemcpyAsync(ctx->ws + ctx->lay.ts, &h, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CR_OK;
+}
+
+cr_status cr_continuation(cr_ctx *ctx, const cr_cont *p, cr_cont_report *out) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    if (!p || !(p->eps0 > 0.0) || !(p->beta > 1.0) || !(p->kappa_gamma > 0.0) || p->stages < 1 ||
+        (!p->iters && p->iters_per_stage < 0) || (p->stop && p->stop->report_every < 1))
+        return fail(ctx, CR_ERR_INVALID_ARG, "cr_continuation: bad parameters");
+    for (int32_t t = 1; t <= p->stages; ++t) {
+        const double g = p->kappa_gamma * p->eps0 / std::pow(p->beta, (double)t);
+        if (!(g > 0.0) || g > 1.0) return fail(ctx, CR_ERR_INVALID_ARG, "cr_continuation: gamma_t must be in (0, 1]");
+        if (p->iters && p->iters[t - 1] < 0) return fail(ctx, CR_ERR_INVALID_ARG, "cr_continuation: iters[t] < 0");
+    }
+    if (out) std::memset(out, 0, sizeof *out);
+    for (int32_t t = 1; t <= p->stages; ++t) {
+        // eps_t = eps0 / beta^t, gamma_t = kappa_gamma eps_t, L_t = sigma^2 / gamma_t
+        const double g = p->kappa_gamma * p->eps0 / std::pow(p->beta, (double)t);
+        if ((st = cr_set_gamma(ctx, g, 0.0)) != CR_OK) return st;
+        cr_report rep{};
+        if ((st = cr_solve(ctx, p->iters ? p->iters[t - 1] : p->iters_per_stage, p->stop, &rep)) != CR_OK) return st;
+        if (out) {
+            out->stages_run = t;
+            out->iters_total += rep.iters;
+            out->gamma_last = ctx->gamma;
+            out->L_last = ctx->L;
+        }
+    }
+    if (out) return eval_stats(ctx, &out->last);
     return CR_OK;
 }
 
