@@ -157,31 +157,6 @@ void slot_tables(int G, int64_t T, int nRB, int nCB, std::vector<int> &slot0, st
     if (slots.empty()) slots.push_back(0);
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-// 2-D tensor map over one Theta buffer (Rp rows x ldT fp32 columns), 128-B swizzled boxes of
-// 32 columns x 128 rows (the tensor-core pass tile).
-bool make_theta_tmap(CUtensorMap *m, void *base, int64_t rows, int64_t ldT) {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !p)
-            return false;
-        fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
-    const cuuint64_t dims[2] = {(cuuint64_t)ldT, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)ldT * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)kTcBN, (cuuint32_t)kTcBM};
-    const cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 }  // namespace
 
 struct cr_ctx {
@@ -218,7 +193,6 @@ struct cr_ctx {
     cudaGraphExec_t graph[9] = {};
     cudaStream_t cap_stream = nullptr;   // private stream used only to record graphs
     // tensor-core pass
-    CUtensorMap tm[3];
     int G_tc = 0, stages = 0, g1stages = 0, g2stages = 0, window = 64, smem_tc = 0;
     int64_t T_tc = 0;
     unsigned long long *trace = nullptr;   // debug timeline buffer (CR_TC_TRACE=<file>)
@@ -267,6 +241,8 @@ PassParams pass_params(cr_ctx *ctx, int b_read, int b_read2, int b_out = -1, boo
     p.Bout = ctx->th[b_out < 0 ? b_read2 : b_out];
     p.adapt = adapt ? 1 : 0;
     p.dcol = Ly.n + 1;
+    p.tiled = Ly.tc ? 1 : 0;
+    p.nCBt = Ly.nCBtc;
     p.ldT = Ly.ldT;
     p.N = Ly.N;
     p.Ns = Ly.Ns;
@@ -347,9 +323,12 @@ SmallParams small_params(cr_ctx *ctx, int sa, int sb, int use_beta, double scale
     return p;
 }
 
-TcParams tc_params(cr_ctx *ctx, bool adapt = false) {
+TcParams tc_params(cr_ctx *ctx, int b1, int b2, int bo, bool adapt = false) {
     const Layout &Ly = ctx->lay;
     TcParams p{};
+    p.B1 = static_cast<const float *>(ctx->th[b1]);
+    p.B2 = static_cast<const float *>(ctx->th[b2]);
+    p.Bout = static_cast<float *>(ctx->th[bo]);
     p.N = Ly.N;
     p.Ns = Ly.Ns;
     p.row0 = Ly.row0;
@@ -425,8 +404,8 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
         CK(cudaEventRecord(e0, ctx->stream));
     }
     if (Ly.tc) {
-        TcParams tp = tc_params(ctx, adapt);
-        CK(launch_pass_tc(ctx->tm[bA], ctx->tm[bB], ctx->tm[bo], tp, ctx->stream));
+        TcParams tp = tc_params(ctx, bA, bB, bo, adapt);
+        CK(launch_pass_tc(tp, ctx->stream));
     } else {
         PassParams p = pass_params(ctx, bA, bB, bo, adapt);
         CK(launch_pass_simt(p, Ly.fp64, Ly.NB, MODE_STEP, ctx->stream));
@@ -519,6 +498,8 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     ResidualParams rp{};
     rp.Theta = ctx->th[b];
     rp.ldT = Ly.ldT;
+    rp.tiled = Ly.tc ? 1 : 0;
+    rp.nCBt = Ly.nCBtc;
     rp.N = Ly.N;
     rp.Ns = Ly.Ns;
     rp.row0 = Ly.row0;
@@ -741,9 +722,9 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         ctx->T_tc = (int64_t)Ly.nRBtc * Ly.nCBtc;
         ctx->G_tc = (int)std::min<int64_t>({ctx->T_tc, (int64_t)nsm, (int64_t)kGMax});
         // Theta ring: 32 KB slots (B1, B2 tiles, 1024-B aligned for the 128-B swizzle); X_J and
-        // X_J^T image rings (hi + lo per slot).  Defaults: 4 Theta slots and 3 + 3 image slots,
-        // reduced (images first, not below 2) until they fit.  CR_TC_STAGES / CR_TC_G1STAGES /
-        // CR_TC_G2STAGES override.
+        // X_J^T image rings (hi + lo per slot).  Defaults: 5 Theta slots and 3 + 3 image slots,
+        // reduced (images first, not below 2, then Theta slots) until they fit: C4 5/3/2, C5 4/2/2.
+        // CR_TC_STAGES / CR_TC_G1STAGES / CR_TC_G2STAGES override.
         const size_t tb = 2 * (size_t)kTcBM * kTcBN * 4, b1 = 2 * (size_t)Ly.NK * 128, b2 = 2 * (size_t)Ly.NP2 * 128;
         const size_t fixed = tc_barrier_bytes() + 1024 + 64;
         const size_t budget = 227 * 1024 - fixed;
@@ -751,7 +732,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
             const char *e = std::getenv(k);
             return e ? std::max(2, std::min(kTcMaxStages, std::atoi(e))) : d;
         };
-        int st = env_int("CR_TC_STAGES", 4), s1 = env_int("CR_TC_G1STAGES", 3), s2 = env_int("CR_TC_G2STAGES", 3);
+        int st = env_int("CR_TC_STAGES", 5), s1 = env_int("CR_TC_G1STAGES", 3), s2 = env_int("CR_TC_G2STAGES", 3);
         auto bytes = [&]() { return st * tb + s1 * b1 + s2 * b2; };
         while (bytes() > budget && (s1 > 2 || s2 > 2)) {
             if (s1 * b1 >= s2 * b2 && s1 > 2) --s1;
@@ -781,11 +762,6 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
             IK(cudaMalloc(&ctx->trace, 5 * 256 * 8 * 8));
             IK(cudaMemsetAsync(ctx->trace, 0, 5 * 256 * 8 * 8, ctx->stream));
         }
-        for (int b = 0; b < Ly.nbuf; ++b)
-            if (!make_theta_tmap(&ctx->tm[b], ctx->th[b], Ly.Rp, Ly.ldT)) {
-                fail(ctx, CR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-                return bail(CR_ERR_CUDA);
-            }
     }
     IK(cudaStreamSynchronize(ctx->stream));   // host vectors go out of scope
 #undef IK
@@ -823,7 +799,16 @@ cr_status cr_set_theta(cr_ctx *ctx, const double *tk1, const double *tk2, double
     drop_graphs(ctx);
     for (int b = 0; b < 2; ++b) {
         CK(cudaMemsetAsync(ctx->th[b], 0, (size_t)Ly.Rp * Ly.ldT * Ly.es, ctx->stream));
-        if (src[b] && Ly.Ns > 0) {
+        if (src[b] && Ly.Ns > 0 && Ly.tc) {
+            // tile-major fp32 image of this rank's rows (theta_off), zero padding, one copy
+            const size_t tiles = (size_t)Ly.nRBtc * Ly.nCBtc;
+            std::vector<float> tmp(tiles * (size_t)kTcBM * kTcBN, 0.f);
+            for (int64_t i = 0; i < Ly.Ns; ++i)
+                for (int64_t j = 0; j < Ly.N; ++j)
+                    tmp[(size_t)theta_off(i, j, Ly.ldT, 1, Ly.nCBtc)] = (float)src[b][i * Ly.N + j];
+            CK(cudaMemcpyAsync(ctx->th[b], tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        } else if (src[b] && Ly.Ns > 0) {
             if (Ly.fp64) {
                 CK(cudaMemcpy2DAsync(ctx->th[b], Ly.ldT * 8, src[b], Ly.N * 8, Ly.N * 8, Ly.Ns,
                                      cudaMemcpyHostToDevice, ctx->stream));
@@ -853,6 +838,19 @@ cr_status cr_set_theta(cr_ctx *ctx, const double *tk1, const double *tk2, double
 static cr_status read_buffer(cr_ctx *ctx, int b, int64_t row0, int64_t nrows, double *out) {
     const Layout &Ly = ctx->lay;
     if (nrows <= 0) return CR_OK;
+    if (Ly.tc) {
+        // tile-major: the row blocks covering the rows are contiguous (row-block-major tiles)
+        const int64_t rb0 = row0 / kTcBM, rb1 = (row0 + nrows - 1) / kTcBM;
+        const size_t per_rb = (size_t)Ly.nCBtc * kTcBM * kTcBN;
+        std::vector<float> tmp((size_t)(rb1 - rb0 + 1) * per_rb);
+        CK(cudaMemcpyAsync(tmp.data(), static_cast<const float *>(ctx->th[b]) + rb0 * per_rb, tmp.size() * 4,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int64_t i = 0; i < nrows; ++i)
+            for (int64_t j = 0; j < Ly.N; ++j)
+                out[i * Ly.N + j] = tmp[(size_t)theta_off(row0 + i - rb0 * kTcBM, j, Ly.ldT, 1, Ly.nCBtc)];
+        return CR_OK;
+    }
     const char *src = static_cast<const char *>(ctx->th[b]) + (size_t)row0 * Ly.ldT * Ly.es;
     if (Ly.fp64) {
         CK(cudaMemcpy2DAsync(out, Ly.N * 8, src, Ly.ldT * 8, Ly.N * 8, nrows, cudaMemcpyDeviceToHost,

@@ -19,6 +19,19 @@ constexpr int kTcBM = 128;        // tensor-core pass tile rows (TMEM lanes)
 constexpr int kTcBN = 32;         // tensor-core pass tile columns
 constexpr int kTcMaxStages = 6;
 
+// Element (i, j) of a Theta buffer (local row i, column j), in elements from the buffer base.
+//   row-major (SIMT configs): i * ldT + j
+//   tile-major (tensor-core configs): 128 x 32 tiles of 16 KB, each contiguous, tiles in
+//   row-block-major order (nCBt tiles per row block); inside a tile row r (128 B) the 16-B chunk
+//   q = (j % 32) / 4 sits at position q ^ (r % 8) -- exactly the 128-B-swizzled shared-memory
+//   image of the tile, so one 16-KB bulk copy moves a tile between HBM and the pass's smem.
+__host__ __device__ inline int64_t theta_off(int64_t i, int64_t j, int64_t ldT, int tiled, int nCBt) {
+    if (!tiled) return i * ldT + j;
+    const int64_t rb = i >> 7, cb = j >> 5;
+    const int r = (int)(i & 127), c = (int)(j & 31);
+    return ((rb * nCBt + cb) << 12) + (r << 5) + ((((c >> 2) ^ (r & 7))) << 2) + (c & 3);
+}
+
 // n-buckets compiled for the SIMT pass (S-GEMM depth NB; P-GEMM width NBP = NB + 4).
 int simt_bucket(int n);           // smallest compiled NB >= n, or 0 if none
 
@@ -33,6 +46,7 @@ struct PassParams {
     const void *B1;        // Theta^{k-1} (read)
     void *B2;              // Theta^{k-2} (read)
     void *Bout;            // Theta^k (MODE_STEP): B2 (in place) or a third buffer (adaptive step)
+    int tiled, nCBt;       // Theta layout (theta_off)
     int adapt;             // 1: row partial column n+1 receives sum_j (Theta^k - theta~)^2
     int dcol;              // that column (n + 1 < NBP)
     int64_t ldT;           // row pitch of Theta, XT, colpart (elements)
@@ -113,8 +127,9 @@ struct AdaptParams {
 cudaError_t launch_adapt_check(const AdaptParams &p, cudaStream_t s);
 
 struct ResidualParams {
-    const void *Theta;     // [Rp][ldT] storage precision
+    const void *Theta;     // storage precision, layout theta_off(tiled, nCBt)
     int64_t ldT, N, Ns, row0, Rp;
+    int tiled, nCBt;
     int n;
     const double *X64, *y64, *Xi64, *a64;
     double *statpart;      // [kStatBlocks][8]
@@ -129,6 +144,8 @@ cudaError_t launch_stats_finalize(const double *pro, int nb_pro, const double *r
                                   DevScalars *ts, cudaStream_t s);
 
 struct TcParams {
+    const float *B1, *B2;            // Theta^{k-1}, Theta^{k-2} (tile-major, theta_off)
+    float *Bout;                     // Theta^k
     int64_t N, Ns, row0, ldT, T;
     int G, nCB, NK, NP2, stages, window;
     int g1stages, g2stages;          // X_J / X_J^T image ring slots
@@ -147,8 +164,7 @@ struct TcParams {
 };
 
 // tcgen05 fused pass (kernels/pass_tc.cu).
-cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const CUtensorMap &tmOut, const TcParams &p,
-                           cudaStream_t s);
+cudaError_t launch_pass_tc(const TcParams &p, cudaStream_t s);
 cudaError_t pass_tc_prepare(int NK, int smem_bytes);
 size_t tc_barrier_bytes();
 cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,

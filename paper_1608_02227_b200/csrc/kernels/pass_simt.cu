@@ -148,11 +148,18 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
     // Theta tile loads for this thread's 4x4 block
     auto load_theta = [&](int64_t t, T (&b1)[4][4], T (&b2)[4][4]) {
         int64_t rb = t / p.nCB, cb = t % p.nCB;
-        const int64_t base = (rb * BM + ty * 4) * ldT + cb * BN + tx * 4;
+        // tile-major buffers hold nCBt * 32 columns (<= the 64-column grid): beyond is zero
+        const bool in = !p.tiled || cb * BN + tx * 4 < (int64_t)p.nCBt * 32;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            ld4cs(B1 + base + r * ldT, b1[r]);
-            if (MODE == MODE_STEP) ld4cs(B2 + base + r * ldT, b2[r]);
+            if (in) {
+                const int64_t o = theta_off(rb * BM + ty * 4 + r, cb * BN + tx * 4, ldT, p.tiled, p.nCBt);
+                ld4cs(B1 + o, b1[r]);
+                if (MODE == MODE_STEP) ld4cs(B2 + o, b2[r]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { b1[r][c] = T(0); b2[r][c] = T(0); }
+            }
         }
     };
 
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
                         dacc[r] = fma(d, d, dacc[r]);
                     }
                 }
-                st4cs(Bout + lr * ldT + gj0, th[r]);
+                if (!p.tiled || gj0 < (int64_t)p.nCBt * 32) st4cs(Bout + theta_off(lr, gj0, ldT, p.tiled, p.nCBt), th[r]);
             }
         } else {
 #pragma unroll

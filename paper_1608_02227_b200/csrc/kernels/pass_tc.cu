@@ -83,8 +83,7 @@ struct Cursor {
 
 template <int NK>
 __global__ void __launch_bounds__(NTHR, 1)
-pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
-               const __grid_constant__ CUtensorMap tmOut, const TcParams p) {
+pass_tc_kernel(const TcParams p) {
     constexpr int NP2 = (NK + 15) / 16 * 16;           // GEMM2 N (multiple of 16 for M = 128)
     extern __shared__ __align__(16) uint8_t smem_raw[];
     // 1024-byte alignment by offsetting the shared pointer itself (an integer round trip would
@@ -177,7 +176,6 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(&bar->tmem_base, 512);
-    if (warp == 0 && lane == 0) { prefetch_tmap(&tmB1); prefetch_tmap(&tmB2); prefetch_tmap(&tmOut); }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -198,8 +196,11 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                     uint8_t *st = stage_ptr(c.s);
                     uint64_t *fb = &bar->full[c.s];
                     mbar_arrive_expect_tx(fb, 2 * TILE_BYTES + TBN * 4);
-                    tma_load_2d(st, &tmB1, c.cb * TBN, c.rb * TBM, fb, pol_stream);
-                    tma_load_2d(st + TILE_BYTES, &tmB2, c.cb * TBN, c.rb * TBM, fb, pol_stream);
+                    // tile-major Theta: each 128 x 32 tile is 16 KB contiguous, already in the
+                    // 128-B-swizzled smem image (theta_off): one bulk copy per tile
+                    const size_t toff = ((size_t)c.rb * nCB + c.cb) * (TILE_BYTES / 4);
+                    bulk_load(st, p.B1 + toff, TILE_BYTES, fb, pol_stream);
+                    bulk_load(st + TILE_BYTES, p.B2 + toff, TILE_BYTES, fb, pol_stream);
                     bulk_load(yring + c.s * 128, p.yv + c.cb * TBN, TBN * 4, fb, pol_keep);
                     adv(c, 1);
                 }
@@ -312,7 +313,8 @@ pass_tc_kernel(const __grid_constant__ CUtensorMap tmB1, const __grid_constant__
                 TC_TRACE(2, c.u, 0);
                 mbar_wait(&bar->st_full[c.s], (uint32_t)c.ph);
                 TC_TRACE(2, c.u, 1);
-                tma_store_2d(&tmOut, c.cb * TBN, c.rb * TBM, stage_ptr(c.s) + TILE_BYTES, pol_stream);
+                bulk_store(p.Bout + ((size_t)c.rb * nCB + c.cb) * (TILE_BYTES / 4), stage_ptr(c.s) + TILE_BYTES,
+                           TILE_BYTES, pol_stream);
                 bulk_commit();
                 bulk_wait_read<0>();                      // slot read by the store engine
                 TC_TRACE(2, c.u, 2);
@@ -573,10 +575,9 @@ __global__ void tc_images_kernel(const double *X64, int64_t N, int n, int NK, in
 
 #define CR_TC_NK_LIST(X) X(8) X(16) X(24) X(32) X(40) X(48) X(56) X(64) X(72) X(80)
 
-cudaError_t launch_pass_tc(const CUtensorMap &tmB1, const CUtensorMap &tmB2, const CUtensorMap &tmOut, const TcParams &p,
-                           cudaStream_t s) {
+cudaError_t launch_pass_tc(const TcParams &p, cudaStream_t s) {
     switch (p.NK) {
-#define CR_CASE(V) case V: pass_tc_kernel<V><<<p.G, NTHR, p.smem_bytes, s>>>(tmB1, tmB2, tmOut, p); break;
+#define CR_CASE(V) case V: pass_tc_kernel<V><<<p.G, NTHR, p.smem_bytes, s>>>(p); break;
         CR_TC_NK_LIST(CR_CASE)
 #undef CR_CASE
         default: return cudaErrorInvalidValue;

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) residual_kernel(const ResidualParams p) {
             double s = 0.0;
             for (int d = 0; d < p.n; ++d) s = fma(xis[ii * p.n + d], xs[d * RBN + c], s);
             const double R = yj + ab[ii] - s;              // y_j - y_i + a_i - xi_i . x_j
-            gap += (double)Th[i * p.ldT + j] * R;
+            gap += (double)Th[theta_off(i, j, p.ldT, p.tiled, p.nCBt)] * R;
             if (R < 0.0) { v2 += R * R; vmax = fmax(vmax, -R); }
         }
     }
