@@ -88,6 +88,7 @@ typedef enum {
                                Theta^{k-2}); +1 Theta matrix of workspace                       */
 
 typedef struct cr_ctx cr_ctx;
+typedef struct cr_group cr_group;   /* in-process group of world contexts sharing one GPU */
 
 typedef struct {
     int64_t N;                  /* observations, N >= 2                                       */
@@ -106,6 +107,9 @@ typedef struct {
     void *workspace;            /* DEVICE memory, >= cr_workspace_size(...) bytes, caller-owned */
     size_t workspace_bytes;
     int32_t flags;              /* CR_FLAG_* (0: constant step only)                           */
+    cr_group *local_group;      /* world > 1 without NCCL: all ranks are contexts of ONE process
+                                   (one host thread each, same or different GPUs) joined by
+                                   cr_local_group_create(world); NULL -> NCCL via nccl_unique_id */
 } cr_config;
 
 /* Diagnostics of eta(Theta^k) (Theorem 1 semantics) reported per P:951 / P:1106. */
@@ -138,6 +142,15 @@ size_t cr_workspace_size(int64_t N, int32_t n, cr_precision prec, cr_kernel kern
 
 /* Largest n this library was built for. */
 int32_t cr_max_dim(void);
+
+/* In-process group for world > 1 contexts driven by `world` host threads of one process
+ * (tests run the row-sharded path on one GPU this way).  Its collectives are host rendezvous
+ * of the rank threads plus cross-stream event dependencies, copies and a fixed-order sum
+ * kernel -- no kernel ever waits on another.  CUDA graphs are not used by contexts in a local
+ * group.  A rank that does not arrive within 120 s breaks the group (CR_ERR_NCCL).
+ * 1 <= world <= 16.  Destroy after all member contexts. */
+cr_status cr_local_group_create(int32_t world, cr_group **out);
+void cr_local_group_destroy(cr_group *g);
 
 /* world > 1 bootstrap: write a fresh 128-byte ncclUniqueId into out (host memory).  Rank 0
  * calls this and broadcasts the bytes to the other ranks (e.g. over torch.distributed). */

@@ -5,7 +5,7 @@ The product is libcr.so (C ABI, include/cr.h) built from ``csrc/``; ``binding`` 
 ctypes layer over it.  See DESIGN.md.
 """
 from .binding import (  # noqa: F401
-    CrError, Solver, load, lipschitz_host, nccl_unique_id, workspace_size, EXPORTS,
+    CrError, LocalGroup, Solver, load, lipschitz_host, nccl_unique_id, workspace_size, EXPORTS,
 )
 
-__all__ = ["CrError", "Solver", "load", "lipschitz_host", "nccl_unique_id", "workspace_size", "EXPORTS"]
+__all__ = ["CrError", "LocalGroup", "Solver", "load", "lipschitz_host", "nccl_unique_id", "workspace_size", "EXPORTS"]

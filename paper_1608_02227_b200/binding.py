@@ -28,7 +28,7 @@ EXPORTS = (
     "cr_get_theta_rows", "cr_get_sums", "cr_dual_step", "cr_solve", "cr_primal", "cr_get_eta", "cr_lipschitz",
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
     "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info", "cr_set_gamma",
-    "cr_continuation",
+    "cr_continuation", "cr_local_group_create", "cr_local_group_destroy",
 )
 
 
@@ -37,7 +37,7 @@ class CrConfig(C.Structure):
                 ("gamma", C.c_double), ("L", C.c_double), ("prec", C.c_int), ("kernel", C.c_int),
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t), ("flags", C.c_int32)]
+                ("workspace_bytes", C.c_size_t), ("flags", C.c_int32), ("local_group", C.c_void_p)]
 
 
 class CrStepStats(C.Structure):
@@ -109,6 +109,8 @@ def load(path: str = LIB_PATH):
         "cr_set_step_rule": (C.c_int, [vp, C.c_int, d, d]),
         "cr_step_info": (C.c_int, [vp, C.POINTER(d), C.POINTER(i64), C.POINTER(i64)]),
         "cr_set_gamma": (C.c_int, [vp, d, d]),
+        "cr_local_group_create": (C.c_int, [i32, C.POINTER(vp)]),
+        "cr_local_group_destroy": (None, [vp]),
         "cr_continuation": (C.c_int, [vp, C.POINTER(CrCont), C.POINTER(CrContReport)]),
     }
     for name, (res, args) in sig.items():
@@ -169,6 +171,33 @@ def broadcast_unique_id(group, device=None) -> bytes:
     return bytes(t.cpu().tolist())
 
 
+class LocalGroup:
+    """In-process group of `world` ranks (cr_local_group_create): every rank is a Solver of this
+    process, driven by its own host thread, all on one GPU (or several).  Used to run the
+    row-sharded path -- all-gather of y, reduce-scatter of the column sums, scalar
+    all-reduces -- end to end on a single B200.  Destroy (close) after the member Solvers."""
+
+    def __init__(self, world: int):
+        self.lib = load()
+        self.world = int(world)
+        h = C.c_void_p()
+        st = self.lib.cr_local_group_create(self.world, C.byref(h))
+        if st != CR_OK:
+            raise CrError(f"cr_local_group_create({world}): status {st}")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cr_local_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Solver:
     """One rank's share of the smoothed-dual P-APG solve (Fig. 2).
 
@@ -178,7 +207,7 @@ class Solver:
     """
 
     def __init__(self, X, ybar, gamma, L=0.0, prec="fp32", kernel="auto", device=None, stream=None,
-                 group=None, adaptive=False):
+                 group=None, adaptive=False, rank=None):
         import torch
         if not torch.cuda.is_available():
             raise CrError("libcr needs a CUDA device (no CPU fallback)")
@@ -192,7 +221,11 @@ class Solver:
         self.device = dev
         self.rank, self.world = 0, 1
         uid = None
-        if group is not None:
+        local = None
+        if isinstance(group, LocalGroup):
+            local = group
+            self.world, self.rank = group.world, int(rank)
+        elif group is not None:
             import torch.distributed as dist
             self.world = dist.get_world_size(group)
             self.rank = dist.get_rank(group)
@@ -210,7 +243,8 @@ class Solver:
                        L=float(L), prec=PREC[prec], kernel=KERNEL[kernel], rank=self.rank, world=self.world,
                        nccl_unique_id=C.cast(uid, C.c_void_p) if uid is not None else None,
                        device=dev.index, stream=self.stream.cuda_stream,
-                       workspace=self.workspace.data_ptr(), workspace_bytes=nbytes, flags=flags)
+                       workspace=self.workspace.data_ptr(), workspace_bytes=nbytes, flags=flags,
+                       local_group=local.h if local is not None else None)
         h = C.c_void_p()
         st = self.lib.cr_init(C.byref(cfg), C.byref(h))
         if st != CR_OK:

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/cr.h"
+#include "comm.h"
 #include "cr_internal.h"
 
 namespace cr {
@@ -196,7 +197,7 @@ struct cr_ctx {
     int G_tc = 0, stages = 0, g1stages = 0, g2stages = 0, window = 64, smem_tc = 0;
     int64_t T_tc = 0;
     unsigned long long *trace = nullptr;   // debug timeline buffer (CR_TC_TRACE=<file>)
-    ncclComm_t comm = nullptr;
+    Comm comm;           // NCCL communicator or in-process local group (world > 1)
 
     template <typename P> P *at(size_t off) { return reinterpret_cast<P *>(ws + off); }
 };
@@ -223,15 +224,11 @@ cr_status fail(cr_ctx *c, cr_status s, const char *fmt, ...) {
             return fail(ctx, CR_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,           \
                         cudaGetErrorString(e_));                                               \
     } while (0)
-#define NK(call)                                                                               \
+#define CM(call)                                                                               \
     do {                                                                                       \
-        ncclResult_t r_ = (call);                                                              \
-        if (r_ != ncclSuccess)                                                                 \
-            return fail(ctx, CR_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,           \
-                        ncclGetErrorString(r_));                                               \
+        const char *m_ = (call);                                                               \
+        if (m_) return fail(ctx, CR_ERR_NCCL, "%s:%d %s", __FILE__, __LINE__, m_);             \
     } while (0)
-
-ncclDataType_t nccl_t(const cr_ctx *ctx) { return ctx->lay.fp64 ? ncclFloat64 : ncclFloat32; }
 
 PassParams pass_params(cr_ctx *ctx, int b_read, int b_read2, int b_out = -1, bool adapt = false) {
     const Layout &Ly = ctx->lay;
@@ -377,8 +374,7 @@ cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
     ctx->launches += 2;
     if (ctx->world > 1)
-        NK(ncclReduceScatter(ctx->at<double>(Ly.cfull), ctx->c[s], (size_t)Ly.S, ncclFloat64, ncclSum,
-                             ctx->comm, ctx->stream));
+        CM(comm_reduce_scatter_f64(ctx->comm, ctx->at<double>(Ly.cfull), ctx->c[s], (size_t)Ly.S, ctx->stream));
     return CR_OK;
 }
 
@@ -392,9 +388,7 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     SmallParams sp = small_params(ctx, bA, bB, 1, scale, false);
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
     if (ctx->world > 1) {
-        char *yv = ctx->ws + Ly.yv;
-        NK(ncclAllGather(yv + (size_t)ctx->rank * Ly.S * Ly.es, yv, (size_t)Ly.S, nccl_t(ctx), ctx->comm,
-                         ctx->stream));
+        CM(comm_allgather(ctx->comm, ctx->ws + Ly.yv, (size_t)Ly.S, (int)Ly.es, ctx->stream));
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (allow_timing && ctx->timing) {
@@ -414,8 +408,7 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     ReduceParams q = reduce_params(ctx, bo, advance_t ? 1 : 0, Ly.tc, adapt);
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
     if (ctx->world > 1)
-        NK(ncclReduceScatter(ctx->at<double>(Ly.cfull), ctx->c[bo], (size_t)Ly.S, ncclFloat64, ncclSum,
-                             ctx->comm, ctx->stream));
+        CM(comm_reduce_scatter_f64(ctx->comm, ctx->at<double>(Ly.cfull), ctx->c[bo], (size_t)Ly.S, ctx->stream));
     ctx->launches += 3;
     return CR_OK;
 }
@@ -462,7 +455,7 @@ cr_status adaptive_step(cr_ctx *ctx) {
         ap.ts = ts;
         CK(launch_adapt_check(ap, ctx->stream));
         ctx->launches += 2;
-        if (ctx->world > 1) NK(ncclAllReduce(ts->stats + 8, ts->stats + 8, 2, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+        if (ctx->world > 1) CM(comm_allreduce_f64(ctx->comm, ts->stats + 8, 2, COLL_SUM, ctx->stream));
         double qd[2];
         CK(cudaMemcpyAsync(qd, ts->stats + 8, sizeof qd, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -492,9 +485,7 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     SmallParams sp = small_params(ctx, s, s, 0, 1.0, true);
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, &nb_pro));
     double *y64 = ctx->at<double>(Ly.y64);
-    if (ctx->world > 1)
-        NK(ncclAllGather(y64 + (size_t)ctx->rank * Ly.S, y64, (size_t)Ly.S, ncclFloat64, ctx->comm,
-                         ctx->stream));
+    if (ctx->world > 1) CM(comm_allgather(ctx->comm, y64, (size_t)Ly.S, 8, ctx->stream));
     ResidualParams rp{};
     rp.Theta = ctx->th[b];
     rp.ldT = Ly.ldT;
@@ -517,11 +508,9 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     ctx->launches += 3;
     if (ctx->world > 1) {
         // stats[0..5] and [7] are sums; [6] is a max
-        NK(ncclGroupStart());
-        NK(ncclAllReduce(ts->stats, ts->stats, 6, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
-        NK(ncclAllReduce(ts->stats + 6, ts->stats + 6, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream));
-        NK(ncclAllReduce(ts->stats + 7, ts->stats + 7, 1, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
-        NK(ncclGroupEnd());
+        CM(comm_allreduce_f64(ctx->comm, ts->stats, 6, COLL_SUM, ctx->stream));
+        CM(comm_allreduce_f64(ctx->comm, ts->stats + 6, 1, COLL_MAX, ctx->stream));
+        CM(comm_allreduce_f64(ctx->comm, ts->stats + 7, 1, COLL_SUM, ctx->stream));
     }
     DevScalars h{};
     CK(cudaMemcpyAsync(&h, ts, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
@@ -604,6 +593,14 @@ const char *cr_last_error(const cr_ctx *ctx) { return ctx ? ctx->err.c_str() : "
 
 int32_t cr_max_dim(void) { return 80; }
 
+cr_status cr_local_group_create(int32_t world, cr_group **out) {
+    if (!out) return CR_ERR_INVALID_ARG;
+    *out = reinterpret_cast<cr_group *>(local_group_create(world));
+    return *out ? CR_OK : CR_ERR_INVALID_ARG;
+}
+
+void cr_local_group_destroy(cr_group *g) { local_group_destroy(reinterpret_cast<LocalGroup *>(g)); }
+
 cr_status cr_nccl_get_unique_id(void *out) {
     if (!out) return CR_ERR_INVALID_ARG;
     ncclUniqueId id;
@@ -635,7 +632,9 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         return CR_ERR_INVALID_ARG;
     if (cfg->L == 0.0 && cfg->gamma > 1.0) return CR_ERR_INVALID_ARG;  // sigma^2/gamma bounds only for gamma<=1
     if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return CR_ERR_INVALID_ARG;
-    if (cfg->world > 1 && !cfg->nccl_unique_id) return CR_ERR_INVALID_ARG;
+    if (cfg->world > 1 && !cfg->nccl_unique_id && !cfg->local_group) return CR_ERR_INVALID_ARG;
+    if (cfg->local_group && local_group_world(reinterpret_cast<const LocalGroup *>(cfg->local_group)) != cfg->world)
+        return CR_ERR_INVALID_ARG;
     if (cfg->prec != CR_FP32 && cfg->prec != CR_FP64) return CR_ERR_INVALID_ARG;
     if (cfg->prec == CR_FP64 && cfg->kernel == CR_KERNEL_TC) return CR_ERR_UNSUPPORTED;
     if (cfg->n > cr_max_dim()) return CR_ERR_UNSUPPORTED;
@@ -765,10 +764,14 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     }
     IK(cudaStreamSynchronize(ctx->stream));   // host vectors go out of scope
 #undef IK
-    if (ctx->world > 1) {
+    ctx->comm.rank = ctx->rank;
+    ctx->comm.world = ctx->world;
+    if (ctx->world > 1 && cfg->local_group) {
+        ctx->comm.local = reinterpret_cast<LocalGroup *>(cfg->local_group);
+    } else if (ctx->world > 1) {
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
-        ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+        ncclResult_t r = ncclCommInitRank(&ctx->comm.nccl, ctx->world, id, ctx->rank);
         if (r != ncclSuccess) {
             fail(ctx, CR_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
             return bail(CR_ERR_NCCL);
@@ -919,7 +922,8 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
     if (max_iters < 0 || (stop && stop->report_every < 1))
         return fail(ctx, CR_ERR_INVALID_ARG, "cr_solve: bad arguments");
     if (out) std::memset(out, 0, sizeof *out);
-    const bool use_graph = !ctx->timing;
+    // no graphs with the in-process local group: its collectives are host rendezvous
+    const bool use_graph = !ctx->timing && !ctx->comm.local;
     const double Nd = (double)ctx->lay.N;
     int64_t it = 0;
     while (it < max_iters) {
@@ -968,7 +972,7 @@ cr_status cr_get_eta(cr_ctx *ctx, double *y, double *xi) {
     double *y64 = ctx->at<double>(Ly.y64);
     if (y && ctx->world > 1) {
         // make sure all ranks' rows are present (eta of a plain step is only local until gathered)
-        NK(ncclAllGather(y64 + (size_t)ctx->rank * Ly.S, y64, (size_t)Ly.S, ncclFloat64, ctx->comm, ctx->stream));
+        CM(comm_allgather(ctx->comm, y64, (size_t)Ly.S, 8, ctx->stream));
     }
     if (y) CK(cudaMemcpyAsync(y, y64, (size_t)Ly.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
     if (xi && Ly.Ns > 0)
@@ -1104,7 +1108,7 @@ void cr_destroy(cr_ctx *ctx) {
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->trace) cudaFree(ctx->trace);
     for (auto e : ctx->ev) cudaEventDestroy(e);
-    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->comm.nccl) ncclCommDestroy(ctx->comm.nccl);
     delete ctx;
 }
 
