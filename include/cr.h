@@ -254,6 +254,14 @@ typedef struct {
 
 cr_status cr_continuation(cr_ctx *ctx, const cr_cont *params, cr_cont_report *out);
 
+/* The fitted estimator at query points: with (y, xi) = eta(Theta^k) (Theorem 1,
+ * P:243), f_hat(z) = max_i  y_i + xi_i^T (z - x_i), the max-affine function the pair
+ * constraints certify (it interpolates y when every constraint holds).  Z: HOST, M x n
+ * row-major; out: HOST, M.  fp64 on the device; with world > 1 each rank maximises over its
+ * rows and the ranks all-reduce (max), so every rank returns the full result.  Synchronizes.
+ * Errors: CR_ERR_INVALID_ARG (M < 0, NULL pointers with M > 0, non-finite Z). */
+cr_status cr_predict(cr_ctx *ctx, const double *Z, int64_t M, double *out);
+
 /* Step constant in use (L_gamma of the current gamma). */
 double cr_lipschitz(const cr_ctx *ctx);
 

@@ -195,3 +195,18 @@ def sigma_max_sq(X, form="auto", tol=1e-13):
 def lipschitz(X, gamma, form="auto"):
     """L_gamma = sigma_max^2(C) / gamma (Eq. (lischitz) P:375)."""
     return sigma_max_sq(X, form) / gamma
+
+
+# ---------------------------------------------------------------------------
+# The fitted estimator (P:66-72, Eq. (original) and the piecewise-linear interpolant it
+# certifies): a feasible (y, xi) defines the max-affine function
+#     f_hat(z) = max_i  y_i + xi_i^T (z - x_i),
+# which interpolates y at the data points when every pair constraint holds.
+# ---------------------------------------------------------------------------
+def predict(X, y, xi, Z):
+    """f_hat at the rows of Z (M x n), written out as the definition (fp64)."""
+    X, y, xi, Z = (np.asarray(a, dtype=np.float64) for a in (X, y, xi, Z))
+    out = np.empty(Z.shape[0])
+    for m in range(Z.shape[0]):
+        out[m] = np.max(y + np.einsum("ij,ij->i", xi, Z[m][None, :] - X))
+    return out

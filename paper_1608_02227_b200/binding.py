@@ -28,7 +28,7 @@ EXPORTS = (
     "cr_get_theta_rows", "cr_get_sums", "cr_dual_step", "cr_solve", "cr_primal", "cr_get_eta", "cr_lipschitz",
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
     "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info", "cr_set_gamma",
-    "cr_continuation", "cr_local_group_create", "cr_local_group_destroy",
+    "cr_continuation", "cr_local_group_create", "cr_local_group_destroy", "cr_predict",
 )
 
 
@@ -109,6 +109,7 @@ def load(path: str = LIB_PATH):
         "cr_set_step_rule": (C.c_int, [vp, C.c_int, d, d]),
         "cr_step_info": (C.c_int, [vp, C.POINTER(d), C.POINTER(i64), C.POINTER(i64)]),
         "cr_set_gamma": (C.c_int, [vp, d, d]),
+        "cr_predict": (C.c_int, [vp, vp, i64, vp]),
         "cr_local_group_create": (C.c_int, [i32, C.POINTER(vp)]),
         "cr_local_group_destroy": (None, [vp]),
         "cr_continuation": (C.c_int, [vp, C.POINTER(CrCont), C.POINTER(CrContReport)]),
@@ -356,6 +357,15 @@ class Solver:
         self.gamma = rep.gamma_last
         return dict(stages_run=rep.stages_run, iters_total=rep.iters_total, gamma_last=rep.gamma_last,
                     L_last=rep.L_last, last=rep.last.as_dict())
+
+    def predict(self, Z):
+        """f_hat(z) = max_i y_i + xi_i^T (z - x_i) at eta(Theta^k), for the rows of Z (M x n)."""
+        Z = _f64(Z)
+        if Z.ndim != 2 or Z.shape[1] != self.n:
+            raise ValueError(f"Z must be M x {self.n}")
+        out = np.empty(Z.shape[0])
+        self._check(self.lib.cr_predict(self.h, Z.ctypes.data, Z.shape[0], out.ctypes.data), "cr_predict")
+        return out
 
     def set_pass_timing(self, on: bool):
         self._check(self.lib.cr_set_pass_timing(self.h, 1 if on else 0), "cr_set_pass_timing")

@@ -20,7 +20,8 @@ struct LocalGroup {
         const void *send = nullptr;
         void *recv = nullptr;
         cudaEvent_t ready = nullptr, done = nullptr;
-        double *scratch = nullptr;   // allreduce result staging (kScratch doubles)
+        double *scratch = nullptr;   // allreduce result staging
+        size_t cap = 0;              // doubles
     };
     std::vector<Slot> slot;
     explicit LocalGroup(int w) : world(w), slot(w) {}
@@ -86,7 +87,6 @@ const char *local_enter(LocalGroup *g, int r, const void *send, void *recv, cuda
     if (!me.ready) {
         LG_CK(cudaEventCreateWithFlags(&me.ready, cudaEventDisableTiming));
         LG_CK(cudaEventCreateWithFlags(&me.done, cudaEventDisableTiming));
-        LG_CK(cudaMalloc(&me.scratch, kScratch * sizeof(double)));
     }
     me.send = send;
     me.recv = recv;
@@ -151,8 +151,13 @@ const char *comm_allreduce_f64(Comm &c, double *buf, size_t count, CollOp op, cu
         ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, op == COLL_MAX ? ncclMax : ncclSum, c.nccl, s);
         return r == ncclSuccess ? nullptr : nccl_err("ncclAllReduce", r);
     }
-    if (count > kScratch) return "local group: allreduce count too large";
     LocalGroup *g = c.local;
+    auto &me = g->slot[c.rank];
+    if (me.cap < count) {                                   // grow this rank's staging buffer
+        if (me.scratch) LG_CK(cudaFree(me.scratch));
+        me.cap = count > kScratch ? count : kScratch;
+        LG_CK(cudaMalloc(&me.scratch, me.cap * sizeof(double)));
+    }
     if (const char *e = local_enter(g, c.rank, buf, buf, s)) return e;
     SrcPtrs src{};
     for (int p = 0; p < g->world; ++p) src.p[p] = static_cast<const double *>(g->slot[p].send);

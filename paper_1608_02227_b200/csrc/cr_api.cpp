@@ -531,6 +531,16 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     return CR_OK;
 }
 
+// eta(Theta^k) (Step-1 formulas at Theta^k, Theorem 1) into y64 (all rows), Xi64, a64.
+cr_status compute_eta(cr_ctx *ctx) {
+    const Layout &Ly = ctx->lay;
+    SmallParams sp = small_params(ctx, ctx->bA, ctx->bA, 0, 1.0, false);
+    CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
+    ctx->launches += 1;
+    if (ctx->world > 1) CM(comm_allgather(ctx->comm, ctx->at<double>(Ly.y64), (size_t)Ly.S, 8, ctx->stream));
+    return CR_OK;
+}
+
 cr_status check_ctx(cr_ctx *ctx) {
     if (!ctx) return CR_ERR_INVALID_ARG;
     if (ctx->poisoned) return CR_ERR_STATE;
@@ -1069,6 +1079,50 @@ cr_status cr_continuation(cr_ctx *ctx, const cr_cont *p, cr_cont_report *out) {
         }
     }
     if (out) return eval_stats(ctx, &out->last);
+    return CR_OK;
+}
+
+cr_status cr_predict(cr_ctx *ctx, const double *Z, int64_t M, double *out) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    if (M < 0 || (M > 0 && (!Z || !out))) return fail(ctx, CR_ERR_INVALID_ARG, "cr_predict: bad arguments");
+    if (M == 0) return CR_OK;
+    const Layout &Ly = ctx->lay;
+    for (int64_t e = 0; e < M * Ly.n; ++e)
+        if (!std::isfinite(Z[e])) return fail(ctx, CR_ERR_INVALID_ARG, "cr_predict: non-finite query");
+    if ((st = compute_eta(ctx)) != CR_OK) return st;
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+    PredictParams p{};
+    p.M = M;
+    p.Ns = Ly.Ns;
+    p.row0 = Ly.row0;
+    p.n = Ly.n;
+    p.splits = predict_splits(M, std::max<int64_t>(Ly.Ns, 1), nsm);
+    p.y = ctx->at<double>(Ly.y64);
+    p.a = ctx->at<double>(Ly.a64);
+    p.Xi = ctx->at<double>(Ly.Xi64);
+    double *dZ = nullptr, *dpart = nullptr, *dout = nullptr;
+    const size_t zb = (size_t)M * Ly.n * 8, pb = (size_t)p.splits * M * 8, ob = (size_t)M * 8;
+    CK(cudaMallocAsync(&dZ, zb, ctx->stream));
+    CK(cudaMallocAsync(&dpart, pb, ctx->stream));
+    CK(cudaMallocAsync(&dout, ob, ctx->stream));
+    CK(cudaMemcpyAsync(dZ, Z, zb, cudaMemcpyHostToDevice, ctx->stream));
+    p.Z = dZ;
+    p.part = dpart;
+    p.out = dout;
+    if (Ly.Ns > 0) {
+        CK(launch_predict(p, ctx->stream));
+        ctx->launches += 2;
+    } else {
+        CK(cudaMemsetAsync(dout, 0xff, ob, ctx->stream));      // NaN pattern; replaced by the max below
+    }
+    if (ctx->world > 1) CM(comm_allreduce_f64(ctx->comm, dout, (size_t)M, COLL_MAX, ctx->stream));
+    CK(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaFreeAsync(dZ, ctx->stream));
+    CK(cudaFreeAsync(dpart, ctx->stream));
+    CK(cudaFreeAsync(dout, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return CR_OK;
 }
 

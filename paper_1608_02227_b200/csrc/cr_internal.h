@@ -170,6 +170,21 @@ size_t tc_barrier_bytes();
 cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,
                              float *g2h, float *g2l, cudaStream_t s);
 
+// Max-affine estimator f_hat(z) = max_i (y_i - a_i) + xi_i . z over this shard's rows
+// (kernels/predict.cu); fp64.
+struct PredictParams {
+    const double *Z;       // [M][n] queries (device)
+    int64_t M, Ns, row0;
+    int n, splits;
+    const double *y;       // [>= row0 + Ns] (global rows)
+    const double *a;       // [Ns] xi_i . x_i
+    const double *Xi;      // [Ns][n]
+    double *part;          // [splits][M]
+    double *out;           // [M]
+};
+int predict_splits(int64_t M, int64_t Ns, int nsm);
+cudaError_t launch_predict(const PredictParams &p, cudaStream_t s);
+
 // Column-major helpers for initialisation.
 cudaError_t launch_fill_inputs(const double *X64, int64_t N, int n, int NB, int NBP, int64_t ldT,
                                int prec_fp64, void *XT, void *Xh, cudaStream_t s);

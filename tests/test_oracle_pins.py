@@ -481,3 +481,22 @@ def test_continuation_stage_is_warm_started_papg():
     b1 = oracle.papg(X, ybar, a[0]["gamma"], a[0]["L"], 7, Tprev=T0, Tt=T0, t=1.0)
     b2 = oracle.papg(X, ybar, a[1]["gamma"], a[1]["L"], 5, Tprev=b1["Tprev"], Tt=b1["Tprev"], t=1.0)
     np.testing.assert_array_equal(a[1]["Theta"], b2["Tprev"])
+
+
+# ---------------------------------------------------------------- max-affine estimator
+def test_predict_from_exact_convex_supports():
+    """With y_i = f(x_i), xi_i = grad f(x_i) of a convex f (every pair constraint of Eq. (original)
+    P:64 holds by the gradient inequality), f_hat interpolates f at the data points and lies
+    below f everywhere (it is a max of supporting hyperplanes)."""
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((40, 3))
+    A = rng.standard_normal((3, 3))
+    Q = A @ A.T + 0.1 * np.eye(3)
+    f = lambda Z: 0.5 * np.einsum("ij,jk,ik->i", Z, Q, Z)
+    y, xi = f(X), X @ Q
+    np.testing.assert_allclose(ref.predict(X, y, xi, X), y, rtol=0, atol=1e-12)
+    Z = rng.standard_normal((200, 3)) * 2
+    assert np.all(ref.predict(X, y, xi, Z) <= f(Z) + 1e-12)
+    # a single data point: f_hat is that point's supporting hyperplane
+    z = rng.standard_normal((5, 3))
+    np.testing.assert_allclose(ref.predict(X[:1], y[:1], xi[:1], z), y[0] + (z - X[0]) @ xi[0], rtol=1e-14)

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest -m gpu -q -x tests/test_gpu_sharded_local.py > gpurun_out/pytest_new.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_new.log
+timeout 900 python -m pytest -m gpu -q -x tests/test_gpu_predict.py > gpurun_out/pytest_new.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_new.log
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
