@@ -528,6 +528,10 @@ pass_tc_kernel(const TcParams p) {
                 double *rp = p.rowpart + ((int64_t)(slot0 + rb - rbA) * TBM + r) * W;
                 rp[NP2 + wg] = rrun;
                 if (adapt) rp[NP2 + 2 + wg] = drun;
+                if (run_start(c) && run_end(c)) {   // 1-tile run: the other warpgroup has no tile in
+                    rp[NP2 + 1 - wg] = 0.0;         // it, so its columns are written here (every
+                    if (adapt) rp[NP2 + 3 - wg] = 0.0;   // slot column is rewritten by every pass)
+                }
                 rrun = 0.0;
                 drun = 0.0;
             }

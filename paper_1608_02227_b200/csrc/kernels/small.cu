@@ -73,8 +73,9 @@ __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
 }
 
 // Blocks [0, ncolb): column sums, 32 columns per block, 8 warps splitting the row-block range
-// (fixed chunks, combined in order).  Remaining blocks: one thread per (row, d <= n) summing
-// that row's run slots in a fixed order and resetting each consumed partial to 0.
+// (fixed chunks, combined in order).  Remaining blocks: one warp per row, lanes over d <= n (+1),
+// summing that row's run slots in a fixed order.  Every pass rewrites every column of the slots
+// it owns, so the partials are read-only here.
 template <typename Tc>
 __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int ncolb) {
     if ((int)blockIdx.x < ncolb) {
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
         if (i < p.Ns) {
             const int rb = i / p.rbm, ii = i - rb * p.rbm;
             const int e0 = p.rb_ptr[rb], ns = p.rb_ptr[rb + 1] - e0;
-            double *rp = const_cast<double *>(p.rowpart);
+            const double *rp = p.rowpart;
             // the row's partial loads are issued 4 at a time before the fixed-order sum
             // (slot ids are broadcast loads: every lane reads the same address)
             for (int base = 0; base < ns; base += 32) {
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
                     double s = base == 0 ? 0.0 : *out;
                     for (int q0 = 0; q0 < m; q0 += 4) {
                         double v[4], w[4];
-                        double *rows[4];
+                        const double *rows[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {           // 4 independent loads in flight
                             const bool ok = q0 + k < m;
@@ -138,8 +139,6 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int n
                             if (q0 + k < m) {
                                 s += v[k];
                                 if (two) s += w[k];
-                                rows[k][col] = 0.0;
-                                if (two) rows[k][col2] = 0.0;
                             }
                         }
                     }
