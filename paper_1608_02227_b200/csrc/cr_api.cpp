@@ -41,11 +41,13 @@ struct Layout {
     int64_t N = 0, S = 0, Ns = 0, row0 = 0, Rp = 0, ldT = 0;
     int n = 0, NB = 0, NBP = 0, nRB = 0, world = 1, fp64 = 0;
     int nbuf = 2;                  // Theta buffers / sums slots (3 with CR_FLAG_ADAPTIVE)
+    bool resident = false;         // small-N SMEM-resident solver eligible (row-major, n <= 32, world 1)
     size_t es = 4;
     // tensor-core pass
     bool tc = false;
     int NK = 0, NP2 = 0, nCBtc = 0, nRBtc = 0;
     // byte offsets
+    size_t yg = 0, cpart = 0;      // resident solver: y of all rows, per-CTA column partials
     size_t th[3] = {0, 0, 0}, XT, Xh, X64, ybar, r[3] = {0, 0, 0}, c[3] = {0, 0, 0}, P[3] = {0, 0, 0}, dsq = 0, y64, yv, bv, XiT, Xi64, a64, colpart, rowpart,
         slot0, rb_ptr, rb_slots, cfull, ts, statpro, statres, g1h, g1l, g2h, g2l, XiR, slot0_tc, rb_ptr_tc, rb_slots_tc,
         total;
@@ -113,6 +115,11 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
         rp_simt = std::max(rp_simt, (size_t)(L->nRBtc + kGMax) * kTcBM * (L->NP2 + 4) * 8);
     }
     L->rowpart = take(rp_simt);
+    L->resident = !L->tc && n <= 32 && world == 1 && N <= kResidentMaxN;
+    if (L->resident) {
+        L->yg = take((size_t)N * 8);
+        L->cpart = take((size_t)kResidentMaxCTAs * N * 8);
+    }
     L->slot0 = take((size_t)kGMax * 4);
     L->rb_ptr = take((size_t)(L->nRB + 1) * 4);
     L->rb_slots = take((size_t)(L->nRB + kGMax) * 4);
@@ -190,6 +197,9 @@ struct cr_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> ev;
     size_t ev_used = 0;
+    int64_t ev_iters = 0;    // iterations covered by the recorded event pairs
+    // small-N SMEM-resident solver (kernels/resident.cu): CTAs, rows per CTA (0: not usable)
+    int res_G = 0, res_R = 0, res_ldS = 0;
     // constant-step graphs per (bA, bB) assignment
     cudaGraphExec_t graph[9] = {};
     cudaStream_t cap_stream = nullptr;   // private stream used only to record graphs
@@ -404,7 +414,10 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
         PassParams p = pass_params(ctx, bA, bB, bo, adapt);
         CK(launch_pass_simt(p, Ly.fp64, Ly.NB, MODE_STEP, ctx->stream));
     }
-    if (e1) CK(cudaEventRecord(e1, ctx->stream));
+    if (e1) {
+        CK(cudaEventRecord(e1, ctx->stream));
+        ctx->ev_iters += 1;
+    }
     ReduceParams q = reduce_params(ctx, bo, advance_t ? 1 : 0, Ly.tc, adapt);
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
     if (ctx->world > 1)
@@ -579,6 +592,64 @@ cr_status build_graph(cr_ctx *ctx, int key) {
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
     return CR_OK;
+}
+
+// K constant-step iterations with the SMEM-resident solver (small N, world 1); the state is
+// left exactly as K graph replays of the streaming path would leave it.
+cr_status enqueue_resident(cr_ctx *ctx, int64_t K) {
+    const Layout &Ly = ctx->lay;
+    ResidentParams p{};
+    p.N = Ly.N;
+    p.ldT = Ly.ldT;
+    p.K = K;
+    p.n = Ly.n;
+    p.R = ctx->res_R;
+    p.ldS = ctx->res_ldS;
+    p.G = ctx->res_G;
+    p.TA = ctx->th[ctx->bA];
+    p.TB = ctx->th[ctx->bB];
+    p.rA = ctx->r[ctx->bA]; p.cA = ctx->c[ctx->bA]; p.PA = ctx->P[ctx->bA];
+    p.rB = ctx->r[ctx->bB]; p.cB = ctx->c[ctx->bB]; p.PB = ctx->P[ctx->bB];
+    p.X64 = ctx->at<double>(Ly.X64);
+    p.ybar = ctx->at<double>(Ly.ybar);
+    p.gamma = ctx->gamma;
+    p.L = ctx->L;
+    p.ts = ctx->at<DevScalars>(Ly.ts);
+    p.yg = ctx->at<double>(Ly.yg);
+    p.y64 = ctx->at<double>(Ly.y64);
+    p.a64 = ctx->at<double>(Ly.a64);
+    p.Xi64 = ctx->at<double>(Ly.Xi64);
+    p.cpart = ctx->at<double>(Ly.cpart);
+    p.trace = ctx->trace;                 // CR_TC_TRACE debug buffer (also sized for this)
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->timing) {
+        e0 = next_event(ctx);
+        e1 = next_event(ctx);
+        if (!e0 || !e1) return fail(ctx, CR_ERR_CUDA, "cudaEventCreate failed");
+        CK(cudaEventRecord(e0, ctx->stream));
+    }
+    CK(launch_resident(p, Ly.fp64, ctx->stream));
+    ctx->launches += 1;
+    if (ctx->trace) {   // debug: dump the phase timeline of CTA 0
+        std::vector<unsigned long long> h(16 * 8);
+        CK(cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (FILE *f = std::fopen(std::getenv("CR_TC_TRACE"), "wb")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
+    if (e1) {
+        CK(cudaEventRecord(e1, ctx->stream));
+        ctx->ev_iters += K;
+    }
+    for (int64_t i = 0; i < K; ++i) advance_host(ctx, ctx->bB);
+    return CR_OK;
+}
+
+bool use_resident(const cr_ctx *ctx) {
+    return ctx->res_G > 0 && ctx->rule == CR_STEP_CONSTANT && !ctx->comm.local && ctx->world == 1 &&
+           !std::getenv("CR_NO_RESIDENT");
 }
 
 }  // namespace
@@ -767,9 +838,31 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         IK(launch_tc_images(ctx->at<double>(Ly.X64), N, n, Ly.NK, Ly.NP2, Ly.nCBtc, ctx->at<float>(Ly.g1h),
                             ctx->at<float>(Ly.g1l), ctx->at<float>(Ly.g2h), ctx->at<float>(Ly.g2l), ctx->stream));
         ctx->launches += 1;
-        if (std::getenv("CR_TC_TRACE")) {
-            IK(cudaMalloc(&ctx->trace, 5 * 256 * 8 * 8));
-            IK(cudaMemsetAsync(ctx->trace, 0, 5 * 256 * 8 * 8, ctx->stream));
+    }
+    if (std::getenv("CR_TC_TRACE")) {     // debug timelines (tcgen05 pass / resident solver)
+        IK(cudaMalloc(&ctx->trace, 5 * 256 * 8 * 8));
+        IK(cudaMemsetAsync(ctx->trace, 0, 5 * 256 * 8 * 8, ctx->stream));
+    }
+    if (Ly.resident) {
+        // SMEM-resident solver geometry: enough CTAs that one iteration's N^2 n work is spread
+        // (~64K pair-features per CTA), at most one per SM (cooperative launch: co-resident),
+        // more if the rows do not fit in shared memory; unusable if even nsm CTAs do not fit
+        int coop = 0;
+        IK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
+        const int64_t work = N * N * (int64_t)n;
+        int G = (int)std::min<int64_t>({(int64_t)nsm, (int64_t)kResidentMaxCTAs, std::max<int64_t>(1, (work + 65535) / 65536)});
+        for (; coop && G <= std::min(nsm, kResidentMaxCTAs); ++G) {
+            ResidentParams rp{};
+            rp.N = N;
+            rp.n = n;
+            rp.R = (int)((N + G - 1) / G);
+            rp.ldS = (int)((N + 3) / 4 * 4);
+            if (resident_smem_bytes(rp, Ly.fp64) <= (size_t)(226 * 1024)) {
+                ctx->res_R = rp.R;
+                ctx->res_G = (int)((N + rp.R - 1) / rp.R);
+                ctx->res_ldS = rp.ldS;
+                break;
+            }
         }
     }
     IK(cudaStreamSynchronize(ctx->stream));   // host vectors go out of scope
@@ -937,7 +1030,13 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
     const double Nd = (double)ctx->lay.N;
     int64_t it = 0;
     while (it < max_iters) {
-        if (ctx->rule == CR_STEP_ADAPTIVE) {
+        if (use_resident(ctx)) {
+            // one cooperative launch for the whole chunk (to the next stop test, or the end)
+            int64_t chunk = max_iters - it;
+            if (stop) chunk = std::min<int64_t>(chunk, stop->report_every - it % stop->report_every);
+            if ((st = enqueue_resident(ctx, chunk)) != CR_OK) return st;
+            it += chunk - 1;
+        } else if (ctx->rule == CR_STEP_ADAPTIVE) {
             if ((st = adaptive_step(ctx)) != CR_OK) return st;
         } else {
             const int bo = ctx->bB;
@@ -1136,6 +1235,7 @@ cr_status cr_set_pass_timing(cr_ctx *ctx, int32_t on) {
     if (!ctx) return CR_ERR_INVALID_ARG;
     ctx->timing = on != 0;
     ctx->ev_used = 0;
+    ctx->ev_iters = 0;
     return CR_OK;
 }
 
@@ -1150,8 +1250,9 @@ cr_status cr_pass_timing(cr_ctx *ctx, double *total_ms, int64_t *launches) {
         tot += ms;
     }
     if (total_ms) *total_ms = tot;
-    if (launches) *launches = (int64_t)(ctx->ev_used / 2);
+    if (launches) *launches = ctx->ev_iters;
     ctx->ev_used = 0;
+    ctx->ev_iters = 0;
     return CR_OK;
 }
 

@@ -18,6 +18,8 @@ constexpr int kStatBlocks = 1024; // max CTAs of the stats/residual kernels
 constexpr int kTcBM = 128;        // tensor-core pass tile rows (TMEM lanes)
 constexpr int kTcBN = 32;         // tensor-core pass tile columns
 constexpr int kTcMaxStages = 6;
+constexpr int64_t kResidentMaxN = 4096;   // SMEM-resident small-N solver: eligible sizes
+constexpr int kResidentMaxCTAs = 256;
 
 // Element (i, j) of a Theta buffer (local row i, column j), in elements from the buffer base.
 //   row-major (SIMT configs): i * ldT + j
@@ -169,6 +171,24 @@ cudaError_t pass_tc_prepare(int NK, int smem_bytes);
 size_t tc_barrier_bytes();
 cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,
                              float *g2h, float *g2l, cudaStream_t s);
+
+// SMEM-resident multi-iteration solver for small N (kernels/resident.cu): K constant-step
+// iterations in one cooperative launch, row-major Theta buffers (SIMT layout), world == 1.
+struct ResidentParams {
+    int64_t N, ldT, K;
+    int n, R, ldS, G;           // rows per CTA, smem row pitch, CTAs
+    void *TA, *TB;              // Theta^{k-1}, Theta^{k-2} (global, row-major)
+    double *rA, *cA, *PA, *rB, *cB, *PB;
+    const double *X64, *ybar;
+    double gamma, L;
+    DevScalars *ts;
+    double *yg;                 // [N] y of the current Step 1 (all rows)
+    double *y64, *a64, *Xi64;   // eta of the last Step 1 (cr_get_eta)
+    double *cpart;              // [G][N]
+    unsigned long long *trace;  // debug: clock64 per phase of CTA 0, first 16 iterations (nullptr = off)
+};
+size_t resident_smem_bytes(const ResidentParams &p, int fp64);
+cudaError_t launch_resident(const ResidentParams &p, int fp64, cudaStream_t s);
 
 // Max-affine estimator f_hat(z) = max_i (y_i - a_i) + xi_i . z over this shard's rows
 // (kernels/predict.cu); fp64.

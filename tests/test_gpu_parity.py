@@ -156,7 +156,10 @@ def test_K_iterations_C3_reduced(crp):
     k_iteration_case(crp, "C3", "fp32", K=300, N=1500)
 
 
-def test_graph_solve_equals_stepwise_and_is_deterministic(crp):
+def test_graph_solve_equals_stepwise_and_is_deterministic(crp, monkeypatch):
+    # the streaming path's graph replay (the SMEM-resident solver, which cr_solve would pick at
+    # this size, is covered by tests/test_gpu_resident.py)
+    monkeypatch.setenv("CR_NO_RESIDENT", "1")
     X, ybar = crdata.random_problem(700, 6, seed=9, fp32=True)
     a = crp.Solver(X, ybar, 1e-3)
     a.solve(37)
