@@ -350,6 +350,7 @@ TcParams tc_params(cr_ctx *ctx, int b1, int b2, int bo, bool adapt = false) {
     p.g1stages = ctx->g1stages;
     p.g2stages = ctx->g2stages;
     p.adapt = adapt ? 1 : 0;
+    p.poll_ns = std::getenv("CR_TC_POLL_NS") ? std::atoi(std::getenv("CR_TC_POLL_NS")) : 64;
     p.smem_bytes = ctx->smem_tc;
     p.g1_hi = ctx->at<float>(Ly.g1h);
     p.g1_lo = ctx->at<float>(Ly.g1l);

@@ -191,7 +191,9 @@ pass_tc_kernel(const TcParams p) {
             const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
             Cursor c = start(), c1 = start(), c2 = start();
             while (c.u < U || c1.u < U || c2.u < U) {
+                bool issued = false;
                 if (c.u < U && mbar_test(&bar->empty[c.s], (uint32_t)(c.ph ^ 1))) {
+                    issued = true;
                     TC_TRACE(0, c.u, 1);
                     uint8_t *st = stage_ptr(c.s);
                     uint64_t *fb = &bar->full[c.s];
@@ -205,6 +207,7 @@ pass_tc_kernel(const TcParams p) {
                     adv(c, 1);
                 }
                 if (c1.u < U && mbar_test(&bar->g1empty[c1.x], (uint32_t)(c1.xph ^ 1))) {
+                    issued = true;
                     TC_TRACE(0, c1.u, 2);
                     uint8_t *xs = g1ring + (size_t)c1.x * 2 * g1_bytes;
                     uint64_t *fb = &bar->g1full[c1.x];
@@ -214,6 +217,7 @@ pass_tc_kernel(const TcParams p) {
                     adv(c1, 1);
                 }
                 if (c2.u < U && mbar_test(&bar->g2empty[c2.z], (uint32_t)(c2.zph ^ 1))) {
+                    issued = true;
                     TC_TRACE(0, c2.u, 3);
                     uint8_t *xs = g2ring + (size_t)c2.z * 2 * g2_bytes;
                     uint64_t *fb = &bar->g2full[c2.z];
@@ -222,6 +226,9 @@ pass_tc_kernel(const TcParams p) {
                     bulk_load(xs + g2_bytes, p.g2_lo + (size_t)c2.cb * NP2 * 32, g2_bytes, fb, pol_keep);
                     adv(c2, 1);
                 }
+                // nothing to issue: back off instead of spinning on the issue slots the
+                // epilogue warps of this scheduler need
+                if (!issued) __nanosleep(p.poll_ns);
             }
         }
     } else if (warp == 1 || warp == 3) {
