@@ -224,25 +224,56 @@ def test_lipschitz_computed_by_library(crp):
 
 
 @pytest.mark.slow
-def test_full_size_C4_sampled_step(crp):
-    """C4 at full size (N=16384, n=40) in the bench's launch configuration: 3 GPU steps from
-    theta^0 = 0, then step 4 checked on sampled rows of Theta^4 and on all of eta^4."""
+def _theta1_rows(ybar, L, rows):
+    """P1 (exact step from theta^0 = 0): Theta^1_ij = (ybar_i - ybar_j)_+ / L, zero diagonal."""
+    T = np.maximum(ybar[rows][:, None] - ybar[None, :], 0.0) / L
+    T[np.arange(len(rows)), rows] = 0.0
+    return T
+
+
+def test_full_size_C4_two_steps(crp):
+    """C4 at full size (N=16384, n=40) in the bench's launch configuration.  Step 1 against the
+    closed form P1 on sampled rows; step 2 against the oracle started from that closed form:
+    eta^2 = eta(Theta^1) on all rows and Theta^2 on sampled rows (no oracle input comes from
+    the GPU)."""
     cfg = crdata.CONFIGS["C4"]
     X, ybar = crdata.make_problem(cfg)
     L = ref.lipschitz(X, cfg.gamma)
-    s = crp.Solver(X, ybar, cfg.gamma, L=L)
-    s.solve(3)
-    T3, T2, t3, t4 = s.get_theta()
-    s.step()
-    y, xi = s.get_eta()
-    Tt = oracle.extrapolate(T3, T2, t3, t4)
-    del T2
-    yo, xio = oracle.eta(X, ybar, cfg.gamma, Tt)
-    assert rel(y, yo) <= 1e-5 and rel(xi, xio) <= 1e-5
+    N = cfg.N
     rows = np.array([0, 1, 777, 8191, 8192, 12345, 16383])
-    want = oracle.project_rows(X, yo, xio, L, rows, Tt[rows])
+    s = crp.Solver(X, ybar, cfg.gamma, L=L)
+    assert s.kernel == "tc"
+    s.step()
+    got1 = np.concatenate([s.get_theta_rows(0, int(r), 1) for r in rows])
+    assert rel(got1, _theta1_rows(ybar, L, rows)) <= 1e-6
+    s.step()                                                    # theta~^2 = Theta^1 (beta_1 = 0)
+    y, xi = s.get_eta()
+    T1 = _theta1_rows(ybar, L, np.arange(N))
+    yo, xio = oracle.eta(X, ybar, cfg.gamma, T1)
+    assert rel(y, yo) <= 1e-5 and rel(xi, xio) <= 1e-5
+    want = oracle.project_rows(X, yo, xio, L, rows, T1[rows])
+    del T1
+    got2 = np.concatenate([s.get_theta_rows(0, int(r), 1) for r in rows])
+    assert rel(got2, want) <= 1e-5
+    s.close()
+
+
+def test_full_size_C5_first_step(crp):
+    """C5 at full size (N=65536, n=80, 2 x 16 GiB of state on one GPU) in the bench's launch
+    configuration: Theta^1 on sampled rows against the closed form P1."""
+    cfg = crdata.CONFIGS["C5"]
+    X, ybar = crdata.make_problem(cfg)
+    L = ref.lipschitz(X, cfg.gamma)
+    rows = np.array([0, 127, 128, 30000, 32767, 32768, 65535])
+    s = crp.Solver(X, ybar, cfg.gamma, L=L)
+    assert s.kernel == "tc"
+    s.step()
     got = np.concatenate([s.get_theta_rows(0, int(r), 1) for r in rows])
-    assert rel(got, want) <= 1e-5
+    assert rel(got, _theta1_rows(ybar, L, rows)) <= 1e-6
+    y, xi = s.get_eta()                                         # eta^1 = eta(0) = (ybar, 0)
+    np.testing.assert_array_equal(y, ybar)
+    assert np.all(xi == 0)
+    s.close()
 
 
 @pytest.mark.parametrize("kernel", ["simt", "tc"])
