@@ -84,8 +84,9 @@ def test_set_gamma_restarts_fig2(crp):
     assert s.L == L1
     s.step()
     T, T1, tk, tk1 = s.get_theta()
-    want = oracle.papg(X, ybar, g1, L1, 1, Tprev=T30, Tt=T30, t=1.0)
-    assert rel(T, want["Tprev"]) <= 1e-12
+    o30 = oracle.papg(X, ybar, g0, L0, 30)["Tprev"]                 # the oracle's own theta^30
+    want = oracle.papg(X, ybar, g1, L1, 1, Tprev=o30, Tt=o30, t=1.0)
+    assert rel(T, want["Tprev"]) <= 1e-11
     np.testing.assert_array_equal(T1, T30)
     assert tk1 == oracle.momentum_next(1.0)
     with pytest.raises(crp.CrError):
