@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--step", default="constant", choices=["constant", "adaptive"],
+                    help="step rule of Step 2: constant 1/L (Fig. 2, the headline) or adaptive (P:400-407)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
@@ -191,7 +193,10 @@ def main():
     X, ybar = crdata.make_problem(cfg)
     prec = cfg.prec
 
-    s = crp.Solver(X, ybar, cfg.gamma, prec=prec, kernel=args.kernel, group=group)
+    adaptive = args.step == "adaptive"
+    s = crp.Solver(X, ybar, cfg.gamma, prec=prec, kernel=args.kernel, group=group, adaptive=adaptive)
+    if adaptive:
+        s.set_step_rule("adaptive", 2.0)
     stream = s.stream
     s.solve(W)                                            # warm-up
     torch.cuda.synchronize()
@@ -201,8 +206,12 @@ def main():
     if rank == 0:
         clk.start()
     mark = clk.mark()
-    s.set_pass_timing(True)
+    # constant rule: per-pass CUDA events inside the timed region (eager launches); adaptive
+    # rule: the timed region replays the per-iteration graphs (device-side trial loop, which
+    # per-pass events would break), the pass time comes from a separate event-timed run below
+    s.set_pass_timing(not adaptive)
     l0 = s.launch_count
+    tr0 = s.step_info()["trials_total"]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if group is not None:
@@ -217,7 +226,13 @@ def main():
     t_ms = e0.elapsed_time(e1)
     pass_ms, pass_n = s.pass_timing()
     launches = s.launch_count - l0
+    trials = s.step_info()["trials_total"] - tr0
     s.set_pass_timing(False)
+    if adaptive:
+        s.set_pass_timing(True)
+        s.solve(min(K, 20))
+        pass_ms, pass_n = s.pass_timing()
+        s.set_pass_timing(False)
     if group is not None:
         t = torch.tensor([t_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -232,7 +247,9 @@ def main():
         if group is not None:
             dist.barrier()
         t0 = time.perf_counter()
-        s2 = crp.Solver(Xp, yp, cfg.gamma, prec=prec, kernel=args.kernel, group=group)
+        s2 = crp.Solver(Xp, yp, cfg.gamma, prec=prec, kernel=args.kernel, group=group, adaptive=adaptive)
+        if adaptive:
+            s2.set_step_rule("adaptive", 2.0)
         s2.solve(K)
         y, xi, _ = s2.primal()
         torch.cuda.synchronize()
@@ -272,7 +289,7 @@ def main():
         "config": {"workload": f"{cfg.name}: N={cfg.N}, n={cfg.n}, {cfg.x_law} x, f0={cfg.f0}, "
                                f"gamma={cfg.gamma}, Theta0=0, step 1/L (Lanczos)",
                    "N": cfg.N, "n": cfg.n, "gamma": cfg.gamma, "iters_timed": K,
-                   "kernel": s.kernel, "parallelism": f"rows{world}",
+                   "kernel": s.kernel, "parallelism": f"rows{world}", "step_rule": args.step,
                    "l2": f"inputs larger than L2: Theta state {2 * bpp // 3 * cfg.N * cfg.N / 2**30:.2f} GiB "
                          f"streamed per iteration vs 126 MB L2" if cfg.N >= 8192 else "L2-resident config"},
         "hbm_gbs_algorithmic": achieved,
@@ -281,6 +298,11 @@ def main():
                      "kernel": f"fused pair pass ({s.kernel})", "bytes_per_launch": per_launch_bytes,
                      "avg_launch_ms": avg_pass_s * 1e3, "pass_share_of_step": pass_ms / max(t_ms, 1e-9)},
         "gpu_launches": launches,
+        **({"adaptive": {"trials_per_iter": trials / K, "passes_timed": pass_n,
+                         "note": "value counts accepted iterations; every trial is one fused pass; the "
+                                 "timed region replays one CUDA graph per iteration (WHILE node over "
+                                 "trials); roofline from a separate 20-iteration event-timed run"}}
+           if adaptive else {}),
         "clocks": clocks,
         "e2e": e2e,
     }

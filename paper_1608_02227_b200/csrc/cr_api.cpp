@@ -184,9 +184,8 @@ struct cr_ctx {
     // step rule: constant 1/L, or adaptive 1/s_k
     cr_step_rule rule = CR_STEP_CONSTANT;
     double ups = 2.0;    // growth factor upsilon > 1
-    double s_cur = 0.0;  // s_{k-1} (adaptive)
-    int max_trials = 64;
-    int64_t trials_last = 0, trials_total = 0;
+    int max_trials = 64;  // (s_{k-1}, trial counters: device-resident, DevScalars::ad)
+    cudaGraphExec_t graph_ad[9] = {};   // adaptive iteration (WHILE loop over trials) per (bA, bB)
     int64_t k = 0;
     int G = 0, nCB = 0;
     int64_t T = 0;
@@ -393,10 +392,12 @@ cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
 // Theta^{k-2} (bB) with step 1/s (scale), then the fused pass writing Theta^k into buffer bo
 // (bB in place for the constant step; the spare buffer for an adaptive trial) and its sums
 // into slot bo.  advance_t: Step 3 on the device (constant step); adapt: also ||D||^2 per row.
-cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, bool advance_t, bool adapt) {
+cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, bool advance_t, bool adapt,
+                       const double *s_dev = nullptr) {
     const Layout &Ly = ctx->lay;
     const int bA = ctx->bA, bB = ctx->bB;
     SmallParams sp = small_params(ctx, bA, bB, 1, scale, false);
+    sp.s_dev = s_dev;
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
     if (ctx->world > 1) {
         CM(comm_allgather(ctx->comm, ctx->ws + Ly.yv, (size_t)Ly.S, (int)Ly.es, ctx->stream));
@@ -435,60 +436,97 @@ void advance_host(cr_ctx *ctx, int bo) {
     ctx->k += 1;
 }
 
-// One adaptive P-APG iteration: trial s = s_{k-1} ups^(l-1), l = 0, 1, ...;
-// Theta^k(s) into the spare buffer; accept when Q <= s ||D||^2 (Eq. (adaptive-check) in
-// quadratic form, R15).  Synchronizes once per trial.
+// One adaptive trial, all on the device: Step 1 with 1/s of the trial (ts->ad),
+// the fused pass writing the trial Theta^k into the spare buffer (+ ||D||^2), the reduce, the
+// check (Eq. (adaptive-check) in quadratic form, R15) and the accept/retry kernel
+// (which drives the WHILE node `cond` when the trial runs inside a CUDA graph).
+cr_status enqueue_adaptive_trial(cr_ctx *ctx, unsigned long long cond, int has_cond, bool allow_timing) {
+    const Layout &Ly = ctx->lay;
+    const int bo = 3 - ctx->bA - ctx->bB;
+    DevScalars *ts = ctx->at<DevScalars>(Ly.ts);
+    cr_status st = enqueue_step(ctx, allow_timing, bo, 0.0, false, true, &ts->ad[AD_STRY]);
+    if (st != CR_OK) return st;
+    AdaptParams ap{};
+    ap.Ns = Ly.Ns;
+    ap.row0 = Ly.row0;
+    ap.n = Ly.n;
+    ap.gamma = ctx->gamma;
+    ap.X64 = ctx->at<double>(Ly.X64);
+    ap.rA = ctx->r[ctx->bA]; ap.cA = ctx->c[ctx->bA]; ap.PA = ctx->P[ctx->bA];
+    ap.rB = ctx->r[ctx->bB]; ap.cB = ctx->c[ctx->bB]; ap.PB = ctx->P[ctx->bB];
+    ap.rO = ctx->r[bo]; ap.cO = ctx->c[bo]; ap.PO = ctx->P[bo];
+    ap.dsq = ctx->at<double>(Ly.dsq);
+    ap.statpart = ctx->at<double>(Ly.statres);
+    ap.ts = ts;
+    CK(launch_adapt_check(ap, ctx->stream));
+    if (ctx->world > 1) CM(comm_allreduce_f64(ctx->comm, ts->stats + 8, 2, COLL_SUM, ctx->stream));
+    CK(launch_adapt_decide(ts, cond, has_cond, ctx->stream));
+    ctx->launches += 3;
+    return CR_OK;
+}
+
+// One adaptive iteration driven from the host (local groups, per-pass timing): one trial per
+// round trip; the accept/retry state lives on the device exactly as in the graph path.
 cr_status adaptive_step(cr_ctx *ctx) {
     const Layout &Ly = ctx->lay;
     const int bo = 3 - ctx->bA - ctx->bB;
     DevScalars *ts = ctx->at<DevScalars>(Ly.ts);
-    double h[2] = {0, 0};
-    CK(cudaMemcpyAsync(h, ts, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    const double t_prev = h[0], t_cur = h[1];
-    const double s_prev = ctx->s_cur;
-    int l = 0;
-    double s_try = 0.0;
-    for (;; ++l) {
-        if (l >= ctx->max_trials)
-            return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check)", ctx->max_trials);
-        s_try = s_prev * std::pow(ctx->ups, (double)l - 1.0);
-        cr_status st = enqueue_step(ctx, true, bo, 1.0 / s_try, false, true);
+    for (;;) {
+        cr_status st = enqueue_adaptive_trial(ctx, 0, 0, true);
         if (st != CR_OK) return st;
-        AdaptParams ap{};
-        ap.Ns = Ly.Ns;
-        ap.row0 = Ly.row0;
-        ap.n = Ly.n;
-        ap.gamma = ctx->gamma;
-        ap.X64 = ctx->at<double>(Ly.X64);
-        ap.rA = ctx->r[ctx->bA]; ap.cA = ctx->c[ctx->bA]; ap.PA = ctx->P[ctx->bA];
-        ap.rB = ctx->r[ctx->bB]; ap.cB = ctx->c[ctx->bB]; ap.PB = ctx->P[ctx->bB];
-        ap.rO = ctx->r[bo]; ap.cO = ctx->c[bo]; ap.PO = ctx->P[bo];
-        ap.dsq = ctx->at<double>(Ly.dsq);
-        ap.statpart = ctx->at<double>(Ly.statres);
-        ap.ts = ts;
-        CK(launch_adapt_check(ap, ctx->stream));
-        ctx->launches += 2;
-        if (ctx->world > 1) CM(comm_allreduce_f64(ctx->comm, ts->stats + 8, 2, COLL_SUM, ctx->stream));
-        double qd[2];
-        CK(cudaMemcpyAsync(qd, ts->stats + 8, sizeof qd, cudaMemcpyDeviceToHost, ctx->stream));
+        double ad[8];
+        CK(cudaMemcpyAsync(ad, ts->ad, sizeof ad, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
-        // g(Theta^k) - [g(theta~) + <grad g(theta~), D> - s/2 ||D||^2] = (s ||D||^2 - Q) / 2 >= 0.
-        // A trial whose Theta^k overflowed the storage precision (a step far too long) cannot
-        // pass: it is rejected like any failing trial.
-        if (std::isfinite(qd[0]) && std::isfinite(qd[1]) && qd[0] <= s_try * qd[1]) break;
+        if (ad[AD_ERR] != 0.0)
+            return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check)", ctx->max_trials);
+        if (ad[AD_L] == 0.0) break;                       // accepted
     }
-    // Step 3 and the role change of Step 4
-    h[0] = t_cur;
-    h[1] = (1.0 + std::sqrt(1.0 + 4.0 * t_cur * t_cur)) / 2.0;
-    (void)t_prev;
-    CK(cudaMemcpyAsync(ts, h, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->s_cur = s_try;
-    ctx->trials_last = l + 1;
-    ctx->trials_total += l + 1;
     advance_host(ctx, bo);
     return CR_OK;
+}
+
+// CUDA graph of one adaptive iteration: a WHILE node whose body is one trial; the decide kernel
+// leaves the loop on acceptance.  One graph per (bA, bB) assignment (the spare buffer differs).
+cr_status build_adaptive_graph(cr_ctx *ctx, int key) {
+    const int bA = ctx->bA, bB = ctx->bB;
+    const int64_t k = ctx->k, launches = ctx->launches;
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return fail(ctx, CR_ERR_CUDA, "adaptive graph: %s", cudaGetErrorString(e));
+    }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->cap_stream;
+    e = cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    cr_status st = e == cudaSuccess ? enqueue_adaptive_trial(ctx, h, 1, false) : CR_ERR_CUDA;
+    cudaGraph_t out = nullptr;
+    const cudaError_t e2 = e == cudaSuccess ? cudaStreamEndCapture(ctx->stream, &out) : e;
+    ctx->stream = user;
+    ctx->bA = bA; ctx->bB = bB; ctx->k = k; ctx->launches = launches;
+    if (st != CR_OK || e2 != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return st != CR_OK ? st : fail(ctx, CR_ERR_CUDA, "adaptive graph capture: %s", cudaGetErrorString(e2));
+    }
+    e = cudaGraphInstantiate(&ctx->graph_ad[key], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "adaptive graph instantiate: %s", cudaGetErrorString(e));
+    return CR_OK;
+}
+
+bool use_adaptive_graph(const cr_ctx *ctx) {
+    return !ctx->comm.local && !ctx->timing && ctx->world == 1 && !std::getenv("CR_NO_ADAPTIVE_GRAPH");
 }
 
 // eta(Theta^k) and diagnostics (Theorem 1 semantics); synchronizes.
@@ -565,6 +603,8 @@ cr_status check_ctx(cr_ctx *ctx) {
 
 void drop_graphs(cr_ctx *ctx) {
     for (auto &g : ctx->graph)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (auto &g : ctx->graph_ad)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
 }
 
@@ -1028,6 +1068,14 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
     if (out) std::memset(out, 0, sizeof *out);
     // no graphs with the in-process local group: its collectives are host rendezvous
     const bool use_graph = !ctx->timing && !ctx->comm.local;
+    int64_t ttot0 = 0;                      // adaptive trials so far (launch accounting of the graph path)
+    if (ctx->rule == CR_STEP_ADAPTIVE && use_adaptive_graph(ctx)) {
+        double v = 0.0;
+        CK(cudaMemcpyAsync(&v, &ctx->at<DevScalars>(ctx->lay.ts)->ad[AD_TTOT], sizeof v, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ttot0 = (int64_t)v;
+    }
     const double Nd = (double)ctx->lay.N;
     int64_t it = 0;
     while (it < max_iters) {
@@ -1037,6 +1085,11 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
             if (stop) chunk = std::min<int64_t>(chunk, stop->report_every - it % stop->report_every);
             if ((st = enqueue_resident(ctx, chunk)) != CR_OK) return st;
             it += chunk - 1;
+        } else if (ctx->rule == CR_STEP_ADAPTIVE && use_adaptive_graph(ctx)) {
+            const int key = 3 * ctx->bA + ctx->bB;
+            if (!ctx->graph_ad[key] && (st = build_adaptive_graph(ctx, key)) != CR_OK) return st;
+            CK(cudaGraphLaunch(ctx->graph_ad[key], ctx->stream));
+            advance_host(ctx, 3 - ctx->bA - ctx->bB);
         } else if (ctx->rule == CR_STEP_ADAPTIVE) {
             if ((st = adaptive_step(ctx)) != CR_OK) return st;
         } else {
@@ -1063,6 +1116,15 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
         }
     }
     if (out) out->iters = it;
+    if (ctx->rule == CR_STEP_ADAPTIVE && use_adaptive_graph(ctx)) {     // trials ran on the device
+        double ad[8];
+        CK(cudaMemcpyAsync(ad, ctx->at<DevScalars>(ctx->lay.ts)->ad, sizeof ad, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->launches += 6 * ((int64_t)ad[AD_TTOT] - ttot0);     // prologue, pass, reduce, check x2, decide
+        const double err = ad[AD_ERR];
+        if (err != 0.0)
+            return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check)", ctx->max_trials);
+    }
     return CR_OK;
 }
 
@@ -1118,17 +1180,27 @@ cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, doubl
             return fail(ctx, CR_ERR_INVALID_ARG, "upsilon must be finite and > 1");
         if (s_prev < 0.0 || !std::isfinite(s_prev)) return fail(ctx, CR_ERR_INVALID_ARG, "s_prev must be >= 0");
         ctx->ups = upsilon;
-        ctx->s_cur = s_prev > 0.0 ? s_prev : ctx->L;     // s_0 = L_gamma
+        const double s0 = s_prev > 0.0 ? s_prev : ctx->L;     // s_0 = L_gamma
+        const double ad[8] = {s0, s0 / upsilon, upsilon, 0.0, 0.0, 0.0, (double)ctx->max_trials, 0.0};
+        CK(cudaMemcpyAsync(ctx->at<DevScalars>(ctx->lay.ts)->ad, ad, sizeof ad, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     ctx->rule = rule;
     return CR_OK;
 }
 
 cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *trials_total) {
-    if (!ctx) return CR_ERR_INVALID_ARG;
-    if (s_k) *s_k = ctx->rule == CR_STEP_ADAPTIVE ? ctx->s_cur : ctx->L;
-    if (trials_last) *trials_last = ctx->rule == CR_STEP_ADAPTIVE ? ctx->trials_last : 1;
-    if (trials_total) *trials_total = ctx->trials_total;
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    double ad[8];
+    CK(cudaMemcpyAsync(ad, ctx->at<DevScalars>(ctx->lay.ts)->ad, sizeof ad, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const bool a = ctx->rule == CR_STEP_ADAPTIVE;
+    if (s_k) *s_k = a ? ad[AD_S] : ctx->L;
+    if (trials_last) *trials_last = a ? (int64_t)ad[AD_TLAST] : 1;
+    if (trials_total) *trials_total = (int64_t)ad[AD_TTOT];
+    if (a && ad[AD_ERR] != 0.0)
+        return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check)", ctx->max_trials);
     return CR_OK;
 }
 
@@ -1142,7 +1214,13 @@ cr_status cr_set_gamma(cr_ctx *ctx, double gamma, double L) {
     drop_graphs(ctx);                       // gamma and 1/L are baked into the captured launches
     ctx->gamma = gamma;
     ctx->L = L > 0.0 ? L : ctx->sigma2 / gamma;
-    if (ctx->rule == CR_STEP_ADAPTIVE) ctx->s_cur = ctx->L;     // s_0 = L_gamma
+    if (ctx->rule == CR_STEP_ADAPTIVE) {                        // s_0 = L_gamma, l = 0
+        const double v[2] = {ctx->L, ctx->L / ctx->ups};
+        const double l0 = 0.0;
+        DevScalars *ts = ctx->at<DevScalars>(ctx->lay.ts);
+        CK(cudaMemcpyAsync(&ts->ad[AD_S], v, sizeof v, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(&ts->ad[AD_L], &l0, sizeof l0, cudaMemcpyHostToDevice, ctx->stream));
+    }
     // restart Fig. 2 at the current iterate: theta~^1 = theta^0 := Theta^k, t_1 = 1;
     // (t_prev, t_cur) = (1, 1) makes beta_0 = 0, so Theta^{k-1}'s buffer is not read
     DevScalars h{};

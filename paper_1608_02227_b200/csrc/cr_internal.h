@@ -41,8 +41,13 @@ int simt_bucket(int n);           // smallest compiled NB >= n, or 0 if none
 struct DevScalars {
     double t_prev;      // t_{k-1}
     double t_cur;       // t_k
-    double stats[16];   // finalized diagnostics (see stats kernels)
+    double stats[16];   // finalized diagnostics (see stats kernels); [8], [9]: adaptive Q, ||D||^2
+    // adaptive step rule state (device-resident so a CUDA-graph WHILE loop can run the trials):
+    // [0] s_{k-1}  [1] s of the next trial  [2] ups  [3] trials of the last iteration
+    // [4] trials in total  [5] l of the next trial  [6] max trials  [7] error (no l passed)
+    double ad[8];
 };
+enum AdaptSlots { AD_S = 0, AD_STRY = 1, AD_UPS = 2, AD_TLAST = 3, AD_TTOT = 4, AD_L = 5, AD_MAX = 6, AD_ERR = 7 };
 
 struct PassParams {
     const void *B1;        // Theta^{k-1} (read)
@@ -89,6 +94,7 @@ struct SmallParams {
     double *statpart;      // [kStatBlocks][8] per-CTA partials
     DevScalars *ts;
     int use_beta;          // 1: beta from ts (Step 1 at theta~^k); 0: beta = 0 (eta(Theta^k))
+    const double *s_dev;   // non-null: scale = 1 / *s_dev (the adaptive trial's s, device-resident)
     float *XiR;            // optional [Rp][NK] row-major xi * scale (tensor-core pass operand)
     int NK;
 };
@@ -127,6 +133,9 @@ struct AdaptParams {
     DevScalars *ts;        // beta from (t_prev, t_cur); results to stats[8], stats[9]
 };
 cudaError_t launch_adapt_check(const AdaptParams &p, cudaStream_t s);
+// Accept / retry after the check (ts->ad, Step 3 on acceptance).  cond != 0: also drive the
+// enclosing CUDA-graph WHILE node (0 = leave the trial loop).
+cudaError_t launch_adapt_decide(DevScalars *ts, unsigned long long cond, int has_cond, cudaStream_t s);
 
 struct ResidualParams {
     const void *Theta;     // storage precision, layout theta_off(tiled, nCBt)

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
     __shared__ double red[4][8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double beta = p.use_beta ? (p.ts->t_prev - 1.0) / p.ts->t_cur : 0.0;
+    const double scale = p.s_dev ? 1.0 / *p.s_dev : p.scale;
     double u2 = 0.0, uy = 0.0, xi2 = 0.0, bad = 0.0;
     T *XiT = static_cast<T *>(p.XiT);
     for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < p.Ns; i += (int64_t)gridDim.x * 8) {
@@ -42,8 +43,8 @@ __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
             const double Pt = P1 + beta * (P1 - P2);
             const double xi = (rt * x[d] - Pt) / p.gamma;   // (A2^T theta~)_i / gamma
             p.Xi64[i * p.n + d] = xi;
-            if (XiT) XiT[(int64_t)d * p.Rp + i] = T(xi * p.scale);
-            if (p.XiR) p.XiR[i * p.NK + d] = (float)(xi * p.scale);
+            if (XiT) XiT[(int64_t)d * p.Rp + i] = T(xi * scale);
+            if (p.XiR) p.XiR[i * p.NK + d] = (float)(xi * scale);
             a += xi * x[d];
             q2 += xi * xi;
         }
@@ -55,8 +56,8 @@ __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
         if (lane == 0) {
             p.y64[gi] = y;
             p.a64[i] = a;
-            static_cast<T *>(p.yv)[gi] = T(y * p.scale);
-            static_cast<T *>(p.bv)[i] = T((a - y) * p.scale);
+            static_cast<T *>(p.yv)[gi] = T(y * scale);
+            static_cast<T *>(p.bv)[i] = T((a - y) * scale);
             u2 += u * u;
             uy += u * p.ybar[gi];
             xi2 += q2;
@@ -189,6 +190,34 @@ __global__ void __launch_bounds__(256) adapt_check_kernel(const AdaptParams p) {
         for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
         p.statpart[blockIdx.x * 8 + threadIdx.x] = t;
     }
+}
+
+// Accept / retry: the trial at s = ad[STRY] passes iff Q <= s ||D||^2 (the quadratic
+// form of Eq. (adaptive-check), R15; a non-finite trial fails).  Accept: s_k = s,
+// Step 3, next iteration starts at l = 0 with s_{k} / ups.  Reject: l += 1, s *= ups.
+__global__ void adapt_decide_kernel(DevScalars *ts, cudaGraphConditionalHandle cond, int has_cond) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double *ad = ts->ad;
+    const double Q = ts->stats[8], D = ts->stats[9], s = ad[AD_STRY];
+    const bool ok = isfinite(Q) && isfinite(D) && Q <= s * D;
+    bool more;
+    if (ok) {
+        const double t = ts->t_cur;
+        ts->t_prev = t;
+        ts->t_cur = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+        ad[AD_S] = s;
+        ad[AD_TLAST] = ad[AD_L] + 1.0;
+        ad[AD_TTOT] += ad[AD_L] + 1.0;
+        ad[AD_L] = 0.0;
+        ad[AD_STRY] = s / ad[AD_UPS];
+        more = false;
+    } else {
+        ad[AD_L] += 1.0;
+        ad[AD_STRY] = s * ad[AD_UPS];
+        more = ad[AD_L] < ad[AD_MAX];
+        if (!more) ad[AD_ERR] = 1.0;
+    }
+    if (has_cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
 }
 
 __global__ void adapt_finalize_kernel(const double *part, int nb, DevScalars *ts) {
@@ -332,6 +361,11 @@ cudaError_t launch_adapt_check(const AdaptParams &p, cudaStream_t s) {
     if (nb > kStatBlocks) nb = kStatBlocks;
     adapt_check_kernel<<<(unsigned)nb, 256, 0, s>>>(p);
     adapt_finalize_kernel<<<1, 32, 0, s>>>(p.statpart, (int)nb, p.ts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adapt_decide(DevScalars *ts, unsigned long long cond, int has_cond, cudaStream_t s) {
+    adapt_decide_kernel<<<1, 32, 0, s>>>(ts, (cudaGraphConditionalHandle)cond, has_cond);
     return cudaGetLastError();
 }
 

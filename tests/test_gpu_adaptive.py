@@ -134,3 +134,28 @@ def test_adaptive_needs_third_buffer(crp):
         s2.set_step_rule("adaptive", 1.0)          # upsilon must be > 1
     s.close()
     s2.close()
+
+
+@pytest.mark.parametrize("N,n,prec,kernel", [(97, 3, "fp64", "auto"), (1000, 20, "fp32", "tc")])
+def test_adaptive_graph_solve_equals_stepwise(crp, N, n, prec, kernel, monkeypatch):
+    """cr_solve runs each adaptive iteration as one CUDA graph (a WHILE node over trials, the
+    accept/retry decision on the device); it must reproduce the host-driven trial loop of
+    cr_dual_step bit for bit, decisions and counters included."""
+    X, ybar = crdata.random_problem(N, n, seed=31, fp32=prec == "fp32")
+    gamma = 1e-3
+    L = ref.lipschitz(X, gamma)
+    a = crp.Solver(X, ybar, gamma, L=L, prec=prec, kernel=kernel, adaptive=True)
+    b = crp.Solver(X, ybar, gamma, L=L, prec=prec, kernel=kernel, adaptive=True)
+    for s in (a, b):
+        s.set_step_rule("adaptive", 2.0)
+    a.solve(15)
+    for _ in range(15):
+        b.step()
+    np.testing.assert_array_equal(a.get_theta()[0], b.get_theta()[0])
+    np.testing.assert_array_equal(a.get_theta()[1], b.get_theta()[1])
+    ia, ib = a.step_info(), b.step_info()
+    assert ia == ib
+    want = oracle.papg_adaptive(X, ybar, gamma, L, 15)
+    assert ia["trials_total"] == int(np.sum(want["trials"])) and ia["s"] == want["s_hist"][-1]
+    a.close()
+    b.close()
