@@ -788,15 +788,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     if (cudaSetDevice(ctx->device) != cudaSuccess) return bail(CR_ERR_CUDA);
 
     // step constant (Eq. (lischitz))
-    if (cfg->L > 0.0) {
-        ctx->L = cfg->L;
-    } else {
-        double L = 0.0;
-        cr_status s = cr_lipschitz_host(N, n, cfg->X, cfg->gamma, &L);
-        if (s != CR_OK) return bail(s);
-        ctx->L = L;
-    }
-    ctx->sigma2 = ctx->L * cfg->gamma;
+    if (cfg->L > 0.0) ctx->L = cfg->L;      // else: device Lanczos once X is on the device (below)
 
     for (int b = 0; b < Ly.nbuf; ++b) ctx->th[b] = ctx->ws + Ly.th[b];
     for (int s = 0; s < Ly.nbuf; ++s) {
@@ -817,6 +809,19 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     IK(cudaMemsetAsync(ctx->ws, 0, Ly.total, ctx->stream));
     IK(cudaMemcpyAsync(ctx->ws + Ly.X64, cfg->X, (size_t)N * n * 8, cudaMemcpyHostToDevice, ctx->stream));
     IK(cudaMemcpyAsync(ctx->ws + Ly.ybar, cfg->ybar, (size_t)N * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (!(cfg->L > 0.0)) {
+        // L = sigma_max(C)^2 / gamma by the device Lanczos (the host cr_lipschitz_host computes
+        // the same iteration; fixed-order reductions, so every rank gets the same L)
+        cudaError_t le = cudaSuccess;
+        const double s2 = sigma_max_sq_lanczos_device(N, n, ctx->at<double>(Ly.X64), 1e-13, 2000, ctx->stream, &le);
+        if (le != cudaSuccess) {
+            fail(ctx, CR_ERR_CUDA, "cr_init Lanczos: %s", cudaGetErrorString(le));
+            return bail(CR_ERR_CUDA);
+        }
+        if (!(s2 > 0.0) || !std::isfinite(s2)) return bail(CR_ERR_INVALID_ARG);
+        ctx->L = s2 / cfg->gamma;
+    }
+    ctx->sigma2 = ctx->L * cfg->gamma;
     IK(launch_fill_inputs(ctx->at<double>(Ly.X64), N, n, Ly.NB, Ly.NBP, Ly.ldT, Ly.fp64, ctx->ws + Ly.XT,
                           ctx->ws + Ly.Xh, ctx->stream));
     ctx->launches += 1;

@@ -200,6 +200,13 @@ struct ResidentParams {
 size_t resident_smem_bytes(const ResidentParams &p, int fp64);
 cudaError_t launch_resident(const ResidentParams &p, int fp64, cudaStream_t s);
 
+// sigma_max(C)^2 (Eq. (lischitz)): host Lanczos helpers (lanczos.cpp) and the device
+// Lanczos (kernels/lanczos.cu, X device fp64 [N][n]; < 0 and *err set on a CUDA error).
+double lanczos_max_ritz(const double *al, const double *be, int m);
+void lanczos_start(int64_t N, int n, double *v);
+double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol, int max_iter, cudaStream_t st,
+                                   cudaError_t *err);
+
 // Max-affine estimator f_hat(z) = max_i (y_i - a_i) + xi_i . z over this shard's rows
 // (kernels/predict.cu); fp64.
 struct PredictParams {

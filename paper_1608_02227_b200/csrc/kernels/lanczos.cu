@@ -1,0 +1,221 @@
+// L_gamma = sigma_max(C)^2 / gamma (Eq. (lischitz)) on the device: the same plain
+// Lanczos as csrc/lanczos.cpp (three-term recurrence, no re-orthogonalisation, identical
+// splitmix64 start vector), with the structured O(N n^2) product of C^T C (see lanczos.cpp for
+// the derivation) and every reduction in a fixed order (deterministic: all ranks agree).
+// The host keeps the tridiagonal (alpha, beta) and the Ritz bisection.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <vector>
+#include "../cr_internal.h"
+
+namespace cr {
+namespace {
+
+constexpr int LB = 256;
+
+// fixed-order block reduction of one value per thread (blockDim = LB)
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = LB / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// S2[d][e] = sum_l X[l][d] X[l][e] (one block per (d, e)); s[d] = sum_l X[l][d] (e == n slot)
+__global__ void __launch_bounds__(LB) lz_gram_kernel(const double *X, int64_t N, int n, double *S2, double *s) {
+    __shared__ double sh[LB];
+    const int d = blockIdx.x / (n + 1), e = blockIdx.x % (n + 1);
+    double acc = 0.0;
+    for (int64_t l = threadIdx.x; l < N; l += LB) acc += X[l * n + d] * (e < n ? X[l * n + e] : 1.0);
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+        if (e < n) S2[(size_t)d * n + e] = acc;
+        else s[d] = acc;
+    }
+}
+
+// per-block partials of Y = sum y, Sa = sum a, Sxi[d] = sum xi_d, w[d] = sum y x_d; a_k = xi_k.x_k
+// part layout per block: [Y, Sa, Sxi[0..n), w[0..n)]
+__global__ void __launch_bounds__(LB) lz_sums_kernel(const double *X, int64_t N, int n, const double *v, double *a,
+                                                     double *part) {
+    __shared__ double sh[LB];
+    const double *y = v, *xi = v + N;
+    const int64_t k0 = (int64_t)blockIdx.x * LB, k = k0 + threadIdx.x;
+    double yk = 0.0, ak = 0.0;
+    if (k < N) {
+        yk = y[k];
+        for (int d = 0; d < n; ++d) ak += xi[k * n + d] * X[k * n + d];
+        a[k] = ak;
+    }
+    double *out = part + (size_t)blockIdx.x * (2 + 2 * n);
+    double r = block_sum(yk, sh);
+    if (threadIdx.x == 0) out[0] = r;
+    r = block_sum(ak, sh);
+    if (threadIdx.x == 0) out[1] = r;
+    for (int d = 0; d < n; ++d) {
+        r = block_sum(k < N ? xi[k * n + d] : 0.0, sh);
+        if (threadIdx.x == 0) out[2 + d] = r;
+        r = block_sum(k < N ? yk * X[k * n + d] : 0.0, sh);
+        if (threadIdx.x == 0) out[2 + n + d] = r;
+    }
+}
+
+// fixed-order sum of the block partials -> tot [2 + 2n]
+__global__ void lz_sums_final_kernel(const double *part, int nb, int n, double *tot) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= 2 + 2 * n) return;
+    double r = 0.0;
+    for (int b = 0; b < nb; ++b) r += part[(size_t)b * (2 + 2 * n) + q];
+    tot[q] = r;
+}
+
+// out = C^T C v (lanczos.cpp CtC::apply), thread per row k
+__global__ void __launch_bounds__(LB) lz_apply_kernel(const double *X, int64_t N, int n, const double *S2,
+                                                      const double *s, const double *v, const double *a,
+                                                      const double *tot, double *out) {
+    const int64_t k = (int64_t)blockIdx.x * LB + threadIdx.x;
+    if (k >= N) return;
+    const double *y = v, *xi = v + N;
+    const double Y = tot[0], Sa = tot[1];
+    const double *Sxi = tot + 2, *w = tot + 2 + n;
+    const double *xk = X + k * n, *xik = xi + k * n;
+    double xs = 0.0, sx = 0.0;
+    for (int d = 0; d < n; ++d) { xs += xik[d] * s[d]; sx += Sxi[d] * xk[d]; }
+    const double Nd = (double)N;
+    const double rho = Y - Nd * y[k] + Nd * a[k] - xs;
+    out[k] = 2.0 * Nd * y[k] - 2.0 * Y + Sa - sx - Nd * a[k] + xs;
+    double *ok = out + N + k * n;
+    for (int d = 0; d < n; ++d) {
+        double t = 0.0;
+        const double *row = S2 + (size_t)d * n;
+        for (int e = 0; e < n; ++e) t += row[e] * xik[e];
+        ok[d] = xk[d] * rho - w[d] + (y[k] - a[k]) * s[d] + t;
+    }
+}
+
+// per-block partial of dot(a, b)
+__global__ void __launch_bounds__(LB) lz_dot_kernel(const double *a, const double *b, int64_t m, double *part) {
+    __shared__ double sh[LB];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * LB + threadIdx.x; i < m; i += (int64_t)gridDim.x * LB) acc += a[i] * b[i];
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// w -= alpha v + beta vprev, per-block partial of |w|^2
+__global__ void __launch_bounds__(LB) lz_update_kernel(double *w, const double *v, const double *vprev, int64_t m,
+                                                       const double *ab, double *part) {
+    __shared__ double sh[LB];
+    const double al = ab[0], bp = ab[1];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * LB + threadIdx.x; i < m; i += (int64_t)gridDim.x * LB) {
+        const double t = w[i] - (al * v[i] + bp * vprev[i]);
+        w[i] = t;
+        acc += t * t;
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void lz_final_kernel(const double *part, int nb, double *dst) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double r = 0.0;
+    for (int b = 0; b < nb; ++b) r += part[b];
+    *dst = r;
+}
+
+// vprev <- v, v <- w / b
+__global__ void lz_shift_kernel(double *v, double *vprev, const double *w, int64_t m, double inv_b) {
+    for (int64_t i = (int64_t)blockIdx.x * LB + threadIdx.x; i < m; i += (int64_t)gridDim.x * LB) {
+        vprev[i] = v[i];
+        v[i] = w[i] * inv_b;
+    }
+}
+
+}  // namespace
+
+// sigma_max(C)^2 by device Lanczos.  X: device [N][n] fp64.  Scratch is stream-ordered
+// (cudaMallocAsync).  start: host start vector of length N (n + 1), unit norm.  Returns < 0 on
+// a CUDA error (then *err holds it).
+double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol, int max_iter, cudaStream_t st,
+                                   cudaError_t *err) {
+    std::vector<double> start((size_t)N * (n + 1));
+    lanczos_start(N, n, start.data());
+    const int64_t m = N * (int64_t)(n + 1);
+    const int nbk = (int)((N + LB - 1) / LB);
+    const int nbv = (int)std::min<int64_t>((m + LB - 1) / LB, 1024);
+    double *S2 = nullptr, *s = nullptr, *v = nullptr, *vp = nullptr, *w = nullptr, *a = nullptr, *part = nullptr,
+           *tot = nullptr, *sc = nullptr;
+    auto ok = [&](cudaError_t e) { if (e != cudaSuccess && *err == cudaSuccess) *err = e; return e == cudaSuccess; };
+    *err = cudaSuccess;
+    const size_t npart = std::max<size_t>((size_t)nbk * (2 + 2 * n), (size_t)nbv);
+    ok(cudaMallocAsync(&S2, sizeof(double) * ((size_t)n * n + n), st));
+    ok(cudaMallocAsync(&v, sizeof(double) * 3 * m, st));
+    ok(cudaMallocAsync(&a, sizeof(double) * N, st));
+    ok(cudaMallocAsync(&part, sizeof(double) * npart, st));
+    ok(cudaMallocAsync(&tot, sizeof(double) * (2 + 2 * n + 4), st));
+    double result = -1.0;
+    if (*err == cudaSuccess) {
+        s = S2 + (size_t)n * n;
+        vp = v + m;
+        w = vp + m;
+        sc = tot + 2 + 2 * n;                    // [alpha, beta_prev, |w|^2, spare]
+        ok(cudaMemcpyAsync(v, start.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
+        ok(cudaMemsetAsync(vp, 0, sizeof(double) * m, st));
+        lz_gram_kernel<<<n * (n + 1), LB, 0, st>>>(X, N, n, S2, s);
+        ok(cudaGetLastError());
+        std::vector<double> al, be;
+        double prev = 0.0, bprev = 0.0;
+        int stable = 0;
+        for (int it = 0; it < std::min<int64_t>(max_iter, m) && *err == cudaSuccess; ++it) {
+            lz_sums_kernel<<<nbk, LB, 0, st>>>(X, N, n, v, a, part);
+            lz_sums_final_kernel<<<1, 256, 0, st>>>(part, nbk, n, tot);
+            lz_apply_kernel<<<nbk, LB, 0, st>>>(X, N, n, S2, s, v, a, tot, w);
+            lz_dot_kernel<<<nbv, LB, 0, st>>>(w, v, m, part);
+            lz_final_kernel<<<1, 32, 0, st>>>(part, nbv, sc);
+            double hv[2];
+            ok(cudaMemcpyAsync(hv, sc, sizeof(double), cudaMemcpyDeviceToHost, st));
+            ok(cudaStreamSynchronize(st));
+            const double al_ = hv[0];
+            hv[0] = al_;
+            hv[1] = bprev;
+            ok(cudaMemcpyAsync(sc, hv, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+            lz_update_kernel<<<nbv, LB, 0, st>>>(w, v, vp, m, sc, part);
+            lz_final_kernel<<<1, 32, 0, st>>>(part, nbv, sc + 2);
+            double b2 = 0.0;
+            ok(cudaMemcpyAsync(&b2, sc + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+            ok(cudaStreamSynchronize(st));
+            const double b = std::sqrt(b2);
+            al.push_back(al_);
+            const double theta = lanczos_max_ritz(al.data(), be.data(), (int)al.size());
+            result = theta;
+            if (it > 2 && std::fabs(theta - prev) <= tol * std::fabs(theta)) {
+                if (++stable >= 3) break;
+            } else {
+                stable = 0;
+            }
+            prev = theta;
+            if (b <= 1e-14 * std::fabs(theta)) break;
+            be.push_back(b);
+            lz_shift_kernel<<<nbv, LB, 0, st>>>(v, vp, w, m, 1.0 / b);
+            ok(cudaGetLastError());
+            bprev = b;
+        }
+    }
+    cudaFreeAsync(S2, st);
+    cudaFreeAsync(v, st);
+    cudaFreeAsync(a, st);
+    cudaFreeAsync(part, st);
+    cudaFreeAsync(tot, st);
+    ok(cudaStreamSynchronize(st));
+    return *err == cudaSuccess ? result : -1.0;
+}
+
+}  // namespace cr

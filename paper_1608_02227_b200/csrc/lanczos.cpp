@@ -106,11 +106,14 @@ uint64_t splitmix(uint64_t &x) {
 
 }  // namespace
 
-// Returns lambda_max(C^T C) (= sigma_max(C)^2); negative on failure.
-double sigma_max_sq_lanczos(int64_t N, int n, const double *X, double tol, int max_iter) {
+// Largest Ritz value of the tridiagonal (al[0..m), be[0..m-1)) (shared with the device Lanczos).
+double lanczos_max_ritz(const double *al, const double *be, int m) {
+    return max_ritz(std::vector<double>(al, al + m), std::vector<double>(be, be + std::max(0, m - 1)));
+}
+
+// The deterministic unit start vector (splitmix64 hash; every rank gets the same one).
+void lanczos_start(int64_t N, int n, double *v) {
     const int64_t dim = N * (int64_t)(n + 1);
-    CtC op(N, n, X);
-    std::vector<double> v(dim), vprev(dim, 0.0), w(dim);
     uint64_t seed = 0x1608022270000001ull;
     double nrm = 0.0;
     for (int64_t i = 0; i < dim; ++i) {
@@ -118,7 +121,15 @@ double sigma_max_sq_lanczos(int64_t N, int n, const double *X, double tol, int m
         nrm += v[i] * v[i];
     }
     nrm = std::sqrt(nrm);
-    for (auto &e : v) e /= nrm;
+    for (int64_t i = 0; i < dim; ++i) v[i] /= nrm;
+}
+
+// Returns lambda_max(C^T C) (= sigma_max(C)^2); negative on failure.
+double sigma_max_sq_lanczos(int64_t N, int n, const double *X, double tol, int max_iter) {
+    const int64_t dim = N * (int64_t)(n + 1);
+    CtC op(N, n, X);
+    std::vector<double> v(dim), vprev(dim, 0.0), w(dim);
+    lanczos_start(N, n, v.data());
     std::vector<double> al, be;
     double prev = 0.0, bprev = 0.0;
     int stable = 0;
