@@ -1186,7 +1186,7 @@ cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, doubl
         if (s_prev < 0.0 || !std::isfinite(s_prev)) return fail(ctx, CR_ERR_INVALID_ARG, "s_prev must be >= 0");
         ctx->ups = upsilon;
         const double s0 = s_prev > 0.0 ? s_prev : ctx->L;     // s_0 = L_gamma
-        const double ad[8] = {s0, s0 / upsilon, upsilon, 0.0, 0.0, 0.0, (double)ctx->max_trials, 0.0};
+        const double ad[8] = {s0, s0 * std::pow(upsilon, -1.0), upsilon, 0.0, 0.0, 0.0, (double)ctx->max_trials, 0.0};
         CK(cudaMemcpyAsync(ctx->at<DevScalars>(ctx->lay.ts)->ad, ad, sizeof ad, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     }
@@ -1220,7 +1220,7 @@ cr_status cr_set_gamma(cr_ctx *ctx, double gamma, double L) {
     ctx->gamma = gamma;
     ctx->L = L > 0.0 ? L : ctx->sigma2 / gamma;
     if (ctx->rule == CR_STEP_ADAPTIVE) {                        // s_0 = L_gamma, l = 0
-        const double v[2] = {ctx->L, ctx->L / ctx->ups};
+        const double v[2] = {ctx->L, ctx->L * std::pow(ctx->ups, -1.0)};
         const double l0 = 0.0;
         DevScalars *ts = ctx->at<DevScalars>(ctx->lay.ts);
         CK(cudaMemcpyAsync(&ts->ad[AD_S], v, sizeof v, cudaMemcpyHostToDevice, ctx->stream));

@@ -209,11 +209,11 @@ __global__ void adapt_decide_kernel(DevScalars *ts, cudaGraphConditionalHandle c
         ad[AD_TLAST] = ad[AD_L] + 1.0;
         ad[AD_TTOT] += ad[AD_L] + 1.0;
         ad[AD_L] = 0.0;
-        ad[AD_STRY] = s / ad[AD_UPS];
+        ad[AD_STRY] = s * pow(ad[AD_UPS], -1.0);           // s_{k-1} ups^(l-1) at l = 0
         more = false;
     } else {
         ad[AD_L] += 1.0;
-        ad[AD_STRY] = s * ad[AD_UPS];
+        ad[AD_STRY] = ad[AD_S] * pow(ad[AD_UPS], ad[AD_L] - 1.0);   // formed afresh, as the oracle does
         more = ad[AD_L] < ad[AD_MAX];
         if (!more) ad[AD_ERR] = 1.0;
     }
@@ -228,20 +228,22 @@ __global__ void adapt_finalize_kernel(const double *part, int nb, DevScalars *ts
     ts->stats[9] = d;
 }
 
-// Residual pass: 128 columns x 32 rows per tile, thread = (column, 16-row half).
+// Residual pass: 64 rows x 128 columns per tile, thread = 8 rows x 4 columns (register-blocked
+// fp64 outer products over d: 12 shared loads -- 8 of them warp broadcasts -- per 32 FMAs).
 template <typename T>
 __global__ void __launch_bounds__(256) residual_kernel(const ResidualParams p) {
-    constexpr int RBM = 32, RBN = 128;
+    constexpr int RBM = 64, RBN = 128;
     extern __shared__ double rsm[];
-    double *xs = rsm;                        // [n][RBN]
-    double *xis = xs + p.n * RBN;            // [RBM][n]
-    double *ab = xis + RBM * p.n;            // [RBM] a_i - y_i
+    double *xs = rsm;                        // [n][RBN]   x_j[d]
+    double *xis = xs + p.n * RBN;            // [n][RBM]   xi_i[d]
+    double *ab = xis + RBM * p.n;            // [RBM]      a_i - y_i
+    double *yj = ab + RBM;                   // [RBN]      y_j
     __shared__ double red[3][256];
     const int nrb = (int)((p.Ns + RBM - 1) / RBM), ncb = (int)((p.N + RBN - 1) / RBN);
     const int64_t ntiles = (int64_t)nrb * ncb;
     const T *Th = static_cast<const T *>(p.Theta);
     double gap = 0.0, v2 = 0.0, vmax = 0.0;
-    const int c = threadIdx.x % RBN, h = threadIdx.x / RBN;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t rb = t / ncb, cb = t % ncb;
         __syncthreads();
@@ -251,26 +253,53 @@ __global__ void __launch_bounds__(256) residual_kernel(const ResidualParams p) {
             xs[e] = j < p.N ? p.X64[j * p.n + d] : 0.0;
         }
         for (int e = threadIdx.x; e < RBM * p.n; e += blockDim.x) {
-            const int64_t i = rb * RBM + e / p.n;
-            xis[e] = i < p.Ns ? p.Xi64[i * p.n + e % p.n] : 0.0;
+            const int ii = e / p.n, d = e % p.n;
+            const int64_t i = rb * RBM + ii;
+            xis[d * RBM + ii] = i < p.Ns ? p.Xi64[i * p.n + d] : 0.0;
         }
         for (int e = threadIdx.x; e < RBM; e += blockDim.x) {
             const int64_t i = rb * RBM + e;
             ab[e] = i < p.Ns ? p.a64[i] - p.y64[p.row0 + i] : 0.0;
         }
+        for (int e = threadIdx.x; e < RBN; e += blockDim.x) {
+            const int64_t j = cb * RBN + e;
+            yj[e] = j < p.N ? p.y64[j] : 0.0;
+        }
         __syncthreads();
-        const int64_t j = cb * RBN + c;
-        if (j >= p.N) continue;
-        const double yj = p.y64[j];
-        for (int q = 0; q < RBM / 2; ++q) {
-            const int ii = h * (RBM / 2) + q;
+        double acc[8][4];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+        for (int d = 0; d < p.n; ++d) {
+            const double2 x01 = *reinterpret_cast<const double2 *>(xs + d * RBN + tx * 4);
+            const double2 x23 = *reinterpret_cast<const double2 *>(xs + d * RBN + tx * 4 + 2);
+            const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
+            double xi[8];
+#pragma unroll
+            for (int r = 0; r < 8; r += 2) {
+                const double2 q = *reinterpret_cast<const double2 *>(xis + d * RBM + ty * 8 + r);
+                xi[r] = q.x;
+                xi[r + 1] = q.y;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] = fma(xi[r], xv[c], acc[r][c]);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int ii = ty * 8 + r;
             const int64_t i = rb * RBM + ii;
-            if (i >= p.Ns || p.row0 + i == j) continue;
-            double s = 0.0;
-            for (int d = 0; d < p.n; ++d) s = fma(xis[ii * p.n + d], xs[d * RBN + c], s);
-            const double R = yj + ab[ii] - s;              // y_j - y_i + a_i - xi_i . x_j
-            gap += (double)Th[theta_off(i, j, p.ldT, p.tiled, p.nCBt)] * R;
-            if (R < 0.0) { v2 += R * R; vmax = fmax(vmax, -R); }
+            if (i >= p.Ns) continue;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int64_t j = cb * RBN + tx * 4 + c;
+                if (j >= p.N || p.row0 + i == j) continue;
+                const double R = yj[tx * 4 + c] + ab[ii] - acc[r][c];   // y_j - y_i + a_i - xi_i . x_j
+                gap += (double)Th[theta_off(i, j, p.ldT, p.tiled, p.nCBt)] * R;
+                if (R < 0.0) { v2 += R * R; vmax = fmax(vmax, -R); }
+            }
         }
     }
     red[0][threadIdx.x] = gap; red[1][threadIdx.x] = v2; red[2][threadIdx.x] = vmax;
@@ -370,10 +399,10 @@ cudaError_t launch_adapt_decide(DevScalars *ts, unsigned long long cond, int has
 }
 
 cudaError_t launch_residual(const ResidualParams &p, int fp64, cudaStream_t s, int *nb_out) {
-    const int64_t nrb = (p.Ns + 31) / 32, ncb = (p.N + 127) / 128;
+    const int64_t nrb = (p.Ns + 63) / 64, ncb = (p.N + 127) / 128;
     int64_t tiles = nrb * ncb;
     int nb = (int)(tiles < kStatBlocks ? (tiles > 0 ? tiles : 1) : kStatBlocks);
-    const size_t smem = sizeof(double) * ((size_t)p.n * 128 + 32 * (size_t)p.n + 32);
+    const size_t smem = sizeof(double) * ((size_t)p.n * 128 + 64 * (size_t)p.n + 64 + 128);
     cudaError_t e;
     if (fp64) {
         e = cudaFuncSetAttribute(residual_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
