@@ -207,6 +207,7 @@ struct cr_ctx {
     int64_t T_tc = 0;
     unsigned long long *trace = nullptr;   // debug timeline buffer (CR_TC_TRACE=<file>)
     Comm comm;           // NCCL communicator or in-process local group (world > 1)
+    bool coll = false;   // collectives active: world > 1, or a 1-rank NCCL comm (CR_FORCE_NCCL test mode)
 
     template <typename P> P *at(size_t off) { return reinterpret_cast<P *>(ws + off); }
 };
@@ -292,7 +293,7 @@ ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance, bool tc = false, 
     q.rb_slots = ctx->at<int>(tc ? Ly.rb_slots_tc : Ly.rb_slots);
     q.r = ctx->r[slot];
     q.P = ctx->P[slot];
-    q.c_out = ctx->world > 1 ? ctx->at<double>(Ly.cfull) : ctx->c[slot];
+    q.c_out = ctx->coll ? ctx->at<double>(Ly.cfull) : ctx->c[slot];
     q.ts = ctx->at<DevScalars>(Ly.ts);
     q.advance_t = advance;
     return q;
@@ -383,7 +384,7 @@ cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
     ReduceParams q = reduce_params(ctx, s, 0);
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
     ctx->launches += 2;
-    if (ctx->world > 1)
+    if (ctx->coll)
         CM(comm_reduce_scatter_f64(ctx->comm, ctx->at<double>(Ly.cfull), ctx->c[s], (size_t)Ly.S, ctx->stream));
     return CR_OK;
 }
@@ -399,7 +400,7 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     SmallParams sp = small_params(ctx, bA, bB, 1, scale, false);
     sp.s_dev = s_dev;
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
-    if (ctx->world > 1) {
+    if (ctx->coll) {
         CM(comm_allgather(ctx->comm, ctx->ws + Ly.yv, (size_t)Ly.S, (int)Ly.es, ctx->stream));
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -422,7 +423,7 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     }
     ReduceParams q = reduce_params(ctx, bo, advance_t ? 1 : 0, Ly.tc, adapt);
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
-    if (ctx->world > 1)
+    if (ctx->coll)
         CM(comm_reduce_scatter_f64(ctx->comm, ctx->at<double>(Ly.cfull), ctx->c[bo], (size_t)Ly.S, ctx->stream));
     ctx->launches += 3;
     return CR_OK;
@@ -459,7 +460,7 @@ cr_status enqueue_adaptive_trial(cr_ctx *ctx, unsigned long long cond, int has_c
     ap.statpart = ctx->at<double>(Ly.statres);
     ap.ts = ts;
     CK(launch_adapt_check(ap, ctx->stream));
-    if (ctx->world > 1) CM(comm_allreduce_f64(ctx->comm, ts->stats + 8, 2, COLL_SUM, ctx->stream));
+    if (ctx->coll) CM(comm_allreduce_f64(ctx->comm, ts->stats + 8, 2, COLL_SUM, ctx->stream));
     CK(launch_adapt_decide(ts, cond, has_cond, ctx->stream));
     ctx->launches += 3;
     return CR_OK;
@@ -526,7 +527,7 @@ cr_status build_adaptive_graph(cr_ctx *ctx, int key) {
 }
 
 bool use_adaptive_graph(const cr_ctx *ctx) {
-    return !ctx->comm.local && !ctx->timing && ctx->world == 1 && !std::getenv("CR_NO_ADAPTIVE_GRAPH");
+    return !ctx->coll && !ctx->timing && ctx->world == 1 && !std::getenv("CR_NO_ADAPTIVE_GRAPH");
 }
 
 // eta(Theta^k) and diagnostics (Theorem 1 semantics); synchronizes.
@@ -537,7 +538,7 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     SmallParams sp = small_params(ctx, s, s, 0, 1.0, true);
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, &nb_pro));
     double *y64 = ctx->at<double>(Ly.y64);
-    if (ctx->world > 1) CM(comm_allgather(ctx->comm, y64, (size_t)Ly.S, 8, ctx->stream));
+    if (ctx->coll) CM(comm_allgather(ctx->comm, y64, (size_t)Ly.S, 8, ctx->stream));
     ResidualParams rp{};
     rp.Theta = ctx->th[b];
     rp.ldT = Ly.ldT;
@@ -558,7 +559,7 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     CK(launch_stats_finalize(ctx->at<double>(Ly.statpro), nb_pro, ctx->at<double>(Ly.statres), nb_res, ts,
                              ctx->stream));
     ctx->launches += 3;
-    if (ctx->world > 1) {
+    if (ctx->coll) {
         // stats[0..5] and [7] are sums; [6] is a max
         CM(comm_allreduce_f64(ctx->comm, ts->stats, 6, COLL_SUM, ctx->stream));
         CM(comm_allreduce_f64(ctx->comm, ts->stats + 6, 1, COLL_MAX, ctx->stream));
@@ -589,7 +590,7 @@ cr_status compute_eta(cr_ctx *ctx) {
     SmallParams sp = small_params(ctx, ctx->bA, ctx->bA, 0, 1.0, false);
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
     ctx->launches += 1;
-    if (ctx->world > 1) CM(comm_allgather(ctx->comm, ctx->at<double>(Ly.y64), (size_t)Ly.S, 8, ctx->stream));
+    if (ctx->coll) CM(comm_allgather(ctx->comm, ctx->at<double>(Ly.y64), (size_t)Ly.S, 8, ctx->stream));
     return CR_OK;
 }
 
@@ -689,7 +690,7 @@ cr_status enqueue_resident(cr_ctx *ctx, int64_t K) {
 }
 
 bool use_resident(const cr_ctx *ctx) {
-    return ctx->res_G > 0 && ctx->rule == CR_STEP_CONSTANT && !ctx->comm.local && ctx->world == 1 &&
+    return ctx->res_G > 0 && ctx->rule == CR_STEP_CONSTANT && !ctx->coll && ctx->world == 1 &&
            !std::getenv("CR_NO_RESIDENT");
 }
 
@@ -915,11 +916,19 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
 #undef IK
     ctx->comm.rank = ctx->rank;
     ctx->comm.world = ctx->world;
+    // CR_FORCE_NCCL (tests): a single rank still runs every collective through a 1-rank NCCL
+    // communicator -- exercises the NCCL calls, their in-place conventions and graph capture
+    const bool force = ctx->world == 1 && std::getenv("CR_FORCE_NCCL") && !cfg->local_group;
+    ctx->coll = ctx->world > 1 || force;
     if (ctx->world > 1 && cfg->local_group) {
         ctx->comm.local = reinterpret_cast<LocalGroup *>(cfg->local_group);
-    } else if (ctx->world > 1) {
+    } else if (ctx->coll) {
         ncclUniqueId id;
-        std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+        if (force) {
+            if (ncclGetUniqueId(&id) != ncclSuccess) return bail(CR_ERR_NCCL);
+        } else {
+            std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+        }
         ncclResult_t r = ncclCommInitRank(&ctx->comm.nccl, ctx->world, id, ctx->rank);
         if (r != ncclSuccess) {
             fail(ctx, CR_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
@@ -1147,7 +1156,7 @@ cr_status cr_get_eta(cr_ctx *ctx, double *y, double *xi) {
     if (st != CR_OK) return st;
     const Layout &Ly = ctx->lay;
     double *y64 = ctx->at<double>(Ly.y64);
-    if (y && ctx->world > 1) {
+    if (y && ctx->coll) {
         // make sure all ranks' rows are present (eta of a plain step is only local until gathered)
         CM(comm_allgather(ctx->comm, y64, (size_t)Ly.S, 8, ctx->stream));
     }
@@ -1300,7 +1309,7 @@ cr_status cr_predict(cr_ctx *ctx, const double *Z, int64_t M, double *out) {
     } else {
         CK(cudaMemsetAsync(dout, 0xff, ob, ctx->stream));      // NaN pattern; replaced by the max below
     }
-    if (ctx->world > 1) CM(comm_allreduce_f64(ctx->comm, dout, (size_t)M, COLL_MAX, ctx->stream));
+    if (ctx->coll) CM(comm_allreduce_f64(ctx->comm, dout, (size_t)M, COLL_MAX, ctx->stream));
     CK(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaFreeAsync(dZ, ctx->stream));
     CK(cudaFreeAsync(dpart, ctx->stream));
