@@ -351,6 +351,14 @@ TcParams tc_params(cr_ctx *ctx, int b1, int b2, int bo, bool adapt = false) {
     p.g2stages = ctx->g2stages;
     p.adapt = adapt ? 1 : 0;
     p.poll_ns = std::getenv("CR_TC_POLL_NS") ? std::atoi(std::getenv("CR_TC_POLL_NS")) : 64;
+    // L2 policy of the Theta stream: evict-normal for loads and stores measured +1.6% at C4
+    // (0.878 -> 0.892), but -1.5% at C5 where the 84 MB of X images (evict-last) need the L2,
+    // and -1% at C3 (state ~ L2): used when the images are small and the state far exceeds L2
+    {
+        const double img = 2.0 * (double)Ly.nCBtc * (Ly.NK + Ly.NP2) * 128.0;
+        p.theta_l2 = (img <= 32e6 && Ly.N >= 8192) ? 3 : 0;
+        if (const char *e = std::getenv("CR_TC_THETA_L2")) p.theta_l2 = std::atoi(e);
+    }
     p.smem_bytes = ctx->smem_tc;
     p.g1_hi = ctx->at<float>(Ly.g1h);
     p.g1_lo = ctx->at<float>(Ly.g1l);

@@ -162,6 +162,7 @@ struct TcParams {
     int g1stages, g2stages;          // X_J / X_J^T image ring slots
     int adapt;                       // 1: also accumulate ||Theta^k - theta~||^2 per row (adaptive step)
     int poll_ns;                     // producer back-off when no ring slot is free (ns)
+    int theta_l2;                    // 1: Theta loads/stores with the evict-normal L2 policy (state ~ L2 size)
     int smem_bytes;
     const float *g1_hi, *g1_lo;      // [nCB][NK * 32]  X_J  tiles (K-major interleave), tf32 hi / lo
     const float *g2_hi, *g2_lo;      // [nCB][NP2 * 32] X_J^T tiles (K-major interleave), tf32 hi / lo

@@ -188,7 +188,9 @@ pass_tc_kernel(const TcParams p) {
         // One thread feeds the three rings, polling their free-slot barriers without blocking:
         // each ring's loads go out as soon as its next slot is released.
         if (lane == 0) {
-            const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+            // Theta streams past L2 (evict-first) unless the whole state fits in it (p.theta_l2)
+            const uint64_t pol_stream = (p.theta_l2 & 1) ? policy_evict_normal() : policy_evict_first();
+            const uint64_t pol_keep = policy_evict_last();
             Cursor c = start(), c1 = start(), c2 = start();
             while (c.u < U || c1.u < U || c2.u < U) {
                 bool issued = false;
@@ -315,7 +317,7 @@ pass_tc_kernel(const TcParams p) {
     } else if (warp == 2) {
         // ============================================================ TMA storer
         if (lane == 0) {
-            const uint64_t pol_stream = policy_evict_first();
+            const uint64_t pol_stream = (p.theta_l2 & 2) ? policy_evict_normal() : policy_evict_first();
             for (Cursor c = start(); c.u < U; adv(c, 1)) {
                 TC_TRACE(2, c.u, 0);
                 mbar_wait(&bar->st_full[c.s], (uint32_t)c.ph);

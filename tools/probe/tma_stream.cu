@@ -18,10 +18,12 @@ __device__ __forceinline__ void bulk_store(void *g, const void *s, uint32_t byte
 }
 
 __global__ void __launch_bounds__(128, 1) stream_kernel(const __grid_constant__ CUtensorMap m1, const __grid_constant__ CUtensorMap m2,
-                                                        const float *A, float *B, int nCB, int64_t T, int S, int mode) {
+                                                        const float *A, float *B, int nCB, int64_t T, int S, int mode,
+                                                        const float *Ximg, int xbytes) {
     extern __shared__ __align__(1024) uint8_t sm_raw[];
     uint8_t *sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
-    Bars *bar = reinterpret_cast<Bars *>(sm + (size_t)S * 2 * TB);
+    Bars *bar = reinterpret_cast<Bars *>(sm + (size_t)S * 2 * TB + (xbytes ? 2 * 24576 : 0));
+    uint8_t *xs = sm + (size_t)S * 2 * TB;
     const int64_t t0 = blockIdx.x * T / gridDim.x, t1 = (blockIdx.x + 1) * T / gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -35,8 +37,10 @@ __global__ void __launch_bounds__(128, 1) stream_kernel(const __grid_constant__ 
         for (int64_t t = t0; t < t1; ++t) {
             mbar_wait(&bar->empty[s], ph ^ 1);
             uint8_t *st = sm + (size_t)s * 2 * TB;
-            mbar_arrive_expect_tx(&bar->full[s], 2 * TB);
+            mbar_arrive_expect_tx(&bar->full[s], 2 * TB + xbytes);
             const int rb = (int)(t / nCB), cb = (int)(t % nCB);
+            if (xbytes)   // emulate the pass's per-column-tile X images (L2-resident, evict-last)
+                bulk_load(xs + (s & 1) * 24576, Ximg + (size_t)cb * (xbytes / 4), xbytes, &bar->full[s], policy_evict_last());
             if (mode == 0) {
                 tma_load_2d(st, &m1, cb * 32, rb * 128, &bar->full[s], pol);
                 tma_load_2d(st + TB, &m2, cb * 32, rb * 128, &bar->full[s], pol);
@@ -73,7 +77,10 @@ int main(int argc, char **argv) {
     const int64_t ldT = N, rows = N;
     const int nCB = (int)(N / 32);
     const int64_t T = (rows / 128) * nCB;
-    float *A, *B;
+    const int xbytes = argc > 2 ? atoi(argv[2]) : 0;
+    float *A, *B, *Xi;
+    cudaMalloc(&Xi, (size_t)(N / 32) * (xbytes > 0 ? xbytes : 4));
+    cudaMemset(Xi, 0, (size_t)(N / 32) * (xbytes > 0 ? xbytes : 4));
     cudaMalloc(&A, rows * ldT * 4);
     cudaMalloc(&B, rows * ldT * 4);
     cudaMemset(A, 0, rows * ldT * 4);
@@ -92,19 +99,21 @@ int main(int argc, char **argv) {
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     int nsm;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    for (int mode = 0; mode < 2; ++mode)
+    printf("X image bytes per tile: %d\n", xbytes);
+    for (int mode = 1; mode < 2; ++mode)
         for (int S = 2; S <= 6; ++S) {
-            const int smem = S * 2 * TB + 2048;
+            const int smem = S * 2 * TB + 2048 + (xbytes ? 2 * 24576 : 0);
+            if (smem > 227 * 1024) continue;
             cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             for (int g : {nsm, 2 * nsm}) {
                 if (g == 2 * nsm && S > 3) continue;
                 cudaEvent_t e0, e1;
                 cudaEventCreate(&e0); cudaEventCreate(&e1);
-                for (int w = 0; w < 3; ++w) stream_kernel<<<g, 128, smem>>>(m1, m2, A, B, nCB, T, S, mode);
+                for (int w = 0; w < 3; ++w) stream_kernel<<<g, 128, smem>>>(m1, m2, A, B, nCB, T, S, mode, Xi, xbytes);
                 float best = 1e9;
                 for (int r = 0; r < 10; ++r) {
                     cudaEventRecord(e0);
-                    stream_kernel<<<g, 128, smem>>>(m1, m2, A, B, nCB, T, S, mode);
+                    stream_kernel<<<g, 128, smem>>>(m1, m2, A, B, nCB, T, S, mode, Xi, xbytes);
                     cudaEventRecord(e1);
                     cudaEventSynchronize(e1);
                     float ms; cudaEventElapsedTime(&ms, e0, e1);
