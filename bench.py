@@ -130,6 +130,12 @@ def cpu_baseline(cfg, budget_s):
                       f"of {cfg.name} (n={cfg.n}), {t_used:.1f} s"}
 
 
+def workload(cfg):
+    """The config description both arms print (the driver pairs the lines by it)."""
+    return (f"{cfg.name}: N={cfg.N}, n={cfg.n}, {cfg.x_law} x, f0={cfg.f0}, gamma={cfg.gamma}, Theta0=0, "
+            f"step 1/L (Lanczos)")
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the oracle timed on host cores (rank 0 only)."""
     if rank != 0:
@@ -157,8 +163,8 @@ def run_reference(args, cfg, rank, world):
     line = {"metric": "pair-constraint updates/s (N^2*iters/s)", "value": v, "unit": "pairs/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": 1e3 * t / K, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{cfg.name}: N={cfg.N}, n={cfg.n} (sampled N'={Np})", "N": cfg.N,
-                       "n": cfg.n, "gamma": cfg.gamma},
+            "config": {"workload": workload(cfg), "N": cfg.N, "n": cfg.n, "gamma": cfg.gamma, "iters_timed": K,
+                       "kernel": "oracle (fp64, CPU)", "sampled_N": Np},
             "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": oracle.max_threads(), "kind": "oracle",
                              "sample": f"{K} full fp64 P-APG iterations on the first N'={Np} of {cfg.N} "
                                        f"observations of {cfg.name}"},
@@ -286,8 +292,7 @@ def main():
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if prec == "fp64" else "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: N={cfg.N}, n={cfg.n}, {cfg.x_law} x, f0={cfg.f0}, "
-                               f"gamma={cfg.gamma}, Theta0=0, step 1/L (Lanczos)",
+        "config": {"workload": workload(cfg),
                    "N": cfg.N, "n": cfg.n, "gamma": cfg.gamma, "iters_timed": K,
                    "kernel": s.kernel, "parallelism": f"rows{world}", "step_rule": args.step,
                    "l2": f"inputs larger than L2: Theta state {2 * bpp // 3 * cfg.N * cfg.N / 2**30:.2f} GiB "

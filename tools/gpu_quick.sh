@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x -k "tc or tensor or C3 or C4 or C5 or full_size" > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
 b() { tag=$1; shift; env "$@" timeout 300 python bench.py --no-cpu-baseline --no-e2e $CFG > gpurun_out/q_$tag.json 2> gpurun_out/q_$tag.err; }
-CFG="--config C4"; b C4 X=1
-CFG="--config C3"; b C3_3 CR_TC_THETA_L2=3
+CFG="--config C4"; b C4_532 X=1; b C4_433 CR_TC_STAGES=4; b C4_522 CR_TC_G1STAGES=2 CR_TC_G2STAGES=2; b C4_333 CR_TC_STAGES=3; b C4_532b X=1; b C4_444 CR_TC_STAGES=4 CR_TC_G1STAGES=4 CR_TC_G2STAGES=4
