@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["Config", "CONFIGS", "make_problem", "random_problem", "random_theta"]
+__all__ = ["Config", "CONFIGS", "make_problem", "random_problem", "random_theta", "paper_problem"]
 
 
 @dataclass(frozen=True)
@@ -109,3 +109,32 @@ def random_theta(N: int, seed: int = 0, scale: float = 1.0, density: float = 0.5
     if fp32:
         T = T.astype(np.float32).astype(np.float64)
     return np.ascontiguousarray(T)
+
+
+def paper_problem(N: int, n: int, f0: str = "quad", seed: int = 0):
+    """The synthetic workload of the paper's Section 4, for context runs only:
+    f0 = 1/2 x^T Q x ("quad": Q = Lambda^T Lambda, Lambda iid N(0,1), singular values mapped
+    affinely onto [s_max/15, s_max] so cond(Q) = 15 -- the paper does not say how it transforms
+    them) or f0 = exp(p^T x) ("exp": p ~ U[0, 0.2]^n); x iid N(0, 4), eps iid N(0, 100),
+    ybar = f0(x) + eps, then 30% of the points (chosen at random) get ybar <- 1.3 ybar.
+    Draw order: X, f0 parameters, noise, the 30% subset.  Returns (X, ybar) in float64."""
+    rng = np.random.default_rng(seed)
+    X = 2.0 * rng.standard_normal(size=(N, n))
+    if f0 == "quad":
+        Lam = rng.standard_normal(size=(n, n))
+        U, sv, Vt = np.linalg.svd(Lam.T @ Lam)
+        smax, smin = sv.max(), sv.min()
+        lo = smax / 15.0
+        sv2 = lo + (sv - smin) * (smax - lo) / max(smax - smin, 1e-300)
+        Q = (U * sv2) @ Vt
+        Q = 0.5 * (Q + Q.T)
+        f = 0.5 * np.einsum("ij,jk,ik->i", X, Q, X)
+    elif f0 == "exp":
+        pv = rng.uniform(0.0, 0.2, size=n)
+        f = np.exp(X @ pv)
+    else:
+        raise ValueError(f0)
+    ybar = f + 10.0 * rng.standard_normal(size=N)
+    moved = rng.choice(N, size=int(round(0.3 * N)), replace=False)
+    ybar[moved] *= 1.3
+    return np.ascontiguousarray(X), np.ascontiguousarray(ybar)

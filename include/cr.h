@@ -78,8 +78,13 @@ typedef enum {
 /* Step rule of Step 2 (P:387 / P:400-407). */
 typedef enum {
     CR_STEP_CONSTANT = 0,  /* step 1/L_gamma, Fig. 2 as printed                                  */
-    CR_STEP_ADAPTIVE = 1   /* step 1/s_k, s_k = s_{k-1} ups^(l_k - 1), l_k >= 0 the smallest
-                              integer passing Eq. (adaptive-check); s_0 = L_gamma */
+    CR_STEP_ADAPTIVE = 1,  /* step 1/s_k, s_k = s_{k-1} ups^(l_k - 1), l_k >= 0 the smallest
+                              integer passing Eq. (adaptive-check); s_0 = L_gamma.
+                              The step may grow every iteration; on the paper's own Section-4
+                              workload at N = 2400 this diverges (R18)              */
+    CR_STEP_BACKTRACK = 2  /* not in the paper: the monotone variant s_k = s_{k-1} ups^(l_k),
+                              same check -- steps never grow (Beck-Teboulle backtracking, whose
+                              O(1/k^2) rate holds with L -> max s_k); start below L via s_prev */
 } cr_step_rule;
 
 /* cr_config.flags */

@@ -37,7 +37,7 @@ def lib():
         L.oracle_stats.argtypes = [i64, i32, _dp, _dp, d, dpn, _dp, _dp, _dp, i32]
         L.oracle_project_rows.argtypes = [i64, i32, _dp, _dp, _dp, d, _ip, i64, _dp, _dp, i32]
         L.oracle_papg_adaptive.argtypes = [i64, i32, _dp, _dp, d, d, i64, _dp, _dp, C.POINTER(d), C.POINTER(d),
-                                           _ip, _dp, dpn, dpn, i32, i32]
+                                           _ip, _dp, dpn, dpn, i32, i32, i32]
         for f in (L.oracle_papg, L.oracle_eta, L.oracle_stats, L.oracle_project_rows, L.oracle_papg_adaptive):
             f.restype = C.c_int
         L.oracle_max_threads.restype = C.c_int
@@ -80,7 +80,8 @@ def papg(X, ybar, gamma, L, K, Tprev=None, Tt=None, t=1.0, nthreads=0):
     return dict(Tprev=Tprev, Tt=Tt, t=tt.value, y=y, xi=xi)
 
 
-def papg_adaptive(X, ybar, gamma, s, K, ups=2.0, Tprev=None, Tt=None, t=1.0, max_trials=200, nthreads=0):
+def papg_adaptive(X, ybar, gamma, s, K, ups=2.0, Tprev=None, Tt=None, t=1.0, max_trials=200, backtrack=False,
+                  nthreads=0):
     """K iterations of P-APG with the adaptive step rule of P:400-407 from state
     (theta^{k-1}, theta~^k, t_k, s_{k-1}); the paper's start is theta^0 = 0, t_1 = 1, s_0 = L.
 
@@ -97,7 +98,7 @@ def papg_adaptive(X, ybar, gamma, s, K, ups=2.0, Tprev=None, Tt=None, t=1.0, max
     tt, ss = C.c_double(float(t)), C.c_double(float(s))
     rc = lib().oracle_papg_adaptive(N, n, X, ybar, float(gamma), float(ups), int(K), Tprev, Tt, C.byref(tt),
                                     C.byref(ss), trials, s_hist, y.ctypes.data, xi.ctypes.data, int(max_trials),
-                                    int(nthreads))
+                                    1 if backtrack else 0, int(nthreads))
     if rc == 1:
         raise MemoryError("oracle_papg_adaptive allocation failed")
     if rc == 2:

@@ -279,10 +279,13 @@ static int dual_value(int64_t N, int n, const double *X, const double *ybar, dou
  * State in/out as oracle_papg plus *s = s_{k-1} (in) / s_{k+K-1} (out).
  * trials[k] (nullable) = l_k + 1 (number of Step-2 evaluations), s_hist[k] (nullable) = s_k.
  * max_trials bounds l_k + 1 (returns 2 if exceeded).
+ * backtrack != 0 selects the monotone variant s_k = s_{k-1} ups^(l_k) (not in the paper; see
+ * DESIGN.md R18): with it the accepted s_k never decrease.
  */
 int oracle_papg_adaptive(int64_t N, int n, const double *X, const double *ybar, double gamma, double ups,
                          int64_t K, double *Tprev, double *Tt, double *t, double *s, int64_t *trials,
-                         double *s_hist, double *y_out, double *xi_out, int max_trials, int nthreads)
+                         double *s_hist, double *y_out, double *xi_out, int max_trials, int backtrack,
+                         int nthreads)
 {
     set_threads(nthreads);
     double *y = (double *)malloc((size_t)N * sizeof(double));
@@ -305,7 +308,9 @@ int oracle_papg_adaptive(int64_t N, int n, const double *X, const double *ybar, 
         double s_k = 0.0;
         int l;
         for (l = 0; l < max_trials; ++l) {
-            s_k = s_prev * pow(ups, (double)l - 1.0);
+            /* paper's rule: s_k = s_{k-1} ups^(l-1) (a step may grow); backtrack != 0: the monotone
+               variant s_k = s_{k-1} ups^l (steps never grow; Beck & Teboulle's backtracking) */
+            s_k = s_prev * pow(ups, backtrack ? (double)l : (double)l - 1.0);
             /* Step 2 with step 1/s_k; <grad g(theta~), D> = -sum R D, ||D||^2. */
             #pragma omp parallel for schedule(dynamic, 1)
             for (int64_t b = 0; b < nb; ++b) {

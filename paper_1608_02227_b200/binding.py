@@ -19,7 +19,7 @@ CR_OK, CR_ERR_INVALID_ARG, CR_ERR_CUDA, CR_ERR_NCCL, CR_ERR_OOM, CR_ERR_STATE, C
 PREC = {"fp32": 0, "fp64": 1}
 KERNEL = {"auto": 0, "simt": 1, "tc": 2}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
-STEP_RULE = {"constant": 0, "adaptive": 1}
+STEP_RULE = {"constant": 0, "adaptive": 1, "backtrack": 2}
 CR_FLAG_ADAPTIVE = 1
 
 # Symbols include/cr.h declares (checked by tests/test_abi.py).

@@ -185,6 +185,7 @@ struct cr_ctx {
     cr_step_rule rule = CR_STEP_CONSTANT;
     double ups = 2.0;    // growth factor upsilon > 1
     int max_trials = 64;  // (s_{k-1}, trial counters: device-resident, DevScalars::ad)
+    bool backtrack = false;  // CR_STEP_BACKTRACK (monotone variant of the adaptive rule)
     cudaGraphExec_t graph_ad[9] = {};   // adaptive iteration (WHILE loop over trials) per (bA, bB)
     int64_t k = 0;
     int G = 0, nCB = 0;
@@ -1193,9 +1194,9 @@ cr_status cr_get_sums(cr_ctx *ctx, int32_t which, double *r, double *c, double *
 cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, double s_prev) {
     cr_status st = check_ctx(ctx);
     if (st != CR_OK) return st;
-    if (rule != CR_STEP_CONSTANT && rule != CR_STEP_ADAPTIVE)
+    if (rule != CR_STEP_CONSTANT && rule != CR_STEP_ADAPTIVE && rule != CR_STEP_BACKTRACK)
         return fail(ctx, CR_ERR_INVALID_ARG, "cr_set_step_rule: unknown rule");
-    if (rule == CR_STEP_ADAPTIVE) {
+    if (rule != CR_STEP_CONSTANT) {
         if (ctx->lay.nbuf < 3)
             return fail(ctx, CR_ERR_STATE, "adaptive step needs the third Theta buffer (cr_config.flags CR_FLAG_ADAPTIVE)");
         if (!(upsilon > 1.0) || !std::isfinite(upsilon))
@@ -1203,11 +1204,14 @@ cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, doubl
         if (s_prev < 0.0 || !std::isfinite(s_prev)) return fail(ctx, CR_ERR_INVALID_ARG, "s_prev must be >= 0");
         ctx->ups = upsilon;
         const double s0 = s_prev > 0.0 ? s_prev : ctx->L;     // s_0 = L_gamma
-        const double ad[8] = {s0, s0 * std::pow(upsilon, -1.0), upsilon, 0.0, 0.0, 0.0, (double)ctx->max_trials, 0.0};
+        const bool mono = rule == CR_STEP_BACKTRACK;
+        const double ad[10] = {s0, mono ? s0 : s0 * std::pow(upsilon, -1.0), upsilon, 0.0, 0.0, 0.0,
+                               (double)ctx->max_trials, 0.0, mono ? 1.0 : 0.0, 0.0};
         CK(cudaMemcpyAsync(ctx->at<DevScalars>(ctx->lay.ts)->ad, ad, sizeof ad, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     }
-    ctx->rule = rule;
+    ctx->rule = rule == CR_STEP_CONSTANT ? CR_STEP_CONSTANT : CR_STEP_ADAPTIVE;   // one trial machinery
+    ctx->backtrack = rule == CR_STEP_BACKTRACK;
     return CR_OK;
 }
 
@@ -1237,7 +1241,7 @@ cr_status cr_set_gamma(cr_ctx *ctx, double gamma, double L) {
     ctx->gamma = gamma;
     ctx->L = L > 0.0 ? L : ctx->sigma2 / gamma;
     if (ctx->rule == CR_STEP_ADAPTIVE) {                        // s_0 = L_gamma, l = 0
-        const double v[2] = {ctx->L, ctx->L * std::pow(ctx->ups, -1.0)};
+        const double v[2] = {ctx->L, ctx->backtrack ? ctx->L : ctx->L * std::pow(ctx->ups, -1.0)};
         const double l0 = 0.0;
         DevScalars *ts = ctx->at<DevScalars>(ctx->lay.ts);
         CK(cudaMemcpyAsync(&ts->ad[AD_S], v, sizeof v, cudaMemcpyHostToDevice, ctx->stream));

@@ -45,9 +45,11 @@ struct DevScalars {
     // adaptive step rule state (device-resident so a CUDA-graph WHILE loop can run the trials):
     // [0] s_{k-1}  [1] s of the next trial  [2] ups  [3] trials of the last iteration
     // [4] trials in total  [5] l of the next trial  [6] max trials  [7] error (no l passed)
-    double ad[8];
+    // [8] variant: 0 the paper's s_{k-1} ups^(l-1), 1 monotone backtracking s_{k-1} ups^l
+    double ad[10];
 };
-enum AdaptSlots { AD_S = 0, AD_STRY = 1, AD_UPS = 2, AD_TLAST = 3, AD_TTOT = 4, AD_L = 5, AD_MAX = 6, AD_ERR = 7 };
+enum AdaptSlots { AD_S = 0, AD_STRY = 1, AD_UPS = 2, AD_TLAST = 3, AD_TTOT = 4, AD_L = 5, AD_MAX = 6, AD_ERR = 7,
+                  AD_MONO = 8 };
 
 struct PassParams {
     const void *B1;        // Theta^{k-1} (read)

@@ -209,11 +209,13 @@ __global__ void adapt_decide_kernel(DevScalars *ts, cudaGraphConditionalHandle c
         ad[AD_TLAST] = ad[AD_L] + 1.0;
         ad[AD_TTOT] += ad[AD_L] + 1.0;
         ad[AD_L] = 0.0;
-        ad[AD_STRY] = s * pow(ad[AD_UPS], -1.0);           // s_{k-1} ups^(l-1) at l = 0
+        // next iteration's first trial: s_{k-1} ups^(l-1) at l = 0, or s_{k-1} (monotone)
+        ad[AD_STRY] = ad[AD_MONO] != 0.0 ? s : s * pow(ad[AD_UPS], -1.0);
         more = false;
     } else {
         ad[AD_L] += 1.0;
-        ad[AD_STRY] = ad[AD_S] * pow(ad[AD_UPS], ad[AD_L] - 1.0);   // formed afresh, as the oracle does
+        // formed afresh from s_{k-1}, as the oracle does
+        ad[AD_STRY] = ad[AD_S] * pow(ad[AD_UPS], ad[AD_L] - (ad[AD_MONO] != 0.0 ? 0.0 : 1.0));
         more = ad[AD_L] < ad[AD_MAX];
         if (!more) ad[AD_ERR] = 1.0;
     }

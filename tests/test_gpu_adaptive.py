@@ -159,3 +159,23 @@ def test_adaptive_graph_solve_equals_stepwise(crp, N, n, prec, kernel, monkeypat
     assert ia["trials_total"] == int(np.sum(want["trials"])) and ia["s"] == want["s_hist"][-1]
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("N,n,prec,kernel", [(120, 3, "fp64", "auto"), (1000, 20, "fp32", "tc")])
+def test_backtrack_variant_matches_oracle(crp, N, n, prec, kernel):
+    """CR_STEP_BACKTRACK (monotone, R18) from s_0 = L/64: same decisions as the oracle."""
+    X, ybar = crdata.random_problem(N, n, seed=N + 7, fp32=prec == "fp32")
+    gamma = 1e-3
+    L = ref.lipschitz(X, gamma)
+    K = 25
+    want = oracle.papg_adaptive(X, ybar, gamma, L / 64, K, backtrack=True)
+    s = crp.Solver(X, ybar, gamma, L=L, prec=prec, kernel=kernel, adaptive=True)
+    s.set_step_rule("backtrack", 2.0, s_prev=L / 64)
+    trials = []
+    for _ in range(K):
+        s.step()
+        trials.append(s.step_info()["trials_last"])
+    np.testing.assert_array_equal(trials, want["trials"])
+    assert s.step_info()["s"] == want["s"]
+    assert rel(s.get_theta()[0], want["Tprev"]) <= (1e-11 if prec == "fp64" else 2e-5)
+    s.close()

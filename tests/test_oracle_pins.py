@@ -500,3 +500,32 @@ def test_predict_from_exact_convex_supports():
     # a single data point: f_hat is that point's supporting hyperplane
     z = rng.standard_normal((5, 3))
     np.testing.assert_allclose(ref.predict(X[:1], y[:1], xi[:1], z), y[0] + (z - X[0]) @ xi[0], rtol=1e-14)
+
+
+def test_backtrack_variant_monotone_minimal_and_constant_from_L():
+    """The monotone variant (DESIGN.md R18): s_k = s_{k-1} ups^(l_k), so accepted s_k never decrease;
+    each accepted step passes Eq. (adaptive-check) (dense re-evaluation) and l_k is minimal; started
+    at s_0 = L it is the constant-step Fig. 2 (L bounds the gradient's Lipschitz constant)."""
+    X, ybar = _tiny(8, 2, seed=9)
+    gamma = 0.05
+    L = ref.lipschitz(X, gamma)
+    st = dict(Tprev=None, Tt=None, t=1.0, s=L / 64)
+    prev_s = 0.0
+    for k in range(20):
+        Tt = np.zeros((8, 8)) if st["Tt"] is None else st["Tt"]
+        nxt = oracle.papg_adaptive(X, ybar, gamma, st["s"], 1, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"],
+                                   backtrack=True)
+        s_k, l_k = nxt["s_hist"][0], int(nxt["trials"][0]) - 1
+        assert s_k >= prev_s and math.isclose(s_k, st["s"] * 2.0 ** l_k, rel_tol=1e-15)
+        Tk = nxt["Tprev"]
+        scale = 1.0 + abs(ref.dual_value_dense(ref.theta_vec(Tt), X, ybar, gamma))
+        assert _adaptive_check_dense(Tt, Tk, s_k, X, ybar, gamma) >= -1e-12 * scale
+        if l_k >= 1:
+            Tr = _dense_step(Tt, s_k / 2.0, X, ybar, gamma)
+            assert _adaptive_check_dense(Tt, Tr, s_k / 2.0, X, ybar, gamma) < 0
+        prev_s = s_k
+        st = dict(Tprev=nxt["Tprev"], Tt=nxt["Tt"], t=nxt["t"], s=nxt["s"])
+    a = oracle.papg_adaptive(X, ybar, gamma, L, 25, backtrack=True)
+    c = oracle.papg(X, ybar, gamma, L, 25)
+    assert np.all(a["trials"] == 1) and np.all(a["s_hist"] == L)
+    np.testing.assert_array_equal(a["Tprev"], c["Tprev"])
