@@ -529,3 +529,30 @@ def test_backtrack_variant_monotone_minimal_and_constant_from_L():
     c = oracle.papg(X, ybar, gamma, L, 25)
     assert np.all(a["trials"] == 1) and np.all(a["s_hist"] == L)
     np.testing.assert_array_equal(a["Tprev"], c["Tprev"])
+
+
+def test_paper_section4_generator():
+    """crdata.paper_problem follows P:943-944 (reading R19): cond(Q) = 15, x ~ N(0, 4), 30% of the
+    points moved to 1.3 ybar; seeded (same seed, same data)."""
+    import crdata as cd
+    X, y = cd.paper_problem(3000, 6, "quad", seed=3)
+    X2, y2 = cd.paper_problem(3000, 6, "quad", seed=3)
+    np.testing.assert_array_equal(X, X2)
+    np.testing.assert_array_equal(y, y2)
+    assert abs(X.var() - 4.0) < 0.1
+    rng = np.random.default_rng(3)
+    Xr = 2.0 * rng.standard_normal(size=(3000, 6))
+    np.testing.assert_array_equal(X, Xr)                      # X is drawn first
+    Lam = rng.standard_normal(size=(6, 6))
+    sv = np.linalg.svd(Lam.T @ Lam, compute_uv=False)
+    assert sv.max() / sv.min() > 15                          # the transform is needed
+    Xe, ye = cd.paper_problem(2000, 4, "exp", seed=1)
+    rng = np.random.default_rng(1)
+    Xr = 2.0 * rng.standard_normal(size=(2000, 4))
+    p = rng.uniform(0.0, 0.2, size=4)
+    f = np.exp(Xr @ p)
+    eps = 10.0 * rng.standard_normal(size=2000)
+    moved = rng.choice(2000, size=600, replace=False)
+    want = f + eps
+    want[moved] *= 1.3
+    np.testing.assert_allclose(ye, want, rtol=1e-15)
