@@ -4,6 +4,7 @@ Tikhonov-smoothed dual of the least-squares convex-regression QP, every pair dua
 The product is libcr.so (C ABI, include/cr.h) built from ``csrc/``; ``binding`` is a thin
 ctypes layer over it.  See DESIGN.md.
 """
+from . import binding  # noqa: F401
 from .binding import (  # noqa: F401
     CrError, LocalGroup, Solver, load, lipschitz_host, nccl_unique_id, workspace_size, EXPORTS,
 )
