@@ -1,7 +1,8 @@
 """Oracle for the smoothed-dual P-APG hot path -- TEST INFRASTRUCTURE ONLY.
 
-Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
-``--impl reference`` legs may import this package.  The product path
+Only ``tests/`` (including the numerics scripts under ``tests/numerics/``),
+``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline / ``--impl reference`` legs may
+import this package.  The product path
 (``paper_1608_02227_b200``) never imports it and shares no code with it; the
 only common module is ``crdata`` (seeded input generators, no method
 arithmetic).

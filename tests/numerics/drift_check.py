@@ -1,12 +1,12 @@
 """Diagnostic: GPU (libcr) vs fp64 oracle drift of eta(Theta^K) diagnostics along a run.
 
-    python tools/drift_check.py C2 500,1000,2000 [fp32|fp64] [simt|tc]
+    python tests/numerics/drift_check.py C2 500,1000,2000 [fp32|fp64] [simt|tc]
 """
 import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import crdata  # noqa: E402

@@ -6,13 +6,13 @@ and reports how far eta(Theta^K)'s diagnostics move from the pure fp64 oracle.  
 storage implementation inherits at least this drift.  Uses only oracle/ (fp64 reference) and
 numpy; the CUDA path is not involved.
 
-    python tools/fp32_storage_floor.py C2 500,1000,2000
+    python tests/numerics/fp32_storage_floor.py C2 500,1000,2000
 """
 import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import crdata  # noqa: E402

@@ -5,12 +5,12 @@ rounded to fp32 once per iteration (the storage precision of the fp32 configs), 
 how far Theta^K and the diagnostics of eta(Theta^K) move from the pure fp64 oracle run, and
 whether the accept/reject decisions stay identical.  Uses only oracle/ and crdata.
 
-    python tools/fp32_storage_floor_adaptive.py 300,5,25 1000,20,25
+    python tests/numerics/fp32_storage_floor_adaptive.py 300,5,25 1000,20,25
 """
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import crdata  # noqa: E402

@@ -40,7 +40,7 @@ def crp():
 @pytest.mark.parametrize("N,n,K,prec,kernel,tol", [
     (50, 2, 40, "fp64", "auto", 1e-11),        # C1 shape, SIMT fp64
     (97, 3, 30, "fp64", "auto", 1e-11),        # ragged tiles
-    (300, 5, 15, "fp32", "simt", 2e-5),        # (its fp32-storage floor grows 8e-5 by K=25: tools/fp32_storage_floor_adaptive.py)
+    (300, 5, 15, "fp32", "simt", 2e-5),        # (its fp32-storage floor grows 8e-5 by K=25: tests/numerics/fp32_storage_floor_adaptive.py)
     (1000, 20, 25, "fp32", "tc", 2e-5),        # tcgen05 pass, several 128-row blocks, ragged tail
     (700, 40, 20, "fp32", "tc", 2e-5),
 ])

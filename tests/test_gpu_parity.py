@@ -139,7 +139,7 @@ def test_K_iterations_C2_500(crp):
 
 def test_K_iterations_C2_full(crp):
     """C2 after its full 2000 iterations.  Objective within 1e-4.  The max violation is bounded by
-    the fp32-storage floor (tools/fp32_storage_floor.py): rounding Theta to
+    the fp32-storage floor (tests/numerics/fp32_storage_floor.py): rounding Theta to
     fp32 once per iteration -- with every other operation exact -- already moves it by 1.6e-3 at
     K = 2000, so the test uses 5e-3 for that quantity."""
     k_iteration_case(crp, "C2", "fp32", tol_viol=5e-3)
