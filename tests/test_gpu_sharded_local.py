@@ -69,6 +69,7 @@ def run_ranks(crp, world, fn):
     (1000, 20, "fp32", "tc", 2, 30, 2e-5),
     (517, 33, "fp32", "tc", 3, 20, 2e-5),         # ragged shards, partial 128-row blocks
     (900, 10, "fp32", "simt", 4, 20, 2e-5),
+    (4000, 20, "fp32", "tc", 4, 20, 2e-5),        # C3 laws' size on 4 ranks (1000 rows each)
 ])
 def test_sharded_solve_matches_oracle(crp, N, n, prec, kernel, world, K, tol):
     X, ybar = crdata.random_problem(N, n, seed=N + world, fp32=prec == "fp32")
