@@ -33,6 +33,13 @@ double sigma_max_sq_lanczos(int64_t N, int n, const double *X, double tol, int m
 
 using namespace cr;
 
+namespace cr {
+bool pdl_enabled() {
+    static const bool on = !std::getenv("CR_NO_PDL");
+    return on;
+}
+}  // namespace cr
+
 namespace {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }

@@ -5,8 +5,33 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace cr {
+
+// Programmatic dependent launch (PDL) for the per-iteration kernel chain: a kernel launched with
+// pdl_launch may be scheduled while its predecessor drains; it calls pdl_wait() before touching
+// the predecessor's outputs (griddepcontrol.wait: all prerequisite grids complete, memory
+// visible) and pdl_trigger() once its own dependents may launch.  CR_NO_PDL=1 disables it.
+bool pdl_enabled();
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#endif
 
 constexpr int kBM = 64;           // SIMT fused-pass tile rows
 constexpr int kBN = 64;           // SIMT fused-pass tile columns

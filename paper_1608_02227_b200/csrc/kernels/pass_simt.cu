@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
     double *Pd = reinterpret_cast<double *>(smem + S::o_pd);
 
     const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31, warp = tid >> 5;
+    pdl_wait();
+    pdl_trigger();
     const int64_t t0 = (int64_t)blockIdx.x * p.T / p.G;
     const int64_t t1 = (int64_t)(blockIdx.x + 1) * p.T / p.G;
     if (t0 >= t1) return;
@@ -361,7 +363,8 @@ cudaError_t launch_one(const PassParams &p, cudaStream_t s) {
     constexpr int NBP = NB + 4;
     using S = Smem<T, NB, NBP>;
     // dynamic-smem attribute is set once by pass_simt_config (not per launch: graph capture)
-    pass_simt_kernel<T, NB, NBP, MODE><<<p.G, NT, S::bytes, s>>>(p);
+    cudaError_t e = pdl_launch(pass_simt_kernel<T, NB, NBP, MODE>, dim3(p.G), dim3(NT), S::bytes, s, p);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -180,6 +180,10 @@ pass_tc_kernel(const TcParams p) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bar->tmem_base;
+    // setup above (barriers, TMEM) overlaps the predecessor's tail under PDL; its outputs (y', b',
+    // xi', Theta) are read only after this wait
+    pdl_wait();
+    pdl_trigger();
     // TMEM columns: D1[2] 0..63 | Theta^k A operand [2] x (hi 32, lo 32) 64..191 | D2 (NP2) | Xi' hi, lo
     const uint32_t c_d1 = 0, c_at = 64, c_d2 = 192, c_xi = 192 + (uint32_t)NP2;
 
@@ -590,7 +594,7 @@ __global__ void tc_images_kernel(const double *X64, int64_t N, int n, int NK, in
 
 cudaError_t launch_pass_tc(const TcParams &p, cudaStream_t s) {
     switch (p.NK) {
-#define CR_CASE(V) case V: pass_tc_kernel<V><<<p.G, NTHR, p.smem_bytes, s>>>(p); break;
+#define CR_CASE(V) case V: { cudaError_t e = pdl_launch(pass_tc_kernel<V>, dim3(p.G), dim3(NTHR), (size_t)p.smem_bytes, s, p); if (e != cudaSuccess) return e; } break;
         CR_TC_NK_LIST(CR_CASE)
 #undef CR_CASE
         default: return cudaErrorInvalidValue;

@@ -24,6 +24,8 @@ namespace {
 template <typename T>
 __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
     __shared__ double red[4][8];
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double beta = p.use_beta ? (p.ts->t_prev - 1.0) / p.ts->t_cur : 0.0;
     const double scale = p.s_dev ? 1.0 / *p.s_dev : p.scale;
@@ -79,6 +81,8 @@ __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
 // it owns, so the partials are read-only here.
 template <typename Tc>
 __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int ncolb) {
+    pdl_wait();
+    pdl_trigger();
     if ((int)blockIdx.x < ncolb) {
         __shared__ double cs[8][32];
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -371,8 +375,9 @@ cudaError_t launch_prologue(const SmallParams &p, int fp64, cudaStream_t s, int 
     int64_t nb = (p.Ns + 7) / 8;
     if (nb < 1) nb = 1;
     if (nb > kStatBlocks) nb = kStatBlocks;
-    if (fp64) prologue_kernel<double><<<(unsigned)nb, 256, 0, s>>>(p);
-    else prologue_kernel<float><<<(unsigned)nb, 256, 0, s>>>(p);
+    cudaError_t e = fp64 ? pdl_launch(prologue_kernel<double>, dim3((unsigned)nb), dim3(256), 0, s, p)
+                         : pdl_launch(prologue_kernel<float>, dim3((unsigned)nb), dim3(256), 0, s, p);
+    if (e != cudaSuccess) return e;
     if (nb_out) *nb_out = (int)nb;
     return cudaGetLastError();
 }
@@ -381,8 +386,9 @@ cudaError_t launch_reduce(const ReduceParams &p, int fp64, cudaStream_t s) {
     const int ncolb = (int)((p.N + 31) / 32);
     const int64_t nrowb = (p.Ns + 7) / 8;
     const unsigned nb = (unsigned)(ncolb + nrowb);
-    if (fp64) reduce_kernel<double><<<nb, 256, 0, s>>>(p, ncolb);
-    else reduce_kernel<float><<<nb, 256, 0, s>>>(p, ncolb);
+    cudaError_t e = fp64 ? pdl_launch(reduce_kernel<double>, dim3(nb), dim3(256), 0, s, p, ncolb)
+                         : pdl_launch(reduce_kernel<float>, dim3(nb), dim3(256), 0, s, p, ncolb);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
