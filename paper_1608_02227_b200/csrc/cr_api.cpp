@@ -1315,6 +1315,15 @@ cr_status cr_predict(cr_ctx *ctx, const double *Z, int64_t M, double *out) {
     p.Xi = ctx->at<double>(Ly.Xi64);
     double *dZ = nullptr, *dpart = nullptr, *dout = nullptr;
     const size_t zb = (size_t)M * Ly.n * 8, pb = (size_t)p.splits * M * 8, ob = (size_t)M * 8;
+    // stream-ordered temporaries, released on every path
+    struct Tmp {
+        cudaStream_t s;
+        double **ptrs[3];
+        ~Tmp() {
+            for (auto pp : ptrs)
+                if (*pp) cudaFreeAsync(*pp, s);
+        }
+    } tmp{ctx->stream, {&dZ, &dpart, &dout}};
     CK(cudaMallocAsync(&dZ, zb, ctx->stream));
     CK(cudaMallocAsync(&dpart, pb, ctx->stream));
     CK(cudaMallocAsync(&dout, ob, ctx->stream));
@@ -1330,9 +1339,6 @@ cr_status cr_predict(cr_ctx *ctx, const double *Z, int64_t M, double *out) {
     }
     if (ctx->coll) CM(comm_allreduce_f64(ctx->comm, dout, (size_t)M, COLL_MAX, ctx->stream));
     CK(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaFreeAsync(dZ, ctx->stream));
-    CK(cudaFreeAsync(dpart, ctx->stream));
-    CK(cudaFreeAsync(dout, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return CR_OK;
 }
