@@ -175,6 +175,26 @@ def test_graph_solve_equals_stepwise_and_is_deterministic(crp, monkeypatch):
     assert a.launch_count > 37 * 3
 
 
+@pytest.mark.parametrize("N,n", [(1000, 20), (777, 40)])
+def test_tc_graph_solve_equals_stepwise(crp, N, n):
+    """tcgen05 path: graph replay (PDL edges captured) == eager steps, bit for bit, and repeatable."""
+    X, ybar = crdata.random_problem(N, n, seed=N, fp32=True)
+    a = crp.Solver(X, ybar, 1e-3, kernel="tc")
+    b = crp.Solver(X, ybar, 1e-3, kernel="tc")
+    c = crp.Solver(X, ybar, 1e-3, kernel="tc")
+    a.solve(23)
+    for _ in range(23):
+        b.step()
+    c.solve(11)
+    c.solve(12)
+    Ta = a.get_theta()[0]
+    np.testing.assert_array_equal(Ta, b.get_theta()[0])
+    np.testing.assert_array_equal(Ta, c.get_theta()[0])
+    np.testing.assert_array_equal(a.get_sums(0)[2], b.get_sums(0)[2])
+    for s in (a, b, c):
+        s.close()
+
+
 def test_constant_ybar_fixed_point(crp):
     """P11 on the GPU: constant ybar keeps Theta = 0, y = ybar, xi = 0."""
     X, _ = crdata.random_problem(300, 4, seed=3, fp32=True)
