@@ -13,6 +13,9 @@ Contents
     fp64 Fig. 2 iteration (P:377-397) with K = N, plain loops + OpenMP over rows;
     the adaptive-step variant (P:400-407, Eq. (adaptive-check)) written out literally;
     the continuation over gamma_t (Section 2.4.1) in core.py on top of it.
+``partition.py``
+    Fig. 2 with a general partition K < N (Assumption 1): Step 1 = per-block exact
+    G-norm projections through the NNLS dual of each block QP.
 ``ref.py``
     dense A1/A2/C (Def. A1A2), the exact regularized optimum via the
     NNLS form of the dual, the univariate sorted-slope convex fit

@@ -556,3 +556,54 @@ def test_paper_section4_generator():
     want = f + eps
     want[moved] *= 1.3
     np.testing.assert_allclose(ye, want, rtol=1e-15)
+
+
+# ---------------------------------------------------------------- general partition K < N (Section 2.1)
+def test_partition_nbar1_is_the_all_pairs_method():
+    """Nbar = 1 (K = N singleton blocks): no intra-block constraints, Step 1 is the closed form."""
+    from oracle import partition
+    X, ybar = _tiny(12, 2, seed=61)
+    L = ref.lipschitz(X, 0.05)
+    a = partition.papg_partition(X, ybar, 0.05, L, 30, 1)
+    b = oracle.papg(X, ybar, 0.05, L, 30)
+    np.testing.assert_allclose(a["Tprev"], b["Tprev"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(a["y"], b["y"], rtol=0, atol=1e-12)
+
+
+def test_partition_single_block_solves_the_qp_in_step1():
+    """Nbar = N (K = 1): nothing is dualized and Step 1 at theta = 0 is the regularized QP itself,
+    so eta^1 is the exact regularized optimum (P3, NNLS) and Theta stays 0."""
+    from oracle import partition
+    X, ybar = _tiny(7, 2, seed=62)
+    gamma = 0.05
+    opt = ref.regularized_optimum(X, ybar, gamma)
+    a = partition.papg_partition(X, ybar, gamma, ref.lipschitz(X, gamma), 1, 7)
+    np.testing.assert_allclose(a["y"], opt["y"], atol=1e-9)
+    np.testing.assert_allclose(a["xi"], opt["xi"], atol=1e-8)
+    assert np.all(a["Tprev"] == 0)
+
+
+def test_block_projection_kkt():
+    """The block projection satisfies its KKT conditions: feasibility, lambda >= 0, stationarity
+    (by construction), complementarity lambda_p (A eta)_p = 0."""
+    from oracle import partition
+    rng = np.random.default_rng(63)
+    Xb = rng.standard_normal((6, 2))
+    y0, xi0 = rng.standard_normal(6), rng.standard_normal((6, 2))
+    y, xi, lam = partition.project_block(Xb, y0, xi0, 0.1)
+    Ae = ref.dense_A1(6) @ y + ref.dense_A2(Xb) @ xi.reshape(-1)
+    assert Ae.min() >= -1e-9 and lam.min() >= 0
+    assert abs(lam @ Ae) <= 1e-8 * (1 + np.abs(lam).sum())
+
+
+def test_partition_converges_to_regularized_optimum():
+    """Any partition solves the same dual problem's primal (strong duality): P-APG with
+    Nbar = 4 on N = 12 reaches the exact regularized optimum (P3)."""
+    from oracle import partition
+    X, ybar = _tiny(12, 2, seed=64)
+    gamma = 0.05
+    opt = ref.regularized_optimum(X, ybar, gamma)
+    L = ref.lipschitz(X, gamma)
+    a = partition.papg_partition(X, ybar, gamma, L, 3000, 4)
+    y, xi = partition.eta_partition(X, ybar, gamma, a["Tprev"], 4)
+    np.testing.assert_allclose(y, opt["y"], atol=3e-5)      # 8e-6 at 3000 iterations (all-pairs: 3e-6)
