@@ -115,6 +115,13 @@ typedef struct {
     cr_group *local_group;      /* world > 1 without NCCL: all ranks are contexts of ONE process
                                    (one host thread each, same or different GPUs) joined by
                                    cr_local_group_create(world); NULL -> NCCL via nccl_unique_id */
+    int64_t nbar;               /* partition block size Nbar (Assumption 1): 0 or 1 =
+                                   every pair dualized (K = N, the paper's experiments); > 1 = K =
+                                   N / Nbar blocks of consecutive rows, only cross-block pairs
+                                   dualized, Step 1 = per-block G-norm projections (Eq.
+                                   (subgradient_split) P:184-187) by an fp64 interior-point kernel.
+                                   Requires N % Nbar == 0, Nbar <= 128, shard rows % Nbar == 0,
+                                   no CR_FLAG_ADAPTIVE; else CR_ERR_UNSUPPORTED                  */
 } cr_config;
 
 /* Diagnostics of eta(Theta^k) (Theorem 1 semantics) reported per P:951 / P:1106. */
@@ -144,6 +151,10 @@ typedef struct {
 /* Bytes of device workspace cr_init needs for this shape / rank / flags (0 if unsupported). */
 size_t cr_workspace_size(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel,
                          int32_t rank, int32_t world, int32_t flags);
+
+/* Same with a partition block size (cr_config.nbar; 0 or 1 = all pairs). */
+size_t cr_workspace_size_ex(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel,
+                            int32_t rank, int32_t world, int32_t flags, int64_t nbar);
 
 /* Largest n this library was built for. */
 int32_t cr_max_dim(void);
@@ -224,6 +235,22 @@ cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, doubl
 /* s_k of the last accepted step (L for the constant rule), trials l_k + 1 of the last
  * adaptive iteration and the total number of adaptive trials; any pointer may be NULL. */
 cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *trials_total);
+
+/* Partition diagnostics (cr_config.nbar) of the block projections of this rank's LAST Step 1. */
+typedef struct {
+    int64_t nbar;                  /* block size in use (1: K = N, nothing below is set)          */
+    int64_t blocks;                /* blocks of this rank                                         */
+    int32_t ipm_iters_max;         /* interior-point iterations (limit 100)                       */
+    int32_t polish_rounds_max;     /* active-set rounds of the polish (limit 6)                   */
+    int32_t multiplier_iters_max;  /* multiplier iterations per penalty (limit 60; rho 1, 10, 100) */
+    int64_t failed_blocks;         /* blocks whose IPM did not meet its tolerance (relative
+                                      residuals and max complementarity 1e-9, 100 iterations)    */
+    int64_t unpolished_blocks;     /* blocks whose polish did not settle: they keep the IPM point
+                                      (feasible to ~1e-9 relative, not exact)                     */
+} cr_partition_stats;
+
+/* Synchronizes.  CR_ERR_STATE (and *out filled) if failed_blocks > 0. */
+cr_status cr_partition_info(cr_ctx *ctx, cr_partition_stats *out);
 
 /* Change the Tikhonov weight (Eq. (regularize)) of the problem being solved and restart
  * Fig. 2 at the current iterate: theta^0 := Theta^k, theta~^1 = theta^0, t_1 = 1.

@@ -28,7 +28,8 @@ EXPORTS = (
     "cr_get_theta_rows", "cr_get_sums", "cr_dual_step", "cr_solve", "cr_primal", "cr_get_eta", "cr_lipschitz",
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
     "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info", "cr_set_gamma",
-    "cr_continuation", "cr_local_group_create", "cr_local_group_destroy", "cr_predict",
+    "cr_continuation", "cr_local_group_create", "cr_local_group_destroy", "cr_predict", "cr_workspace_size_ex",
+    "cr_partition_info",
 )
 
 
@@ -37,7 +38,8 @@ class CrConfig(C.Structure):
                 ("gamma", C.c_double), ("L", C.c_double), ("prec", C.c_int), ("kernel", C.c_int),
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t), ("flags", C.c_int32), ("local_group", C.c_void_p)]
+                ("workspace_bytes", C.c_size_t), ("flags", C.c_int32), ("local_group", C.c_void_p),
+                ("nbar", C.c_int64)]
 
 
 class CrStepStats(C.Structure):
@@ -67,6 +69,12 @@ class CrContReport(C.Structure):
                 ("L_last", C.c_double), ("last", CrStepStats)]
 
 
+class CrPartitionStats(C.Structure):
+    _fields_ = [("nbar", C.c_int64), ("blocks", C.c_int64), ("ipm_iters_max", C.c_int32),
+                ("polish_rounds_max", C.c_int32), ("multiplier_iters_max", C.c_int32), ("failed_blocks", C.c_int64),
+                ("unpolished_blocks", C.c_int64)]
+
+
 class CrError(RuntimeError):
     pass
 
@@ -86,6 +94,8 @@ def load(path: str = LIB_PATH):
     vp, i64, i32, d = C.c_void_p, C.c_int64, C.c_int32, C.c_double
     sig = {
         "cr_workspace_size": (C.c_size_t, [i64, i32, C.c_int, C.c_int, i32, i32, i32]),
+        "cr_workspace_size_ex": (C.c_size_t, [i64, i32, C.c_int, C.c_int, i32, i32, i32, i64]),
+        "cr_partition_info": (C.c_int, [vp, C.POINTER(CrPartitionStats)]),
         "cr_max_dim": (i32, []),
         "cr_nccl_get_unique_id": (C.c_int, [vp]),
         "cr_init": (C.c_int, [C.POINTER(CrConfig), C.POINTER(vp)]),
@@ -129,9 +139,9 @@ def _f64(a, shape=None):
     return a
 
 
-def workspace_size(N, n, prec="fp32", kernel="auto", rank=0, world=1, flags=0) -> int:
-    return int(load().cr_workspace_size(int(N), int(n), PREC[prec], KERNEL[kernel], int(rank), int(world),
-                                        int(flags)))
+def workspace_size(N, n, prec="fp32", kernel="auto", rank=0, world=1, flags=0, nbar=1) -> int:
+    return int(load().cr_workspace_size_ex(int(N), int(n), PREC[prec], KERNEL[kernel], int(rank), int(world),
+                                           int(flags), int(nbar)))
 
 
 def lipschitz_host(X, gamma) -> float:
@@ -208,7 +218,7 @@ class Solver:
     """
 
     def __init__(self, X, ybar, gamma, L=0.0, prec="fp32", kernel="auto", device=None, stream=None,
-                 group=None, adaptive=False, rank=None):
+                 group=None, adaptive=False, rank=None, nbar=1):
         import torch
         if not torch.cuda.is_available():
             raise CrError("libcr needs a CUDA device (no CPU fallback)")
@@ -235,9 +245,11 @@ class Solver:
         self._uid = uid
         self.row0, self.rows = shard_range(self.N, self.rank, self.world)
         flags = CR_FLAG_ADAPTIVE if adaptive else 0
-        nbytes = workspace_size(self.N, self.n, prec, kernel, self.rank, self.world, flags)
+        self.nbar = int(nbar)
+        nbytes = workspace_size(self.N, self.n, prec, kernel, self.rank, self.world, flags, self.nbar)
         if nbytes == 0:
-            raise CrError(f"unsupported shape/precision: N={self.N} n={self.n} prec={prec} kernel={kernel}")
+            raise CrError(f"unsupported shape/precision: N={self.N} n={self.n} prec={prec} kernel={kernel} "
+                          f"nbar={self.nbar}")
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.stream = torch.cuda.current_stream(dev) if stream is None else stream
         cfg = CrConfig(N=self.N, n=self.n, X=self.X.ctypes.data, ybar=self.ybar.ctypes.data, gamma=self.gamma,
@@ -245,7 +257,7 @@ class Solver:
                        nccl_unique_id=C.cast(uid, C.c_void_p) if uid is not None else None,
                        device=dev.index, stream=self.stream.cuda_stream,
                        workspace=self.workspace.data_ptr(), workspace_bytes=nbytes, flags=flags,
-                       local_group=local.h if local is not None else None)
+                       local_group=local.h if local is not None else None, nbar=self.nbar)
         h = C.c_void_p()
         st = self.lib.cr_init(C.byref(cfg), C.byref(h))
         if st != CR_OK:
@@ -331,6 +343,15 @@ class Solver:
         """Step rule of Step 2: "constant" (1/L) or "adaptive" (needs adaptive=True)."""
         self._check(self.lib.cr_set_step_rule(self.h, STEP_RULE[rule], float(upsilon), float(s_prev)),
                     "cr_set_step_rule")
+
+    def partition_info(self, check: bool = True):
+        """The block projections of the last Step 1 (partition K < N): nbar, blocks, ipm_iters_max,
+        polish_rounds_max, multiplier_iters_max, failed_blocks.  check: raise if any block failed."""
+        ps = CrPartitionStats()
+        st = self.lib.cr_partition_info(self.h, C.byref(ps))
+        if check:
+            self._check(st, "cr_partition_info")
+        return {f: getattr(ps, f) for f, _ in ps._fields_}
 
     def step_info(self):
         """dict(s = s_k of the last accepted step, trials_last = l_k + 1, trials_total)."""

@@ -48,6 +48,10 @@ struct Layout {
     int64_t N = 0, S = 0, Ns = 0, row0 = 0, Rp = 0, ldT = 0;
     int n = 0, NB = 0, NBP = 0, nRB = 0, world = 1, fp64 = 0;
     int nbuf = 2;                  // Theta buffers / sums slots (3 with CR_FLAG_ADAPTIVE)
+    int64_t nbar = 1;              // partition block size (Assumption 1; 1: K = N, all pairs dualized)
+    int64_t ipm_blocks = 0;        // blocks per shard (nbar > 1)
+    size_t ipm_pb = 0, ipm = 0, ipm_it = 0;   // per-block scratch (doubles), scratch and iteration offsets
+    int ipm_smem = 0, ipm_G = 0;
     bool resident = false;         // small-N SMEM-resident solver eligible (row-major, n <= 32, world 1)
     size_t es = 4;
     // tensor-core pass
@@ -70,9 +74,20 @@ bool use_tc(int n, cr_precision prec, cr_kernel kernel) {
 }
 
 bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank, int world, int flags,
-                 Layout *L) {
+                 int64_t nbar, Layout *L) {
     if (N < 2 || n < 1 || world < 1 || rank < 0 || rank >= world) return false;
     if (flags & ~CR_FLAG_ADAPTIVE) return false;
+    if (nbar < 0) return false;
+    L->nbar = std::max<int64_t>(nbar, 1);
+    if (L->nbar > 1) {
+        // Assumption 1: N = K nbar; blocks may not straddle shards; the adaptive check's
+        // quadratic form (R15) holds only for the unconstrained Step 1 (K = N)
+        if (N % L->nbar || L->nbar > kIpmMaxNbar || (flags & CR_FLAG_ADAPTIVE)) return false;
+        if (world > 1 && ((N + world - 1) / world) % L->nbar) return false;
+        L->ipm_G = block_ipm_group((int)L->nbar, n, kIpmMaxSmem);
+        if (L->ipm_G < 1) return false;
+        L->ipm_smem = (int)block_ipm_smem((int)L->nbar, n, L->ipm_G);
+    }
     L->nbuf = (flags & CR_FLAG_ADAPTIVE) ? 3 : 2;
     if (kernel == CR_KERNEL_TC && prec != CR_FP32) return false;
     L->tc = use_tc(n, prec, kernel);
@@ -122,7 +137,7 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
         rp_simt = std::max(rp_simt, (size_t)(L->nRBtc + kGMax) * kTcBM * (L->NP2 + 4) * 8);
     }
     L->rowpart = take(rp_simt);
-    L->resident = !L->tc && n <= 32 && world == 1 && N <= kResidentMaxN;
+    L->resident = !L->tc && n <= 32 && world == 1 && N <= kResidentMaxN && L->nbar == 1;
     if (L->resident) {
         L->yg = take((size_t)N * 8);
         L->cpart = take((size_t)kResidentMaxCTAs * N * 8);
@@ -134,6 +149,12 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     L->ts = take(sizeof(DevScalars));
     L->statpro = take((size_t)kStatBlocks * 8 * 8);
     L->statres = take((size_t)kStatBlocks * 8 * 8);
+    if (L->nbar > 1) {
+        L->ipm_blocks = L->S / L->nbar;
+        L->ipm_pb = block_ipm_scratch_per_block((int)L->nbar, n);
+        L->ipm = take((size_t)L->ipm_blocks * L->ipm_pb * 8);
+        L->ipm_it = take((size_t)L->ipm_blocks * 16);
+    }
     if (L->tc) {
         L->g1h = take((size_t)L->nCBtc * L->NK * 128);
         L->g1l = take((size_t)L->nCBtc * L->NK * 128);
@@ -262,6 +283,7 @@ PassParams pass_params(cr_ctx *ctx, int b_read, int b_read2, int b_out = -1, boo
     p.N = Ly.N;
     p.Ns = Ly.Ns;
     p.row0 = Ly.row0;
+    p.nbar = Ly.nbar;
     p.nRB = Ly.nRB;
     p.nCB = ctx->nCB;
     p.T = ctx->T;
@@ -347,6 +369,7 @@ TcParams tc_params(cr_ctx *ctx, int b1, int b2, int bo, bool adapt = false) {
     p.N = Ly.N;
     p.Ns = Ly.Ns;
     p.row0 = Ly.row0;
+    p.nbar = Ly.nbar;
     p.ldT = Ly.ldT;
     p.T = ctx->T_tc;
     p.G = ctx->G_tc;
@@ -405,6 +428,34 @@ cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
     return CR_OK;
 }
 
+// Partition K < N (Assumption 1): Step 1 = the closed-form point just written by the prologue
+// projected per block onto the intra-block constraints (block_ipm), then the prologue again in
+// from_eta mode to refresh a, the pass operands and (stats) the objective partials.
+cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro) {
+    const Layout &Ly = ctx->lay;
+    BlockIpmParams bp{};
+    bp.nbar = (int)Ly.nbar;
+    bp.n = Ly.n;
+    bp.max_iter = kIpmMaxIter;
+    bp.nblocks = Ly.Ns / Ly.nbar;
+    bp.row0 = Ly.row0;
+    bp.gamma = ctx->gamma;
+    bp.tol = kIpmTol;
+    bp.X64 = ctx->at<double>(Ly.X64);
+    bp.y64 = ctx->at<double>(Ly.y64);
+    bp.Xi64 = ctx->at<double>(Ly.Xi64);
+    bp.scratch = ctx->at<double>(Ly.ipm);
+    bp.scratch_per_block = Ly.ipm_pb;
+    bp.iters = ctx->at<int>(Ly.ipm_it);
+    bp.smem = Ly.ipm_smem;
+    bp.lgroup = Ly.ipm_G;
+    CK(launch_block_ipm(bp, ctx->stream));
+    sp.from_eta = 1;
+    CK(launch_prologue(sp, Ly.fp64, ctx->stream, nb_pro));
+    ctx->launches += 2;
+    return CR_OK;
+}
+
 // One P-APG iteration (no host sync): Step 1 at theta~^k from the sums of Theta^{k-1} (bA) and
 // Theta^{k-2} (bB) with step 1/s (scale), then the fused pass writing Theta^k into buffer bo
 // (bB in place for the constant step; the spare buffer for an adaptive trial) and its sums
@@ -416,6 +467,10 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     SmallParams sp = small_params(ctx, bA, bB, 1, scale, false);
     sp.s_dev = s_dev;
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
+    if (Ly.nbar > 1) {
+        cr_status st = project_blocks(ctx, sp, nullptr);
+        if (st != CR_OK) return st;
+    }
     if (ctx->coll) {
         CM(comm_allgather(ctx->comm, ctx->ws + Ly.yv, (size_t)Ly.S, (int)Ly.es, ctx->stream));
     }
@@ -553,6 +608,10 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     int nb_pro = 0, nb_res = 0;
     SmallParams sp = small_params(ctx, s, s, 0, 1.0, true);
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, &nb_pro));
+    if (Ly.nbar > 1) {
+        cr_status st = project_blocks(ctx, sp, &nb_pro);
+        if (st != CR_OK) return st;
+    }
     double *y64 = ctx->at<double>(Ly.y64);
     if (ctx->coll) CM(comm_allgather(ctx->comm, y64, (size_t)Ly.S, 8, ctx->stream));
     ResidualParams rp{};
@@ -590,8 +649,10 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
         out->k = ctx->k;
         out->t_k = h.t_cur;
         out->r_gamma = 0.5 * u2 + 0.5 * ctx->gamma * xi2;                 // Eq. (regularize)
-        out->g = -0.5 * u2 - 0.5 * ctx->gamma * xi2 - uy;                 // g at eta(theta)
         out->gap = h.stats[4];                                            // <theta, C eta>
+        // g at eta(theta): the Lagrangian at its minimizer, r_gamma - <theta, C eta>; at
+        // K = N its closed form (no cancellation between r_gamma and gap)
+        out->g = Ly.nbar > 1 ? out->r_gamma - out->gap : -0.5 * u2 - 0.5 * ctx->gamma * xi2 - uy;
         out->max_violation = h.stats[6];
         out->infeas_norm = std::sqrt(h.stats[5]) / std::sqrt(Nd * Nd - Nd);
         out->nonfinite = (h.stats[3] + h.stats[7]) > 0 ||
@@ -606,6 +667,10 @@ cr_status compute_eta(cr_ctx *ctx) {
     SmallParams sp = small_params(ctx, ctx->bA, ctx->bA, 0, 1.0, false);
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
     ctx->launches += 1;
+    if (Ly.nbar > 1) {
+        cr_status st = project_blocks(ctx, sp, nullptr);
+        if (st != CR_OK) return st;
+    }
     if (ctx->coll) CM(comm_allgather(ctx->comm, ctx->at<double>(Ly.y64), (size_t)Ly.S, 8, ctx->stream));
     return CR_OK;
 }
@@ -750,8 +815,13 @@ cr_status cr_nccl_get_unique_id(void *out) {
 
 size_t cr_workspace_size(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel, int32_t rank,
                          int32_t world, int32_t flags) {
+    return cr_workspace_size_ex(N, n, prec, kernel, rank, world, flags, 1);
+}
+
+size_t cr_workspace_size_ex(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel, int32_t rank,
+                            int32_t world, int32_t flags, int64_t nbar) {
     Layout L;
-    if (!make_layout(N, n, prec, kernel, rank, world, flags, &L)) return 0;
+    if (!make_layout(N, n, prec, kernel, rank, world, flags, nbar, &L)) return 0;
     return L.total;
 }
 
@@ -793,7 +863,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     ctx->world = cfg->world;
     ctx->device = cfg->device;
     ctx->stream = static_cast<cudaStream_t>(cfg->stream);
-    if (!make_layout(N, n, cfg->prec, cfg->kernel, cfg->rank, cfg->world, cfg->flags, &ctx->lay)) {
+    if (!make_layout(N, n, cfg->prec, cfg->kernel, cfg->rank, cfg->world, cfg->flags, cfg->nbar, &ctx->lay)) {
         delete ctx;
         return CR_ERR_UNSUPPORTED;
     }
@@ -824,6 +894,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         }                                                                                          \
     } while (0)
     IK(cudaMemsetAsync(ctx->ws, 0, Ly.total, ctx->stream));
+    if (Ly.nbar > 1) IK(block_ipm_prepare(Ly.ipm_smem));
     IK(cudaMemcpyAsync(ctx->ws + Ly.X64, cfg->X, (size_t)N * n * 8, cudaMemcpyHostToDevice, ctx->stream));
     IK(cudaMemcpyAsync(ctx->ws + Ly.ybar, cfg->ybar, (size_t)N * 8, cudaMemcpyHostToDevice, ctx->stream));
     if (!(cfg->L > 0.0)) {
@@ -969,8 +1040,8 @@ cr_status cr_set_theta(cr_ctx *ctx, const double *tk1, const double *tk2, double
                 const double v = src[b][i * Ly.N + j];
                 if (!(v >= 0.0) || !std::isfinite(v))
                     return fail(ctx, CR_ERR_INVALID_ARG, "Theta entries must be finite and >= 0");
-                if (Ly.row0 + i == j && v != 0.0)
-                    return fail(ctx, CR_ERR_INVALID_ARG, "Theta diagonal must be 0");
+                if ((Ly.row0 + i) / Ly.nbar == j / Ly.nbar && v != 0.0)
+                    return fail(ctx, CR_ERR_INVALID_ARG, "Theta must be 0 on the diagonal / intra-block pairs");
             }
     }
     drop_graphs(ctx);
@@ -1234,6 +1305,33 @@ cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *
     if (trials_total) *trials_total = (int64_t)ad[AD_TTOT];
     if (a && ad[AD_ERR] != 0.0)
         return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check)", ctx->max_trials);
+    return CR_OK;
+}
+
+cr_status cr_partition_info(cr_ctx *ctx, cr_partition_stats *out) {
+    cr_status st = check_ctx(ctx);
+    if (st != CR_OK) return st;
+    if (!out) return fail(ctx, CR_ERR_INVALID_ARG, "cr_partition_info: out is NULL");
+    const Layout &Ly = ctx->lay;
+    *out = cr_partition_stats{};
+    out->nbar = Ly.nbar;
+    if (Ly.nbar > 1 && Ly.Ns > 0) {
+        const int64_t nb = Ly.Ns / Ly.nbar;
+        std::vector<int32_t> it((size_t)(4 * nb));
+        CK(cudaMemcpyAsync(it.data(), ctx->at<int>(Ly.ipm_it), it.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        out->blocks = nb;
+        for (int64_t b = 0; b < nb; ++b) {
+            out->ipm_iters_max = std::max(out->ipm_iters_max, it[4 * b]);
+            out->polish_rounds_max = std::max(out->polish_rounds_max, it[4 * b + 1]);
+            out->multiplier_iters_max = std::max(out->multiplier_iters_max, it[4 * b + 2]);
+            out->failed_blocks += it[4 * b + 3] == 1;
+            out->unpolished_blocks += it[4 * b + 3] == 2;
+        }
+    }
+    if (out->failed_blocks)
+        return fail(ctx, CR_ERR_STATE, "block projection failed in %lld of %lld blocks", (long long)out->failed_blocks,
+                    (long long)out->blocks);
     return CR_OK;
 }
 

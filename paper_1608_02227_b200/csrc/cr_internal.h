@@ -43,6 +43,10 @@ constexpr int kStatBlocks = 1024; // max CTAs of the stats/residual kernels
 constexpr int kTcBM = 128;        // tensor-core pass tile rows (TMEM lanes)
 constexpr int kTcBN = 32;         // tensor-core pass tile columns
 constexpr int kTcMaxStages = 6;
+constexpr int64_t kIpmMaxNbar = 128;         // partition block size limit (block_ipm smem: S, X, Z)
+constexpr size_t kIpmMaxSmem = 220 * 1024;
+constexpr int kIpmMaxIter = 100;             // interior-point iterations per projection
+constexpr double kIpmTol = 1e-9;             // relative residuals / max complementarity (then the polish)
 constexpr int64_t kResidentMaxN = 4096;   // SMEM-resident small-N solver: eligible sizes
 constexpr int kResidentMaxCTAs = 256;
 
@@ -85,6 +89,7 @@ struct PassParams {
     int dcol;              // that column (n + 1 < NBP)
     int64_t ldT;           // row pitch of Theta, XT, colpart (elements)
     int64_t N, Ns, row0;   // global size, shard rows, first global row of the shard
+    int64_t nbar;          // partition block size (Assumption 1): Theta_ij = 0 when i / nbar == j / nbar
     int nRB, nCB;          // tile grid (row blocks of kBM, column tiles of kBN)
     int64_t T;             // nRB * nCB
     int G;                 // CTAs
@@ -124,6 +129,8 @@ struct SmallParams {
     const double *s_dev;   // non-null: scale = 1 / *s_dev (the adaptive trial's s, device-resident)
     float *XiR;            // optional [Rp][NK] row-major xi * scale (tensor-core pass operand)
     int NK;
+    int from_eta;          // 1: take (y, xi) from y64 / Xi64 (after the block projections) instead of
+                           //    the closed form; refreshes a64, the pass operands and the stat partials
 };
 
 cudaError_t launch_prologue(const SmallParams &p, int prec_fp64, cudaStream_t s, int *nblocks_out);
@@ -190,6 +197,7 @@ struct TcParams {
     int adapt;                       // 1: also accumulate ||Theta^k - theta~||^2 per row (adaptive step)
     int poll_ns;                     // producer back-off when no ring slot is free (ns)
     int theta_l2;                    // 1: Theta loads/stores with the evict-normal L2 policy (state ~ L2 size)
+    int64_t nbar;                    // partition block size (1: all pairs dualized)
     int smem_bytes;
     const float *g1_hi, *g1_lo;      // [nCB][NK * 32]  X_J  tiles (K-major interleave), tf32 hi / lo
     const float *g2_hi, *g2_lo;      // [nCB][NP2 * 32] X_J^T tiles (K-major interleave), tf32 hi / lo
@@ -249,6 +257,28 @@ struct PredictParams {
 };
 int predict_splits(int64_t M, int64_t Ns, int nsm);
 cudaError_t launch_predict(const PredictParams &p, cudaStream_t s);
+
+// Step 1 for a partition K < N (kernels/block_ipm.cu): per block of nbar rows, the G-norm
+// projection of (y64, Xi64) onto the intra-block constraints, in place, by a primal-dual
+// interior-point method; one CTA per block, fp64.
+struct BlockIpmParams {
+    int nbar, n, max_iter;
+    int64_t nblocks, row0;          // blocks of this shard; first global row of the shard
+    double gamma, tol;
+    const double *X64;              // [N][n] (global rows)
+    double *y64;                    // [>= row0 + Ns] (global rows)
+    double *Xi64;                   // [Rp][n] (shard rows)
+    double *scratch;                // [nblocks][scratch_per_block]
+    size_t scratch_per_block;
+    int *iters;                     // [nblocks][4] IPM iterations, polish rounds, multiplier iterations, status
+    int smem;                       // dynamic shared memory bytes
+    int lgroup;                     // points factored concurrently (block_ipm_group)
+};
+size_t block_ipm_scratch_per_block(int nbar, int n);   // doubles
+int block_ipm_group(int nbar, int n, size_t smem_max);  // 0: does not fit
+size_t block_ipm_smem(int nbar, int n, int G);
+cudaError_t launch_block_ipm(const BlockIpmParams &p, cudaStream_t s);
+cudaError_t block_ipm_prepare(int smem);
 
 // Column-major helpers for initialisation.
 cudaError_t launch_fill_inputs(const double *X64, int64_t N, int n, int NB, int NBP, int64_t ldT,

@@ -282,10 +282,12 @@ __global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const int64_t lr = lr0 + r, gr = p.row0 + lr;
+                const int64_t bs = p.nbar > 1 ? gr - gr % p.nbar : gr;   // first row of gr's block
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const int64_t gj = gj0 + c;
-                    const bool ok = (lr < p.Ns) && (gj < p.N) && (gj != gr);
+                    // dualized pairs only: cross-block (Assumption 1; K = N: j != i)
+                    const bool ok = (lr < p.Ns) && (gj < p.N) && (gj < bs || gj >= bs + p.nbar);
                     // theta~ (Step 4 of the previous iteration) - (C eta)/L, combined in fp64 so
                     // the stored value carries one rounding
                     const double b1 = (double)cb1[r][c];

@@ -435,7 +435,14 @@ pass_tc_kernel(const TcParams p) {
             // valid-column bit mask of this thread's row; 'dirty' warps (diagonal / tails) take a
             // separate, warp-uniform masking branch
             uint32_t vmask = row_ok ? (nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u)) : 0u;
-            if (dcol >= 0) vmask &= ~(1u << dcol);
+            if (p.nbar > 1) {
+                // partition (Assumption 1): no dual variable on the intra-block pairs
+                const int64_t bs = (p.row0 + lr) - (p.row0 + lr) % p.nbar - j0;
+                const int lo = (int)max(bs, (int64_t)0), hi = (int)min(bs + p.nbar, (int64_t)TBN);
+                if (lo < hi) vmask &= ~((hi - lo >= 32 ? 0xffffffffu : ((1u << (hi - lo)) - 1u)) << lo);
+            } else if (dcol >= 0) {
+                vmask &= ~(1u << dcol);
+            }
             const bool dirty = __any_sync(0xffffffffu, vmask != 0xffffffffu);
             float rtile = 0.f, dtile = 0.f;
             float *colw = my_colS + ((((c.u >> 1) & 1) * 4) + q) * 32;

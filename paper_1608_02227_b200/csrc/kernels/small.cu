@@ -32,19 +32,30 @@ __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
     double u2 = 0.0, uy = 0.0, xi2 = 0.0, bad = 0.0;
     T *XiT = static_cast<T *>(p.XiT);
     for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < p.Ns; i += (int64_t)gridDim.x * 8) {
-        const double r1 = p.r1[i], r2 = p.r2[i], c1 = p.c1[i], c2 = p.c2[i];
-        const double rt = r1 + beta * (r1 - r2);
-        const double ct = c1 + beta * (c1 - c2);
         const int64_t gi = p.row0 + i;
-        const double u = ct - rt;                       // (A1^T theta~)_i
-        const double y = p.ybar[gi] + u;
+        double rt = 0.0, y, u;
+        if (p.from_eta) {                               // projected Step-1 point (partition K < N)
+            y = p.y64[gi];
+            u = y - p.ybar[gi];
+        } else {
+            const double r1 = p.r1[i], r2 = p.r2[i], c1 = p.c1[i], c2 = p.c2[i];
+            rt = r1 + beta * (r1 - r2);
+            const double ct = c1 + beta * (c1 - c2);
+            u = ct - rt;                                // (A1^T theta~)_i
+            y = p.ybar[gi] + u;
+        }
         const double *x = p.X64 + gi * p.n;
         double a = 0.0, q2 = 0.0;
         for (int d = lane; d < p.n; d += 32) {
-            const double P1 = p.P1[i * p.n + d], P2 = p.P2[i * p.n + d];
-            const double Pt = P1 + beta * (P1 - P2);
-            const double xi = (rt * x[d] - Pt) / p.gamma;   // (A2^T theta~)_i / gamma
-            p.Xi64[i * p.n + d] = xi;
+            double xi;
+            if (p.from_eta) {
+                xi = p.Xi64[i * p.n + d];
+            } else {
+                const double P1 = p.P1[i * p.n + d], P2 = p.P2[i * p.n + d];
+                const double Pt = P1 + beta * (P1 - P2);
+                xi = (rt * x[d] - Pt) / p.gamma;        // (A2^T theta~)_i / gamma
+                p.Xi64[i * p.n + d] = xi;
+            }
             if (XiT) XiT[(int64_t)d * p.Rp + i] = T(xi * scale);
             if (p.XiR) p.XiR[i * p.NK + d] = (float)(xi * scale);
             a += xi * x[d];
@@ -56,7 +67,7 @@ __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
             q2 += __shfl_xor_sync(0xffffffffu, q2, o);
         }
         if (lane == 0) {
-            p.y64[gi] = y;
+            if (!p.from_eta) p.y64[gi] = y;
             p.a64[i] = a;
             static_cast<T *>(p.yv)[gi] = T(y * scale);
             static_cast<T *>(p.bv)[i] = T((a - y) * scale);

@@ -50,6 +50,19 @@ def test_workspace_sizes_and_unsupported(lib):
     assert crp.workspace_size(100, 4, rank=3, world=2) == 0
 
 
+def test_workspace_sizes_partition(lib):
+    """cr_config.nbar (Assumption 1): N % nbar == 0, nbar <= 128, shards aligned, no adaptive."""
+    base = crp.workspace_size(1200, 3, "fp64")
+    assert crp.workspace_size(1200, 3, "fp64", nbar=1) == base == crp.workspace_size(1200, 3, "fp64", nbar=0)
+    assert crp.workspace_size(1200, 3, "fp64", nbar=12) > 0
+    assert crp.workspace_size(1200, 3, "fp64", nbar=7) == 0             # N % nbar
+    assert crp.workspace_size(129 * 2, 3, "fp64", nbar=129) == 0        # nbar > 128
+    assert crp.workspace_size(1200, 3, "fp64", nbar=12, flags=1) == 0   # adaptive check assumes K = N
+    assert crp.workspace_size(1200, 3, "fp64", nbar=12, rank=0, world=2) > 0      # S = 600
+    assert crp.workspace_size(1200, 3, "fp64", nbar=24, rank=0, world=4) == 0     # S = 300
+    assert crp.workspace_size(1200, 3, "fp64", nbar=-1) == 0
+
+
 def test_status_strings(lib):
     assert lib.cr_status_string(0) == b"CR_OK"
     assert lib.cr_status_string(6) == b"CR_ERR_UNSUPPORTED"
