@@ -22,7 +22,7 @@ namespace {
 // sums, coalesced writes of xi; a_i by a fixed-order warp reduction.  Per-block partials of
 // |u|^2, u.ybar, |xi|^2 and a nonfinite flag go to statpart (fixed order: deterministic).
 template <typename T>
-__global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
+__global__ void __launch_bounds__(256, 4) prologue_kernel(const SmallParams p) {
     __shared__ double red[4][8];
     pdl_wait();
     pdl_trigger();
@@ -86,37 +86,72 @@ __global__ void __launch_bounds__(256) prologue_kernel(const SmallParams p) {
     }
 }
 
-// Blocks [0, ncolb): column sums, 32 columns per block, 8 warps splitting the row-block range
+// Blocks [0, ncolb): column sums, 128 (fp32 partials, float4 per lane) or 32 (fp64) columns per
+// block, 8 warps splitting the row-block range
 // (fixed chunks, combined in order).  Remaining blocks: one warp per row, lanes over d <= n (+1),
 // summing that row's run slots in a fixed order.  Every pass rewrites every column of the slots
 // it owns, so the partials are read-only here.
 template <typename Tc>
-__global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p, int ncolb) {
+__global__ void __launch_bounds__(256, 4) reduce_kernel(const ReduceParams p, int ncolb) {
     pdl_wait();
     pdl_trigger();
     if ((int)blockIdx.x < ncolb) {
-        __shared__ double cs[8][32];
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-        const Tc *cp = static_cast<const Tc *>(p.colpart);
         const int rb0 = (int)((int64_t)p.nRB * warp / 8), rb1 = (int)((int64_t)p.nRB * (warp + 1) / 8);
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        if (j < p.N) {
-            int rb = rb0;
-            for (; rb + 4 <= rb1; rb += 4) {
-                s0 += (double)cp[(int64_t)rb * p.ldT + j];
-                s1 += (double)cp[(int64_t)(rb + 1) * p.ldT + j];
-                s2 += (double)cp[(int64_t)(rb + 2) * p.ldT + j];
-                s3 += (double)cp[(int64_t)(rb + 3) * p.ldT + j];
+        if constexpr (sizeof(Tc) == 4) {
+            // fp32 partials: 128 columns per block, a float4 of 4 columns per lane, 4 row blocks
+            // of loads in flight per lane
+            __shared__ double cs4[8][128];
+            const int64_t j = (int64_t)blockIdx.x * 128 + 4 * lane;      // ldT % 4 == 0: in bounds
+            const float *cp = static_cast<const float *>(p.colpart);
+            double s[4] = {0.0, 0.0, 0.0, 0.0};
+            if (j < p.N) {
+                int rb = rb0;
+                for (; rb + 4 <= rb1; rb += 4) {
+                    float4 v[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4 *>(cp + (int64_t)(rb + k) * p.ldT + j);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        s[0] += (double)v[k].x; s[1] += (double)v[k].y; s[2] += (double)v[k].z; s[3] += (double)v[k].w;
+                    }
+                }
+                for (; rb < rb1; ++rb) {
+                    const float4 v = *reinterpret_cast<const float4 *>(cp + (int64_t)rb * p.ldT + j);
+                    s[0] += (double)v.x; s[1] += (double)v.y; s[2] += (double)v.z; s[3] += (double)v.w;
+                }
             }
-            for (; rb < rb1; ++rb) s0 += (double)cp[(int64_t)rb * p.ldT + j];
-        }
-        cs[warp][lane] = (s0 + s1) + (s2 + s3);
-        __syncthreads();
-        if (warp == 0 && j < p.N) {
-            double s = 0.0;
-            for (int w = 0; w < 8; ++w) s += cs[w][lane];
-            p.c_out[j] = s;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cs4[warp][4 * lane + q] = s[q];
+            __syncthreads();
+            if (threadIdx.x < 128) {
+                const int64_t jj = (int64_t)blockIdx.x * 128 + threadIdx.x;
+                double t = 0.0;
+                for (int w = 0; w < 8; ++w) t += cs4[w][threadIdx.x];
+                if (jj < p.N) p.c_out[jj] = t;
+            }
+        } else {
+            __shared__ double cs[8][32];
+            const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+            const Tc *cp = static_cast<const Tc *>(p.colpart);
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            if (j < p.N) {
+                int rb = rb0;
+                for (; rb + 4 <= rb1; rb += 4) {
+                    s0 += (double)cp[(int64_t)rb * p.ldT + j];
+                    s1 += (double)cp[(int64_t)(rb + 1) * p.ldT + j];
+                    s2 += (double)cp[(int64_t)(rb + 2) * p.ldT + j];
+                    s3 += (double)cp[(int64_t)(rb + 3) * p.ldT + j];
+                }
+                for (; rb < rb1; ++rb) s0 += (double)cp[(int64_t)rb * p.ldT + j];
+            }
+            cs[warp][lane] = (s0 + s1) + (s2 + s3);
+            __syncthreads();
+            if (warp == 0 && j < p.N) {
+                double t = 0.0;
+                for (int w = 0; w < 8; ++w) t += cs[w][lane];
+                p.c_out[j] = t;
+            }
         }
     } else {
         // one warp per row, lanes over d <= n (32-bit index math: Ns < 2^31)
@@ -394,7 +429,7 @@ cudaError_t launch_prologue(const SmallParams &p, int fp64, cudaStream_t s, int 
 }
 
 cudaError_t launch_reduce(const ReduceParams &p, int fp64, cudaStream_t s) {
-    const int ncolb = (int)((p.N + 31) / 32);
+    const int ncolb = (int)((p.N + (fp64 ? 31 : 127)) / (fp64 ? 32 : 128));
     const int64_t nrowb = (p.Ns + 7) / 8;
     const unsigned nb = (unsigned)(ncolb + nrowb);
     cudaError_t e = fp64 ? pdl_launch(reduce_kernel<double>, dim3(nb), dim3(256), 0, s, p, ncolb)

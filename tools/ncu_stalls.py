@@ -13,10 +13,15 @@ import tempfile
 
 rep, NK = sys.argv[1], sys.argv[2]
 reason = sys.argv[3] if len(sys.argv) > 3 else "Warp Stall Sampling (All Samples)"
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kf = ["-k", "regex:" + os.environ["KFILTER"]] if os.environ.get("KFILTER") else []
+raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + kf,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, data = rows[1], rows[2:]
+for _i, _r in enumerate(data):                      # several kernels: keep the first section
+    if _r and _r[0] == "Kernel Name":
+        data = data[:_i]
+        break
 ai, si, ri = h.index("Address"), h.index("Source"), h.index(reason)
 base = int(data[0][ai], 16)
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
