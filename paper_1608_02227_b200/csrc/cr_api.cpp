@@ -50,7 +50,7 @@ struct Layout {
     int nbuf = 2;                  // Theta buffers / sums slots (3 with CR_FLAG_ADAPTIVE)
     int64_t nbar = 1;              // partition block size (Assumption 1; 1: K = N, all pairs dualized)
     int64_t ipm_blocks = 0;        // blocks per shard (nbar > 1)
-    size_t ipm_pb = 0, ipm = 0, ipm_it = 0;   // per-block scratch (doubles), scratch and iteration offsets
+    size_t ipm_pb = 0, ipm = 0, ipm_it = 0, ipm_prof = 0;   // per-block scratch (doubles), scratch and iteration offsets
     int ipm_smem = 0, ipm_G = 0;
     bool resident = false;         // small-N SMEM-resident solver eligible (row-major, n <= 32, world 1)
     size_t es = 4;
@@ -154,6 +154,7 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
         L->ipm_pb = block_ipm_scratch_per_block((int)L->nbar, n);
         L->ipm = take((size_t)L->ipm_blocks * L->ipm_pb * 8);
         L->ipm_it = take((size_t)L->ipm_blocks * 16);
+        L->ipm_prof = take((size_t)L->ipm_blocks * 64);
     }
     if (L->tc) {
         L->g1h = take((size_t)L->nCBtc * L->NK * 128);
@@ -449,6 +450,7 @@ cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro) {
     bp.iters = ctx->at<int>(Ly.ipm_it);
     bp.smem = Ly.ipm_smem;
     bp.lgroup = Ly.ipm_G;
+    bp.prof = std::getenv("CR_IPM_PROF") ? ctx->at<unsigned long long>(Ly.ipm_prof) : nullptr;
     CK(launch_block_ipm(bp, ctx->stream));
     sp.from_eta = 1;
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nb_pro));
@@ -1328,6 +1330,12 @@ cr_status cr_partition_info(cr_ctx *ctx, cr_partition_stats *out) {
             out->failed_blocks += it[4 * b + 3] == 1;
             out->unpolished_blocks += it[4 * b + 3] == 2;
         }
+    }
+    if (std::getenv("CR_IPM_PROF") && Ly.nbar > 1 && Ly.Ns > 0) {
+        unsigned long long pf[8];
+        CK(cudaMemcpy(pf, ctx->at<unsigned long long>(Ly.ipm_prof), sizeof pf, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "block_ipm block 0 cycles: factor %llu solve %llu A %llu AT %llu total %llu\n", pf[0], pf[1],
+                     pf[2], pf[3], pf[4]);
     }
     if (out->failed_blocks)
         return fail(ctx, CR_ERR_STATE, "block projection failed in %lld of %lld blocks", (long long)out->failed_blocks,

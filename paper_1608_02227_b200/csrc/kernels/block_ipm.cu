@@ -117,8 +117,9 @@ __device__ void chol(double *A, int k, int lda, double *red) {
     for (int j = 0; j < k; ++j) {
         const double djj = sqrt(fmax(A[j * lda + j], floor_));
         __syncthreads();                                    // everyone has read A[j][j]
-        if (threadIdx.x == 0) A[j * lda + j] = djj;
-        for (int i = j + 1 + threadIdx.x; i < k; i += IT) A[i * lda + j] /= djj;
+        const double rj = 1.0 / djj;
+        if (threadIdx.x == 0) A[j * lda + j] = rj;           // the factor's diagonal is stored inverted
+        for (int i = j + 1 + threadIdx.x; i < k; i += IT) A[i * lda + j] *= rj;
         __syncthreads();
         for (int i = j + 1 + ty; i < k; i += 16) {
             const double aij = A[i * lda + j];
@@ -139,8 +140,9 @@ __device__ void chol_warp(double *A, int k, int lda) {
     for (int j = 0; j < k; ++j) {
         const double djj = sqrt(fmax(A[j * lda + j], floor_));
         __syncwarp();
-        if (lane == 0) A[j * lda + j] = djj;
-        for (int i = j + 1 + lane; i < k; i += 32) A[i * lda + j] /= djj;
+        const double rj = 1.0 / djj;
+        if (lane == 0) A[j * lda + j] = rj;                  // the factor's diagonal is stored inverted
+        for (int i = j + 1 + lane; i < k; i += 32) A[i * lda + j] *= rj;
         __syncwarp();
         for (int i = j + 1 + lane; i < k; i += 32) {
             const double aij = A[i * lda + j];
@@ -150,19 +152,19 @@ __device__ void chol_warp(double *A, int k, int lda) {
     }
 }
 
-// in place: v <- (L L^T)^{-1} v, L the k x k lower factor in smem (row-major, ld k); one warp,
+// in place: v <- (L L^T)^{-1} v, L the k x k lower factor (row-major, ld k, diagonal stored inverted); one warp,
 // column-oriented substitutions (lanes over the rows below / above the pivot)
 __device__ void chol_solve_warp(const double *Lm, int k, double *v) {
     const int lane = threadIdx.x & 31;
     for (int c = 0; c < k; ++c) {
-        if (lane == 0) v[c] /= Lm[c * k + c];
+        if (lane == 0) v[c] *= Lm[c * k + c];
         __syncwarp();
         const double vc = v[c];
         for (int i = c + 1 + lane; i < k; i += 32) v[i] -= Lm[i * k + c] * vc;
         __syncwarp();
     }
     for (int c = k - 1; c >= 0; --c) {
-        if (lane == 0) v[c] /= Lm[c * k + c];
+        if (lane == 0) v[c] *= Lm[c * k + c];
         __syncwarp();
         const double vc = v[c];
         for (int i = lane; i < c; i += 32) v[i] -= Lm[c * k + i] * vc;
@@ -220,7 +222,7 @@ __device__ void factor(const Blk &B) {
                 for (int d = 0; d < n; ++d) {
                     double s = Zl[d * nb + lp];
                     for (int c = 0; c < d; ++c) s -= Ml[d * n + c] * Zl[c * nb + lp];
-                    Zl[d * nb + lp] = s / Ml[d * n + d];
+                    Zl[d * nb + lp] = s * Ml[d * n + d];
                 }
             for (int e = lane; e < n * n; e += 32) B.Lf[(size_t)l * n * n + e] = Ml[e];
         }
@@ -329,6 +331,11 @@ __device__ void solve(const Blk &B, double *by, double *bxi, double *t) {
 
 __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p) {
     extern __shared__ double bsm[];
+    // optional phase timing (thread 0, clock64): [0] factor, [1] solve, [2] A, [3] A^T, [4] total
+    unsigned long long pt[5] = {0, 0, 0, 0, 0}, pt0 = 0;
+    const unsigned long long tk0 = clock64();
+#define PROF_BEGIN() do { if (p.prof && threadIdx.x == 0) pt0 = clock64(); } while (0)
+#define PROF_END(c) do { if (p.prof && threadIdx.x == 0) pt[c] += clock64() - pt0; } while (0)
     __shared__ double red[IT];
     const int nb = p.nbar, n = p.n, m = nb * (nb - 1);
     const int64_t blk = blockIdx.x;
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
     Blk B{nb, n, p.gamma, Xs, S, Mll, Z, Lf, D, red, Drow, G};
     double *ey = eta, *exi = eta + nb, *ry = rhs, *rxi = rhs + nb;
     // starting point: s = max(A eta0, 0) + sc, lambda = sc, sc from the data scale
-    apply_A(B, ey, exi, a);
+    PROF_BEGIN(); apply_A(B, ey, exi, a); PROF_END(2);
     __syncthreads();
     double amax = 0.0;
     for (int q = threadIdx.x; q < m; q += IT) amax = fmax(amax, fabs(a[q]));
@@ -367,8 +374,8 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
     int it = 0;
     for (; it < p.max_iter; ++it) {
         // residuals: r_p = A eta - s (in a), r_d = G (eta - eta0) - A^T lambda (in rhs, negated below)
-        apply_A(B, ey, exi, a);
-        apply_AT(B, lam, ry, rxi);
+        PROF_BEGIN(); apply_A(B, ey, exi, a); PROF_END(2);
+        PROF_BEGIN(); apply_AT(B, lam, ry, rxi); PROF_END(3);
         __syncthreads();
         double mu = 0.0, cmax = 0.0, rp = 0.0, rdn = 0.0;
         for (int q = threadIdx.x; q < m; q += IT) {
@@ -390,16 +397,16 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
         rdn = block_reduce(rdn, red, true);
         if (!isfinite(mu) || !isfinite(rdn) || !isfinite(rp)) { it = p.max_iter; break; }
         if (cmax <= p.tol * sc * sc && rp <= p.tol * sc && rdn <= p.tol * sc) break;
-        factor(B);
+        PROF_BEGIN(); factor(B); PROF_END(0);
         // ---- predictor: w = -lambda - D r_p ; rhs_aff = -r_d + A^T w
         for (int q = threadIdx.x; q < m; q += IT) w[q] = -lam[q] - D[q] * a[q];
         __syncthreads();
-        apply_AT(B, w, tv, tv + nb);
+        PROF_BEGIN(); apply_AT(B, w, tv, tv + nb); PROF_END(3);
         __syncthreads();
         for (int k = threadIdx.x; k < nb * (n + 1); k += IT) ds[k] = -rhs[k] + tv[k];
         __syncthreads();
-        solve(B, ds, ds + nb, tv);                        // ds[0 .. nb (n+1)) = d eta_aff
-        apply_A(B, ds, ds + nb, dsa);                     // A d eta
+        PROF_BEGIN(); solve(B, ds, ds + nb, tv); PROF_END(1);                        // ds[0 .. nb (n+1)) = d eta_aff
+        PROF_BEGIN(); apply_A(B, ds, ds + nb, dsa); PROF_END(2);                     // A d eta
         __syncthreads();
         double ap = 1.0, ad = 1.0;
         for (int q = threadIdx.x; q < m; q += IT) {
@@ -417,12 +424,12 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
         // ---- corrector: w = -lambda + sigma mu / s - D r_p - ds_aff dl_aff / s
         for (int q = threadIdx.x; q < m; q += IT) w[q] = -lam[q] + (sigma * mu - dsa[q] * dla[q]) / s[q] - D[q] * a[q];
         __syncthreads();
-        apply_AT(B, w, tv, tv + nb);
+        PROF_BEGIN(); apply_AT(B, w, tv, tv + nb); PROF_END(3);
         __syncthreads();
         for (int k = threadIdx.x; k < nb * (n + 1); k += IT) ds[k] = -rhs[k] + tv[k];
         __syncthreads();
-        solve(B, ds, ds + nb, tv);
-        apply_A(B, ds, ds + nb, dsa);
+        PROF_BEGIN(); solve(B, ds, ds + nb, tv); PROF_END(1);
+        PROF_BEGIN(); apply_A(B, ds, ds + nb, dsa); PROF_END(2);
         __syncthreads();
         ap = 1.0;
         ad = 1.0;
@@ -466,15 +473,15 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
                 const double rho = kRho * (attempt == 0 ? 1.0 : attempt == 1 ? 10.0 : 100.0);
                 for (int q = threadIdx.x; q < m; q += IT) D[q] = rho * dla[q];
                 __syncthreads();
-                factor(B);
+                PROF_BEGIN(); factor(B); PROF_END(0);
                 bool conv = false;
                 for (int r = 0; r < kPolishIters; ++r) {
-                    apply_AT(B, dsa, ry, rxi);
+                    PROF_BEGIN(); apply_AT(B, dsa, ry, rxi); PROF_END(3);
                     __syncthreads();
                     for (int k = threadIdx.x; k < ne; k += IT) rhs[k] += (k < nb ? 1.0 : p.gamma) * eta0[k];
                     __syncthreads();
-                    solve(B, ry, rxi, tv);
-                    apply_A(B, ry, rxi, a);
+                    PROF_BEGIN(); solve(B, ry, rxi, tv); PROF_END(1);
+                    PROF_BEGIN(); apply_A(B, ry, rxi, a); PROF_END(2);
                     __syncthreads();
                     double cm = 0.0, lm = 0.0;
                     for (int q = threadIdx.x; q < m; q += IT)
@@ -508,6 +515,10 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
 
     for (int k = threadIdx.x; k < nb; k += IT) p.y64[p.row0 + row0 + k] = eta[k];
     for (int e = threadIdx.x; e < nb * n; e += IT) p.Xi64[row0 * n + e] = eta[nb + e];
+    if (p.prof && threadIdx.x == 0) {
+        pt[4] = clock64() - tk0;
+        for (int c = 0; c < 5; ++c) p.prof[8 * blk + c] = pt[c];
+    }
     if (threadIdx.x == 0) {
         // [0] IPM iterations, [1] polish rounds, [2] max multiplier iterations in a round,
         // [3] status: 0 ok, 1 IPM failed (limit / non-finite), 2 polish did not settle
