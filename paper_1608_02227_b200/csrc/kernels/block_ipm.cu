@@ -16,7 +16,8 @@
 namespace cr {
 namespace {
 
-constexpr int IT = 256;
+constexpr int IT = 512;
+constexpr int TY = IT / 16;           // rows of the 16-wide thread grid (Cholesky update, S tiles)
 constexpr int kMaxNbar = 128;         // == kIpmMaxNbar
 constexpr double kRho = 1.0;          // multiplier-method penalty of the polish (G-scaled problem)
 constexpr int kPolishRounds = 6;
@@ -106,7 +107,7 @@ __device__ void apply_AT(const Blk &B, const double *w, double *oy, double *oxi)
 }
 
 // Cholesky (lower, in place) of the k x k smem matrix A (row-major, lda); right-looking, the
-// trailing update on a 16 x 16 thread grid.  Pivots are floored at 1e-15 of the largest diagonal
+// trailing update on a 16-wide thread grid.  Pivots are floored at 1e-15 of the largest diagonal
 // entry (the Schur complement of a late interior-point iteration can lose definiteness to
 // rounding; the polish removes the effect).  Only the lower triangle is read or written.
 __device__ void chol(double *A, int k, int lda, double *red) {
@@ -121,7 +122,7 @@ __device__ void chol(double *A, int k, int lda, double *red) {
         if (threadIdx.x == 0) A[j * lda + j] = rj;           // the factor's diagonal is stored inverted
         for (int i = j + 1 + threadIdx.x; i < k; i += IT) A[i * lda + j] *= rj;
         __syncthreads();
-        for (int i = j + 1 + ty; i < k; i += 16) {
+        for (int i = j + 1 + ty; i < k; i += TY) {
             const double aij = A[i * lda + j];
             for (int c = j + 1 + tx; c <= i; c += 16) A[i * lda + c] -= aij * A[c * lda + j];
         }
@@ -227,10 +228,10 @@ __device__ void factor(const Blk &B) {
             for (int e = lane; e < n * n; e += 32) B.Lf[(size_t)l * n * n + e] = Ml[e];
         }
         __syncthreads();
-        // S -= sum_w Z_w^T Z_w on the lower triangle: 4 x 4 register tiles on a 16 x 16 thread grid
+        // S -= sum_w Z_w^T Z_w on the lower triangle: 4 x 4 register tiles on a 16 x TY thread grid
         const int gw = min(G, nb - l0), K = gw * n;
         const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-        for (int i0 = 4 * ty; i0 < nb; i0 += 64)
+        for (int i0 = 4 * ty; i0 < nb; i0 += 4 * TY)
             for (int j0 = 4 * tx; j0 <= i0; j0 += 64) {
                 double acc[4][4] = {};
                 for (int kk = 0; kk < K; ++kk) {
