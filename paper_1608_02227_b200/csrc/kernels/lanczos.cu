@@ -41,29 +41,58 @@ __global__ void __launch_bounds__(LB) lz_gram_kernel(const double *X, int64_t N,
     }
 }
 
-// per-block partials of Y = sum y, Sa = sum a, Sxi[d] = sum xi_d, w[d] = sum y x_d; a_k = xi_k.x_k
-// part layout per block: [Y, Sa, Sxi[0..n), w[0..n)]
+constexpr int LQ = 4;                 // feature slots per lane: n <= 128
+constexpr int LW = LB / 32;           // warps per block
+constexpr int LROWS = 64;             // rows per block in the per-row kernels
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// per-block partials of Y = sum y, Sa = sum a, Sxi[d] = sum xi_d, w[d] = sum y x_d; a_k = xi_k.x_k.
+// Warp per row (lanes over d, coalesced), rows [b LROWS, (b+1) LROWS) of block b, warp w taking
+// rows w, w + LW, ...; warps combined in order.  part layout per block: [Y, Sa, Sxi[0..n), w[0..n)]
 __global__ void __launch_bounds__(LB) lz_sums_kernel(const double *X, int64_t N, int n, const double *v, double *a,
                                                      double *part) {
-    __shared__ double sh[LB];
+    __shared__ double sh[LW][2 + 2 * 32 * LQ];
     const double *y = v, *xi = v + N;
-    const int64_t k0 = (int64_t)blockIdx.x * LB, k = k0 + threadIdx.x;
-    double yk = 0.0, ak = 0.0;
-    if (k < N) {
-        yk = y[k];
-        for (int d = 0; d < n; ++d) ak += xi[k * n + d] * X[k * n + d];
-        a[k] = ak;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double Y = 0.0, Sa = 0.0, Sx[LQ], W[LQ];
+#pragma unroll
+    for (int q = 0; q < LQ; ++q) { Sx[q] = 0.0; W[q] = 0.0; }
+    const int64_t r0 = (int64_t)blockIdx.x * LROWS, r1 = min(N, r0 + LROWS);
+    for (int64_t k = r0 + warp; k < r1; k += LW) {
+        const double yk = y[k];
+        double ak = 0.0;
+#pragma unroll
+        for (int q = 0; q < LQ; ++q) {
+            const int d = lane + 32 * q;
+            if (d < n) {
+                const double xv = X[k * n + d], xiv = xi[k * n + d];
+                ak += xiv * xv;
+                Sx[q] += xiv;
+                W[q] += yk * xv;
+            }
+        }
+        ak = warp_sum(ak);
+        if (lane == 0) a[k] = ak;
+        Y += yk;
+        Sa += ak;
     }
+    if (lane == 0) { sh[warp][0] = Y; sh[warp][1] = Sa; }
+#pragma unroll
+    for (int q = 0; q < LQ; ++q) {
+        const int d = lane + 32 * q;
+        if (d < n) { sh[warp][2 + d] = Sx[q]; sh[warp][2 + n + d] = W[q]; }
+    }
+    __syncthreads();
     double *out = part + (size_t)blockIdx.x * (2 + 2 * n);
-    double r = block_sum(yk, sh);
-    if (threadIdx.x == 0) out[0] = r;
-    r = block_sum(ak, sh);
-    if (threadIdx.x == 0) out[1] = r;
-    for (int d = 0; d < n; ++d) {
-        r = block_sum(k < N ? xi[k * n + d] : 0.0, sh);
-        if (threadIdx.x == 0) out[2 + d] = r;
-        r = block_sum(k < N ? yk * X[k * n + d] : 0.0, sh);
-        if (threadIdx.x == 0) out[2 + n + d] = r;
+    for (int qq = threadIdx.x; qq < 2 + 2 * n; qq += LB) {
+        double r = 0.0;
+        for (int w = 0; w < LW; ++w) r += sh[w][qq];
+        out[qq] = r;
     }
 }
 
@@ -71,32 +100,68 @@ __global__ void __launch_bounds__(LB) lz_sums_kernel(const double *X, int64_t N,
 __global__ void lz_sums_final_kernel(const double *part, int nb, int n, double *tot) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= 2 + 2 * n) return;
-    double r = 0.0;
-    for (int b = 0; b < nb; ++b) r += part[(size_t)b * (2 + 2 * n) + q];
-    tot[q] = r;
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
+    int b = 0;
+    for (; b + 4 <= nb; b += 4) {
+        r0 += part[(size_t)b * (2 + 2 * n) + q];
+        r1 += part[(size_t)(b + 1) * (2 + 2 * n) + q];
+        r2 += part[(size_t)(b + 2) * (2 + 2 * n) + q];
+        r3 += part[(size_t)(b + 3) * (2 + 2 * n) + q];
+    }
+    for (; b < nb; ++b) r0 += part[(size_t)b * (2 + 2 * n) + q];
+    tot[q] = (r0 + r1) + (r2 + r3);
 }
 
-// out = C^T C v (lanczos.cpp CtC::apply), thread per row k
+// out = C^T C v (lanczos.cpp CtC::apply), warp per row k (lanes over d); S2 is symmetric, so
+// lane d reads S2[e][d] (coalesced) for t_d = sum_e S2[d][e] xi_k[e]
 __global__ void __launch_bounds__(LB) lz_apply_kernel(const double *X, int64_t N, int n, const double *S2,
                                                       const double *s, const double *v, const double *a,
                                                       const double *tot, double *out) {
-    const int64_t k = (int64_t)blockIdx.x * LB + threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t k = (int64_t)blockIdx.x * LW + warp;
     if (k >= N) return;
     const double *y = v, *xi = v + N;
     const double Y = tot[0], Sa = tot[1];
     const double *Sxi = tot + 2, *w = tot + 2 + n;
-    const double *xk = X + k * n, *xik = xi + k * n;
+    double xk[LQ], xik[LQ], sd[LQ];
     double xs = 0.0, sx = 0.0;
-    for (int d = 0; d < n; ++d) { xs += xik[d] * s[d]; sx += Sxi[d] * xk[d]; }
-    const double Nd = (double)N;
-    const double rho = Y - Nd * y[k] + Nd * a[k] - xs;
-    out[k] = 2.0 * Nd * y[k] - 2.0 * Y + Sa - sx - Nd * a[k] + xs;
+#pragma unroll
+    for (int q = 0; q < LQ; ++q) {
+        const int d = lane + 32 * q;
+        xk[q] = d < n ? X[k * n + d] : 0.0;
+        xik[q] = d < n ? xi[k * n + d] : 0.0;
+        sd[q] = d < n ? s[d] : 0.0;
+        xs += xik[q] * sd[q];
+        sx += (d < n ? Sxi[d] : 0.0) * xk[q];
+    }
+    xs = warp_sum(xs);
+    sx = warp_sum(sx);
+    const double Nd = (double)N, yk = y[k], ak = a[k];
+    const double rho = Y - Nd * yk + Nd * ak - xs;
+    if (lane == 0) out[k] = 2.0 * Nd * yk - 2.0 * Y + Sa - sx - Nd * ak + xs;
+    double t[LQ];
+#pragma unroll
+    for (int q = 0; q < LQ; ++q) t[q] = 0.0;
+#pragma unroll
+    for (int qe = 0; qe < LQ; ++qe) {
+        if (32 * qe >= n) break;
+        for (int src = 0; src < 32; ++src) {
+            const int e = 32 * qe + src;
+            const double xe = __shfl_sync(0xffffffffu, xik[qe], src);
+            if (e >= n) break;
+            const double *row = S2 + (size_t)e * n;
+#pragma unroll
+            for (int q = 0; q < LQ; ++q) {
+                const int d = lane + 32 * q;
+                if (d < n) t[q] += row[d] * xe;
+            }
+        }
+    }
     double *ok = out + N + k * n;
-    for (int d = 0; d < n; ++d) {
-        double t = 0.0;
-        const double *row = S2 + (size_t)d * n;
-        for (int e = 0; e < n; ++e) t += row[e] * xik[e];
-        ok[d] = xk[d] * rho - w[d] + (y[k] - a[k]) * s[d] + t;
+#pragma unroll
+    for (int q = 0; q < LQ; ++q) {
+        const int d = lane + 32 * q;
+        if (d < n) ok[d] = xk[q] * rho - w[d] + (yk - ak) * sd[q] + t[q];
     }
 }
 
@@ -124,11 +189,13 @@ __global__ void __launch_bounds__(LB) lz_update_kernel(double *w, const double *
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
-__global__ void lz_final_kernel(const double *part, int nb, double *dst) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// fixed-order sum of nb partials (one block of LB threads: strided partial sums, then a tree)
+__global__ void __launch_bounds__(LB) lz_final_kernel(const double *part, int nb, double *dst) {
+    __shared__ double sh[LB];
     double r = 0.0;
-    for (int b = 0; b < nb; ++b) r += part[b];
-    *dst = r;
+    for (int b = threadIdx.x; b < nb; b += LB) r += part[b];
+    r = block_sum(r, sh);
+    if (threadIdx.x == 0) *dst = r;
 }
 
 // vprev <- v, v <- w / b
@@ -149,7 +216,8 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
     std::vector<double> start((size_t)N * (n + 1));
     lanczos_start(N, n, start.data());
     const int64_t m = N * (int64_t)(n + 1);
-    const int nbk = (int)((N + LB - 1) / LB);
+    const int nbk = (int)((N + LROWS - 1) / LROWS);           // lz_sums blocks
+    const int nba = (int)((N + LW - 1) / LW);                 // lz_apply blocks (warp per row)
     const int nbv = (int)std::min<int64_t>((m + LB - 1) / LB, 1024);
     double *S2 = nullptr, *s = nullptr, *v = nullptr, *vp = nullptr, *w = nullptr, *a = nullptr, *part = nullptr,
            *tot = nullptr, *sc = nullptr;
@@ -177,9 +245,9 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
         for (int it = 0; it < std::min<int64_t>(max_iter, m) && *err == cudaSuccess; ++it) {
             lz_sums_kernel<<<nbk, LB, 0, st>>>(X, N, n, v, a, part);
             lz_sums_final_kernel<<<1, 256, 0, st>>>(part, nbk, n, tot);
-            lz_apply_kernel<<<nbk, LB, 0, st>>>(X, N, n, S2, s, v, a, tot, w);
+            lz_apply_kernel<<<nba, LB, 0, st>>>(X, N, n, S2, s, v, a, tot, w);
             lz_dot_kernel<<<nbv, LB, 0, st>>>(w, v, m, part);
-            lz_final_kernel<<<1, 32, 0, st>>>(part, nbv, sc);
+            lz_final_kernel<<<1, LB, 0, st>>>(part, nbv, sc);
             double hv[2];
             ok(cudaMemcpyAsync(hv, sc, sizeof(double), cudaMemcpyDeviceToHost, st));
             ok(cudaStreamSynchronize(st));
@@ -188,7 +256,7 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
             hv[1] = bprev;
             ok(cudaMemcpyAsync(sc, hv, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
             lz_update_kernel<<<nbv, LB, 0, st>>>(w, v, vp, m, sc, part);
-            lz_final_kernel<<<1, 32, 0, st>>>(part, nbv, sc + 2);
+            lz_final_kernel<<<1, LB, 0, st>>>(part, nbv, sc + 2);
             double b2 = 0.0;
             ok(cudaMemcpyAsync(&b2, sc + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
             ok(cudaStreamSynchronize(st));

@@ -299,10 +299,10 @@ __global__ void __launch_bounds__(256) residual_kernel(const ResidualParams p) {
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t rb = t / ncb, cb = t % ncb;
         __syncthreads();
-        for (int e = threadIdx.x; e < p.n * RBN; e += blockDim.x) {
-            const int d = e / RBN, cc = e % RBN;
+        for (int f = threadIdx.x; f < p.n * RBN; f += blockDim.x) {      // contiguous rows of X
+            const int cc = f / p.n, d = f % p.n;
             const int64_t j = cb * RBN + cc;
-            xs[e] = j < p.N ? p.X64[j * p.n + d] : 0.0;
+            xs[d * RBN + cc] = j < p.N ? p.X64[j * p.n + d] : 0.0;
         }
         for (int e = threadIdx.x; e < RBM * p.n; e += blockDim.x) {
             const int ii = e / p.n, d = e % p.n;
