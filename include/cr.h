@@ -247,6 +247,9 @@ typedef struct {
                                       residuals and max complementarity 1e-9, 100 iterations)    */
     int64_t unpolished_blocks;     /* blocks whose polish did not settle: they keep the IPM point
                                       (feasible to ~1e-9 relative, not exact)                     */
+    int64_t warm_blocks;           /* blocks solved from the previous Step 1's active set and
+                                      multipliers alone (exact; no interior-point run;
+                                      CR_IPM_COLD=1 in the environment disables the warm start)   */
 } cr_partition_stats;
 
 /* Synchronizes.  CR_ERR_STATE (and *out filled) if failed_blocks > 0. */

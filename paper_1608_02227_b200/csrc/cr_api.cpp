@@ -153,7 +153,7 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
         L->ipm_blocks = L->S / L->nbar;
         L->ipm_pb = block_ipm_scratch_per_block((int)L->nbar, n);
         L->ipm = take((size_t)L->ipm_blocks * L->ipm_pb * 8);
-        L->ipm_it = take((size_t)L->ipm_blocks * 16);
+        L->ipm_it = take((size_t)L->ipm_blocks * 32);
         L->ipm_prof = take((size_t)L->ipm_blocks * 64);
     }
     if (L->tc) {
@@ -450,6 +450,7 @@ cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro) {
     bp.iters = ctx->at<int>(Ly.ipm_it);
     bp.smem = Ly.ipm_smem;
     bp.lgroup = Ly.ipm_G;
+    bp.warm = std::getenv("CR_IPM_COLD") ? 0 : 1;
     bp.prof = std::getenv("CR_IPM_PROF") ? ctx->at<unsigned long long>(Ly.ipm_prof) : nullptr;
     CK(launch_block_ipm(bp, ctx->stream));
     sp.from_eta = 1;
@@ -1319,16 +1320,17 @@ cr_status cr_partition_info(cr_ctx *ctx, cr_partition_stats *out) {
     out->nbar = Ly.nbar;
     if (Ly.nbar > 1 && Ly.Ns > 0) {
         const int64_t nb = Ly.Ns / Ly.nbar;
-        std::vector<int32_t> it((size_t)(4 * nb));
+        std::vector<int32_t> it((size_t)(8 * nb));
         CK(cudaMemcpyAsync(it.data(), ctx->at<int>(Ly.ipm_it), it.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         out->blocks = nb;
         for (int64_t b = 0; b < nb; ++b) {
-            out->ipm_iters_max = std::max(out->ipm_iters_max, it[4 * b]);
-            out->polish_rounds_max = std::max(out->polish_rounds_max, it[4 * b + 1]);
-            out->multiplier_iters_max = std::max(out->multiplier_iters_max, it[4 * b + 2]);
-            out->failed_blocks += it[4 * b + 3] == 1;
-            out->unpolished_blocks += it[4 * b + 3] == 2;
+            out->ipm_iters_max = std::max(out->ipm_iters_max, it[8 * b]);
+            out->polish_rounds_max = std::max(out->polish_rounds_max, it[8 * b + 1]);
+            out->multiplier_iters_max = std::max(out->multiplier_iters_max, it[8 * b + 2]);
+            out->failed_blocks += it[8 * b + 3] == 1;
+            out->unpolished_blocks += it[8 * b + 3] == 2;
+            out->warm_blocks += it[8 * b + 4] == 1;
         }
     }
     if (std::getenv("CR_IPM_PROF") && Ly.nbar > 1 && Ly.Ns > 0) {

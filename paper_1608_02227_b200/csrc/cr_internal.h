@@ -270,7 +270,9 @@ struct BlockIpmParams {
     double *Xi64;                   // [Rp][n] (shard rows)
     double *scratch;                // [nblocks][scratch_per_block]
     size_t scratch_per_block;
-    int *iters;                     // [nblocks][4] IPM iterations, polish rounds, multiplier iterations, status
+    int *iters;                     // [nblocks][8] IPM iterations, polish rounds, multiplier iterations,
+                                    // status, warm start settled
+    int warm;                       // 1: try the previous projection's active set first
     int smem;                       // dynamic shared memory bytes
     int lgroup;                     // points factored concurrently (block_ipm_group)
     unsigned long long *prof;       // optional [nblocks][8] clock64 phase totals (CR_IPM_PROF)

@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
     double *s = g, *lam = s + m, *D = lam + m, *a = D + m, *dsa = a + m, *dla = dsa + m, *w = dla + m;
     double *eta = w + m, *eta0 = eta + ne, *rhs = eta0 + ne, *ds = rhs + ne, *tv = ds + ne;
     double *Lf = tv + ne;
+    double *wact = Lf + (size_t)nb * n * n, *wla = wact + m, *wflag = wla + m;   // warm start (persists)
     for (int e = threadIdx.x; e < nb * n; e += IT) Xs[e] = p.X64[(p.row0 + row0) * n + e];
     for (int k = threadIdx.x; k < nb; k += IT) {
         eta0[k] = p.y64[p.row0 + row0 + k];
@@ -360,112 +361,21 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
     __syncthreads();
     Blk B{nb, n, p.gamma, Xs, S, Mll, Z, Lf, D, red, Drow, G};
     double *ey = eta, *exi = eta + nb, *ry = rhs, *rxi = rhs + nb;
-    // starting point: s = max(A eta0, 0) + sc, lambda = sc, sc from the data scale
+    // sc: the data scale of this projection (thresholds below are relative to it)
     PROF_BEGIN(); apply_A(B, ey, exi, a); PROF_END(2);
     __syncthreads();
     double amax = 0.0;
     for (int q = threadIdx.x; q < m; q += IT) amax = fmax(amax, fabs(a[q]));
     amax = block_reduce(amax, red, true);
     const double sc = fmax(1.0, amax);
-    for (int q = threadIdx.x; q < m; q += IT) {
-        s[q] = fmax(a[q], 0.0) + sc;
-        lam[q] = sc * 1e-2;
-    }
-    __syncthreads();
-    int it = 0;
-    for (; it < p.max_iter; ++it) {
-        // residuals: r_p = A eta - s (in a), r_d = G (eta - eta0) - A^T lambda (in rhs, negated below)
-        PROF_BEGIN(); apply_A(B, ey, exi, a); PROF_END(2);
-        PROF_BEGIN(); apply_AT(B, lam, ry, rxi); PROF_END(3);
-        __syncthreads();
-        double mu = 0.0, cmax = 0.0, rp = 0.0, rdn = 0.0;
-        for (int q = threadIdx.x; q < m; q += IT) {
-            a[q] -= s[q];
-            mu += s[q] * lam[q];
-            cmax = fmax(cmax, s[q] * lam[q]);
-            rp = fmax(rp, fabs(a[q]));
-            D[q] = lam[q] / s[q];
-        }
-        for (int k = threadIdx.x; k < nb * (n + 1); k += IT) {
-            const double gk = k < nb ? 1.0 : p.gamma;
-            const double rd = gk * (eta[k] - eta0[k]) - rhs[k];
-            rhs[k] = rd;                                  // r_d
-            rdn = fmax(rdn, fabs(rd));
-        }
-        mu = block_reduce(mu, red, false) / m;
-        cmax = block_reduce(cmax, red, true);
-        rp = block_reduce(rp, red, true);
-        rdn = block_reduce(rdn, red, true);
-        if (!isfinite(mu) || !isfinite(rdn) || !isfinite(rp)) { it = p.max_iter; break; }
-        if (cmax <= p.tol * sc * sc && rp <= p.tol * sc && rdn <= p.tol * sc) break;
-        PROF_BEGIN(); factor(B); PROF_END(0);
-        // ---- predictor: w = -lambda - D r_p ; rhs_aff = -r_d + A^T w
-        for (int q = threadIdx.x; q < m; q += IT) w[q] = -lam[q] - D[q] * a[q];
-        __syncthreads();
-        PROF_BEGIN(); apply_AT(B, w, tv, tv + nb); PROF_END(3);
-        __syncthreads();
-        for (int k = threadIdx.x; k < nb * (n + 1); k += IT) ds[k] = -rhs[k] + tv[k];
-        __syncthreads();
-        PROF_BEGIN(); solve(B, ds, ds + nb, tv); PROF_END(1);                        // ds[0 .. nb (n+1)) = d eta_aff
-        PROF_BEGIN(); apply_A(B, ds, ds + nb, dsa); PROF_END(2);                     // A d eta
-        __syncthreads();
-        double ap = 1.0, ad = 1.0;
-        for (int q = threadIdx.x; q < m; q += IT) {
-            dsa[q] += a[q];                               // ds_aff = A d eta + r_p
-            dla[q] = w[q] - D[q] * (dsa[q] - a[q]);       // dl_aff = w - D A d eta
-            if (dsa[q] < 0) ap = fmin(ap, -s[q] / dsa[q]);
-            if (dla[q] < 0) ad = fmin(ad, -lam[q] / dla[q]);
-        }
-        ap = -block_reduce(-ap, red, true);
-        ad = -block_reduce(-ad, red, true);
-        double mua = 0.0;
-        for (int q = threadIdx.x; q < m; q += IT) mua += (s[q] + ap * dsa[q]) * (lam[q] + ad * dla[q]);
-        mua = block_reduce(mua, red, false) / m;
-        const double sigma = fmin(1.0, pow(mua / mu, 3.0));
-        // ---- corrector: w = -lambda + sigma mu / s - D r_p - ds_aff dl_aff / s
-        for (int q = threadIdx.x; q < m; q += IT) w[q] = -lam[q] + (sigma * mu - dsa[q] * dla[q]) / s[q] - D[q] * a[q];
-        __syncthreads();
-        PROF_BEGIN(); apply_AT(B, w, tv, tv + nb); PROF_END(3);
-        __syncthreads();
-        for (int k = threadIdx.x; k < nb * (n + 1); k += IT) ds[k] = -rhs[k] + tv[k];
-        __syncthreads();
-        PROF_BEGIN(); solve(B, ds, ds + nb, tv); PROF_END(1);
-        PROF_BEGIN(); apply_A(B, ds, ds + nb, dsa); PROF_END(2);
-        __syncthreads();
-        ap = 1.0;
-        ad = 1.0;
-        for (int q = threadIdx.x; q < m; q += IT) {
-            const double dsq = dsa[q] + a[q];
-            const double dlq = w[q] - D[q] * dsa[q];
-            dsa[q] = dsq;
-            dla[q] = dlq;
-            if (dsq < 0) ap = fmin(ap, -s[q] / dsq);
-            if (dlq < 0) ad = fmin(ad, -lam[q] / dlq);
-        }
-        ap = fmin(1.0, 0.995 * (-block_reduce(-ap, red, true)));
-        ad = fmin(1.0, 0.995 * (-block_reduce(-ad, red, true)));
-        for (int q = threadIdx.x; q < m; q += IT) {
-            s[q] += ap * dsa[q];
-            lam[q] += ad * dla[q];
-        }
-        for (int k = threadIdx.x; k < nb * (n + 1); k += IT) eta[k] += ap * ds[k];
-        __syncthreads();
-    }
-    // ---- polish: the IPM leaves eta ~1e-10 off the projection (its Newton systems degrade as
-    // lambda / s spreads); take its active set {lambda > s} and solve the equality-constrained
-    // projection exactly by the method of multipliers, (G + rho A_a^T A_a) eta = G eta0 + A_a^T la,
-    // la <- la - rho A_a eta, adding violated / dropping negative-multiplier constraints between
-    // rounds (a primal active-set correction).  la_full in dsa, the active flags in dla.
+    // ---- polish: solve the equality-constrained projection on a guessed active set exactly by
+    // the method of multipliers, (G + rho A_a^T A_a) eta = G eta0 + A_a^T la, la <- la - rho A_a eta,
+    // adding violated / dropping negative-multiplier constraints between rounds (a primal
+    // active-set correction); settles only at a KKT point of the projection.  Active flags in
+    // dla, multipliers in dsa (set by the caller); eta is overwritten only on success.
     bool polished = false;
     int rounds = 0, mult_iters = 0;
-    const bool ipm_ok = it < p.max_iter;
-    if (ipm_ok) {
-        for (int q = threadIdx.x; q < m; q += IT) {
-            const bool act = lam[q] > s[q];
-            dla[q] = act ? 1.0 : 0.0;
-            dsa[q] = act ? lam[q] : 0.0;
-        }
-        __syncthreads();
+    auto polish = [&]() {
         for (int round = 0; round < kPolishRounds && !polished; ++round) {
             rounds = round + 1;
             double lmax = 0.0;
@@ -512,8 +422,124 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
             }
             __syncthreads();
         }
+    };
+    // 1) warm start: the previous Step 1's active set and multipliers (blocks move little between
+    //    P-APG iterations), verified by the polish itself
+    const bool warm = p.warm && wflag[0] != 0.0;
+    if (warm) {
+        for (int q = threadIdx.x; q < m; q += IT) { dla[q] = wact[q]; dsa[q] = wla[q]; }
+        __syncthreads();
+        polish();
     }
+    // 2) otherwise the interior point method from s = max(A eta0, 0) + sc, lambda = sc / 100, then
+    //    the polish from its active set {lambda > s}
+    int it = 0;
+    bool ipm_ok = true;
+    if (!polished) {
+        rounds = 0;
+        if (warm) {                                       // the failed polish left A eta in a
+            PROF_BEGIN(); apply_A(B, ey, exi, a); PROF_END(2);
+            __syncthreads();
+        }
+        for (int q = threadIdx.x; q < m; q += IT) {
+            s[q] = fmax(a[q], 0.0) + sc;
+            lam[q] = sc * 1e-2;
+        }
+        __syncthreads();
+        for (; it < p.max_iter; ++it) {
+            // residuals: r_p = A eta - s (in a), r_d = G (eta - eta0) - A^T lambda (in rhs, negated below)
+            PROF_BEGIN(); apply_A(B, ey, exi, a); PROF_END(2);
+            PROF_BEGIN(); apply_AT(B, lam, ry, rxi); PROF_END(3);
+            __syncthreads();
+            double mu = 0.0, cmax = 0.0, rp = 0.0, rdn = 0.0;
+            for (int q = threadIdx.x; q < m; q += IT) {
+                a[q] -= s[q];
+                mu += s[q] * lam[q];
+                cmax = fmax(cmax, s[q] * lam[q]);
+                rp = fmax(rp, fabs(a[q]));
+                D[q] = lam[q] / s[q];
+            }
+            for (int k = threadIdx.x; k < nb * (n + 1); k += IT) {
+                const double gk = k < nb ? 1.0 : p.gamma;
+                const double rd = gk * (eta[k] - eta0[k]) - rhs[k];
+                rhs[k] = rd;                                  // r_d
+                rdn = fmax(rdn, fabs(rd));
+            }
+            mu = block_reduce(mu, red, false) / m;
+            cmax = block_reduce(cmax, red, true);
+            rp = block_reduce(rp, red, true);
+            rdn = block_reduce(rdn, red, true);
+            if (!isfinite(mu) || !isfinite(rdn) || !isfinite(rp)) { it = p.max_iter; break; }
+            if (cmax <= p.tol * sc * sc && rp <= p.tol * sc && rdn <= p.tol * sc) break;
+            PROF_BEGIN(); factor(B); PROF_END(0);
+            // ---- predictor: w = -lambda - D r_p ; rhs_aff = -r_d + A^T w
+            for (int q = threadIdx.x; q < m; q += IT) w[q] = -lam[q] - D[q] * a[q];
+            __syncthreads();
+            PROF_BEGIN(); apply_AT(B, w, tv, tv + nb); PROF_END(3);
+            __syncthreads();
+            for (int k = threadIdx.x; k < nb * (n + 1); k += IT) ds[k] = -rhs[k] + tv[k];
+            __syncthreads();
+            PROF_BEGIN(); solve(B, ds, ds + nb, tv); PROF_END(1);                        // ds[0 .. nb (n+1)) = d eta_aff
+            PROF_BEGIN(); apply_A(B, ds, ds + nb, dsa); PROF_END(2);                     // A d eta
+            __syncthreads();
+            double ap = 1.0, ad = 1.0;
+            for (int q = threadIdx.x; q < m; q += IT) {
+                dsa[q] += a[q];                               // ds_aff = A d eta + r_p
+                dla[q] = w[q] - D[q] * (dsa[q] - a[q]);       // dl_aff = w - D A d eta
+                if (dsa[q] < 0) ap = fmin(ap, -s[q] / dsa[q]);
+                if (dla[q] < 0) ad = fmin(ad, -lam[q] / dla[q]);
+            }
+            ap = -block_reduce(-ap, red, true);
+            ad = -block_reduce(-ad, red, true);
+            double mua = 0.0;
+            for (int q = threadIdx.x; q < m; q += IT) mua += (s[q] + ap * dsa[q]) * (lam[q] + ad * dla[q]);
+            mua = block_reduce(mua, red, false) / m;
+            const double sigma = fmin(1.0, pow(mua / mu, 3.0));
+            // ---- corrector: w = -lambda + sigma mu / s - D r_p - ds_aff dl_aff / s
+            for (int q = threadIdx.x; q < m; q += IT) w[q] = -lam[q] + (sigma * mu - dsa[q] * dla[q]) / s[q] - D[q] * a[q];
+            __syncthreads();
+            PROF_BEGIN(); apply_AT(B, w, tv, tv + nb); PROF_END(3);
+            __syncthreads();
+            for (int k = threadIdx.x; k < nb * (n + 1); k += IT) ds[k] = -rhs[k] + tv[k];
+            __syncthreads();
+            PROF_BEGIN(); solve(B, ds, ds + nb, tv); PROF_END(1);
+            PROF_BEGIN(); apply_A(B, ds, ds + nb, dsa); PROF_END(2);
+            __syncthreads();
+            ap = 1.0;
+            ad = 1.0;
+            for (int q = threadIdx.x; q < m; q += IT) {
+                const double dsq = dsa[q] + a[q];
+                const double dlq = w[q] - D[q] * dsa[q];
+                dsa[q] = dsq;
+                dla[q] = dlq;
+                if (dsq < 0) ap = fmin(ap, -s[q] / dsq);
+                if (dlq < 0) ad = fmin(ad, -lam[q] / dlq);
+            }
+            ap = fmin(1.0, 0.995 * (-block_reduce(-ap, red, true)));
+            ad = fmin(1.0, 0.995 * (-block_reduce(-ad, red, true)));
+            for (int q = threadIdx.x; q < m; q += IT) {
+                s[q] += ap * dsa[q];
+                lam[q] += ad * dla[q];
+            }
+            for (int k = threadIdx.x; k < nb * (n + 1); k += IT) eta[k] += ap * ds[k];
+            __syncthreads();
+        }
 
+        ipm_ok = it < p.max_iter;
+        if (ipm_ok) {
+            for (int q = threadIdx.x; q < m; q += IT) {
+                const bool act = lam[q] > s[q];
+                dla[q] = act ? 1.0 : 0.0;
+                dsa[q] = act ? lam[q] : 0.0;
+            }
+            __syncthreads();
+            polish();
+        }
+    }
+    if (polished && p.warm) {
+        for (int q = threadIdx.x; q < m; q += IT) { wact[q] = dla[q]; wla[q] = dsa[q]; }
+        if (threadIdx.x == 0) wflag[0] = 1.0;
+    }
     for (int k = threadIdx.x; k < nb; k += IT) p.y64[p.row0 + row0 + k] = eta[k];
     for (int e = threadIdx.x; e < nb * n; e += IT) p.Xi64[row0 * n + e] = eta[nb + e];
     if (p.prof && threadIdx.x == 0) {
@@ -522,11 +548,13 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
     }
     if (threadIdx.x == 0) {
         // [0] IPM iterations, [1] polish rounds, [2] max multiplier iterations in a round,
-        // [3] status: 0 ok, 1 IPM failed (limit / non-finite), 2 polish did not settle
-        p.iters[4 * blk + 0] = it;
-        p.iters[4 * blk + 1] = rounds;
-        p.iters[4 * blk + 2] = mult_iters;
-        p.iters[4 * blk + 3] = !ipm_ok ? 1 : (!polished ? 2 : 0);
+        // [3] status: 0 ok, 1 IPM failed (limit / non-finite), 2 polish did not settle,
+        // [4] 1 if the warm start settled (no IPM run)
+        p.iters[8 * blk + 0] = it;
+        p.iters[8 * blk + 1] = rounds;
+        p.iters[8 * blk + 2] = mult_iters;
+        p.iters[8 * blk + 3] = !ipm_ok ? 1 : (!polished ? 2 : 0);
+        p.iters[8 * blk + 4] = (warm && it == 0 && polished) ? 1 : 0;
     }
 }
 
@@ -545,7 +573,7 @@ size_t block_ipm_smem(int nbar, int n, int G) {
 
 size_t block_ipm_scratch_per_block(int nbar, int n) {
     const size_t m = (size_t)nbar * (nbar - 1);
-    return 7 * m + 5 * (size_t)nbar * (n + 1) + (size_t)nbar * n * n;
+    return 7 * m + 5 * (size_t)nbar * (n + 1) + (size_t)nbar * n * n + 2 * m + 1;
 }
 
 cudaError_t block_ipm_prepare(int smem) {

@@ -55,7 +55,9 @@ def test_partition_iterations_fp64(crp, N, n, nbar, K, gamma, seed):
     for _ in range(K):
         s.step()
     info = s.partition_info()
-    assert info["nbar"] == nbar and 0 < info["ipm_iters_max"] < 100 and info["failed_blocks"] == 0 and info["unpolished_blocks"] == 0
+    assert info["nbar"] == nbar and info["ipm_iters_max"] < 100
+    assert info["failed_blocks"] == 0 and info["unpolished_blocks"] == 0
+    assert info["blocks"] == N // nbar and 0 < info["warm_blocks"] <= info["blocks"]     # warm starts in use
     T, _, tk, _ = s.get_theta()
     y, xi = s.get_eta()                      # eta of the last Step 1 (at theta~^K)
     mask = partition.block_mask(N, nbar)
@@ -97,6 +99,21 @@ def test_partition_single_step_fp32(crp, N, n, nbar, kernel, K0, seed):
     assert np.all(T[~partition.block_mask(N, nbar)] == 0)
     assert rel(T, want["Tprev"]) <= 1e-5
     assert rel(y, want["y"]) <= 1e-5 and rel(xi, want["xi"]) <= 1e-5
+    s.close()
+
+
+def test_partition_cold_start_matches(crp, monkeypatch):
+    """CR_IPM_COLD=1 (every projection by the interior point + polish) gives the same iterates."""
+    N, n, nbar, K, gamma = 120, 3, 12, 6, 1e-2
+    X, ybar = crdata.random_problem(N, n, seed=11)
+    L = ref.lipschitz(X, gamma)
+    want = partition.papg_partition(X, ybar, gamma, L, K, nbar)
+    monkeypatch.setenv("CR_IPM_COLD", "1")
+    s = crp.Solver(X, ybar, gamma, L=L, prec="fp64", nbar=nbar)
+    s.solve(K)
+    info = s.partition_info()
+    assert info["warm_blocks"] == 0 and info["ipm_iters_max"] > 0
+    assert rel(s.get_theta()[0], want["Tprev"]) <= 1e-8
     s.close()
 
 
