@@ -46,6 +46,8 @@ def crp():
     (96, 5, 32, 5, 1e-2, 1),
     (200, 2, 8, 10, 1e-3, 2),
     (400, 2, 100, 3, 1e-3, 3),               # the paper's block size
+    (60, 1, 2, 6, 1e-2, 4),                  # smallest blocks (2 constraints each), n = 1
+    (64, 7, 64, 3, 1e-2, 5),                 # one block of 64: Nbar = N, Theta = 0
 ])
 def test_partition_iterations_fp64(crp, N, n, nbar, K, gamma, seed):
     X, ybar = crdata.random_problem(N, n, seed=seed)
