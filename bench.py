@@ -259,7 +259,11 @@ def main():
                         nbar=args.nbar)
         if adaptive:
             s2.set_step_rule("adaptive", 2.0)
+        torch.cuda.synchronize()
+        t_init = time.perf_counter() - t0
         s2.solve(K)
+        torch.cuda.synchronize()
+        t_solve = time.perf_counter() - t0 - t_init
         y, xi, _ = s2.primal()
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
@@ -271,7 +275,8 @@ def main():
         e2e = {"value": cfg.N * cfg.N * K / te, "unit": "pairs/s",
                "h2d_bytes_per_step": (X.nbytes + ybar.nbytes) / K,
                "d2h_bytes_per_step": (y.nbytes + xi.nbytes + 64) / K,
-               "timed": "Solver(X, ybar) [H2D + Lanczos L + init] + solve(K) + primal() [D2H y, xi]"}
+               "timed": "Solver(X, ybar) [H2D + Lanczos L + init] + solve(K) + primal() [D2H y, xi]",
+               "split_ms": {"init": 1e3 * t_init, "solve": 1e3 * t_solve, "primal": 1e3 * (te - t_init - t_solve)}}
 
     if rank != 0:
         if group is not None:

@@ -903,8 +903,12 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     if (!(cfg->L > 0.0)) {
         // L = sigma_max(C)^2 / gamma by the device Lanczos (the host cr_lipschitz_host computes
         // the same iteration; fixed-order reductions, so every rank gets the same L)
+        // Small problems (C1-sized) take the host iteration: ~50 Lanczos steps of O(N n^2) host
+        // work beat ~100 device round trips; deterministic either way.
         cudaError_t le = cudaSuccess;
-        const double s2 = sigma_max_sq_lanczos_device(N, n, ctx->at<double>(Ly.X64), 1e-13, 2000, ctx->stream, &le);
+        const bool host = (int64_t)N * (n + 1) <= kLanczosHostMax;
+        const double s2 = host ? sigma_max_sq_lanczos(N, n, cfg->X, 1e-13, 2000)
+                               : sigma_max_sq_lanczos_device(N, n, ctx->at<double>(Ly.X64), 1e-13, 2000, ctx->stream, &le);
         if (le != cudaSuccess) {
             fail(ctx, CR_ERR_CUDA, "cr_init Lanczos: %s", cudaGetErrorString(le));
             return bail(CR_ERR_CUDA);

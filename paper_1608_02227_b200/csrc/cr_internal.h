@@ -47,6 +47,7 @@ constexpr int64_t kIpmMaxNbar = 128;         // partition block size limit (bloc
 constexpr size_t kIpmMaxSmem = 220 * 1024;
 constexpr int kIpmMaxIter = 100;             // interior-point iterations per projection
 constexpr double kIpmTol = 1e-9;             // relative residuals / max complementarity (then the polish)
+constexpr int64_t kLanczosHostMax = 1 << 14;   // N (n + 1) at or below: L by the host Lanczos in cr_init
 constexpr int64_t kResidentMaxN = 4096;   // SMEM-resident small-N solver: eligible sizes
 constexpr int kResidentMaxCTAs = 256;
 
