@@ -221,6 +221,7 @@ def main():
     l0 = s.launch_count
     tr0 = s.step_info()["trials_total"]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ps0 = s.partition_info(check=False) if args.nbar > 1 else None
     torch.cuda.synchronize()
     if group is not None:
         dist.barrier()
@@ -322,7 +323,25 @@ def main():
         "e2e": e2e,
     }
     if args.nbar > 1:
-        line["partition_stats"] = s.partition_info(check=False)
+        # the dominant kernel is the per-block projection: fp64 CUDA-core arithmetic, counted
+        # with the work model of DESIGN.md §9 (FMAs per factorization / solve / product)
+        ps1 = s.partition_info(check=False)
+        nb_, n_ = args.nbar, cfg.n
+        f_fact = nb_ * (n_ * n_ * nb_ + n_ * nb_ + n_ ** 3 / 6) + nb_ ** 3 * n_ / 2 + nb_ ** 3 / 6 + nb_ * nb_
+        f_solve = 2 * nb_ * n_ * n_ + 3 * nb_ * nb_ * n_ + nb_ * nb_
+        f_prod = nb_ * nb_ * n_
+        fmas = (f_fact * (ps1["factorizations"] - ps0["factorizations"]) + f_solve * (ps1["solves"] - ps0["solves"])
+                + f_prod * (ps1["products"] - ps0["products"]))
+        bp_s = ps1["timed_ms"] / 1e3
+        tf = 2 * fmas / max(bp_s, 1e-12) / 1e12
+        fp64_peak = 33.48
+        line["roofline_pass"] = line["roofline"]
+        line["roofline"] = {"bound": "alu", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": tf / fp64_peak,
+                            "traffic": None, "peak_kind": "measured fp64 FFMA (tools/probe/fprate.cu, profiles/r01/fprate.txt)",
+                            "kernel": "block_ipm (per-block projections)", "flops_timed": 2 * fmas,
+                            "avg_launch_ms": ps1["timed_ms"] / max(ps1["timed_launches"], 1),
+                            "share_of_step": ps1["timed_ms"] / max(t_ms, 1e-9)}
+        line["partition_stats"] = ps1
     if not args.no_cpu_baseline and world == 1 and args.nbar == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_budget_s)
     print(json.dumps(line), flush=True)

@@ -250,6 +250,12 @@ typedef struct {
     int64_t warm_blocks;           /* blocks solved from the previous Step 1's active set and
                                       multipliers alone (exact; no interior-point run;
                                       CR_IPM_COLD=1 in the environment disables the warm start)   */
+    int64_t factorizations;        /* cumulative since cr_init, summed over this rank's blocks:   */
+    int64_t solves;                /*   normal-matrix factorizations, solves with them, and       */
+    int64_t products;              /*   A / A^T products (the work model of DESIGN.md §9)         */
+    double timed_ms;               /* summed duration of the block-projection launches of the
+                                      last pass-timing window (cr_set_pass_timing / cr_pass_timing) */
+    int64_t timed_launches;
 } cr_partition_stats;
 
 /* Synchronizes.  CR_ERR_STATE (and *out filled) if failed_blocks > 0. */

@@ -72,7 +72,8 @@ class CrContReport(C.Structure):
 class CrPartitionStats(C.Structure):
     _fields_ = [("nbar", C.c_int64), ("blocks", C.c_int64), ("ipm_iters_max", C.c_int32),
                 ("polish_rounds_max", C.c_int32), ("multiplier_iters_max", C.c_int32), ("failed_blocks", C.c_int64),
-                ("unpolished_blocks", C.c_int64), ("warm_blocks", C.c_int64)]
+                ("unpolished_blocks", C.c_int64), ("warm_blocks", C.c_int64), ("factorizations", C.c_int64),
+                ("solves", C.c_int64), ("products", C.c_int64), ("timed_ms", C.c_double), ("timed_launches", C.c_int64)]
 
 
 class CrError(RuntimeError):

@@ -50,7 +50,7 @@ struct Layout {
     int nbuf = 2;                  // Theta buffers / sums slots (3 with CR_FLAG_ADAPTIVE)
     int64_t nbar = 1;              // partition block size (Assumption 1; 1: K = N, all pairs dualized)
     int64_t ipm_blocks = 0;        // blocks per shard (nbar > 1)
-    size_t ipm_pb = 0, ipm = 0, ipm_it = 0, ipm_prof = 0;   // per-block scratch (doubles), scratch and iteration offsets
+    size_t ipm_pb = 0, ipm = 0, ipm_it = 0, ipm_prof = 0, ipm_work = 0;   // per-block scratch (doubles), scratch and iteration offsets
     int ipm_smem = 0, ipm_G = 0;
     bool resident = false;         // small-N SMEM-resident solver eligible (row-major, n <= 32, world 1)
     size_t es = 4;
@@ -155,6 +155,7 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
         L->ipm = take((size_t)L->ipm_blocks * L->ipm_pb * 8);
         L->ipm_it = take((size_t)L->ipm_blocks * 32);
         L->ipm_prof = take((size_t)L->ipm_blocks * 64);
+        L->ipm_work = take((size_t)L->ipm_blocks * 24);
     }
     if (L->tc) {
         L->g1h = take((size_t)L->nCBtc * L->NK * 128);
@@ -226,6 +227,10 @@ struct cr_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> ev;
     size_t ev_used = 0;
+    std::vector<cudaEvent_t> bp_ev;   // block-projection launches (partition K < N), same switch
+    size_t bp_ev_used = 0;
+    double bp_ms = 0.0;               // their summed time, collected by cr_pass_timing
+    int64_t bp_launches = 0;
     int64_t ev_iters = 0;    // iterations covered by the recorded event pairs
     // small-N SMEM-resident solver (kernels/resident.cu): CTAs, rows per CTA (0: not usable)
     int res_G = 0, res_R = 0, res_ldS = 0;
@@ -407,6 +412,15 @@ TcParams tc_params(cr_ctx *ctx, int b1, int b2, int bo, bool adapt = false) {
     return p;
 }
 
+cudaEvent_t next_bp_event(cr_ctx *ctx) {
+    if (ctx->bp_ev_used == ctx->bp_ev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        ctx->bp_ev.push_back(e);
+    }
+    return ctx->bp_ev[ctx->bp_ev_used++];
+}
+
 cudaEvent_t next_event(cr_ctx *ctx) {
     if (ctx->ev_used == ctx->ev.size()) {
         cudaEvent_t e;
@@ -432,7 +446,7 @@ cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
 // Partition K < N (Assumption 1): Step 1 = the closed-form point just written by the prologue
 // projected per block onto the intra-block constraints (block_ipm), then the prologue again in
 // from_eta mode to refresh a, the pass operands and (stats) the objective partials.
-cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro) {
+cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro, bool allow_timing = false) {
     const Layout &Ly = ctx->lay;
     BlockIpmParams bp{};
     bp.nbar = (int)Ly.nbar;
@@ -451,8 +465,17 @@ cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro) {
     bp.smem = Ly.ipm_smem;
     bp.lgroup = Ly.ipm_G;
     bp.warm = std::getenv("CR_IPM_COLD") ? 0 : 1;
+    bp.work = ctx->at<unsigned long long>(Ly.ipm_work);
     bp.prof = std::getenv("CR_IPM_PROF") ? ctx->at<unsigned long long>(Ly.ipm_prof) : nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (allow_timing && ctx->timing) {
+        e0 = next_bp_event(ctx);
+        e1 = next_bp_event(ctx);
+        if (!e0 || !e1) return fail(ctx, CR_ERR_CUDA, "cudaEventCreate failed");
+        CK(cudaEventRecord(e0, ctx->stream));
+    }
     CK(launch_block_ipm(bp, ctx->stream));
+    if (e1) CK(cudaEventRecord(e1, ctx->stream));
     sp.from_eta = 1;
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nb_pro));
     ctx->launches += 2;
@@ -471,7 +494,7 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     sp.s_dev = s_dev;
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
     if (Ly.nbar > 1) {
-        cr_status st = project_blocks(ctx, sp, nullptr);
+        cr_status st = project_blocks(ctx, sp, nullptr, allow_timing);
         if (st != CR_OK) return st;
     }
     if (ctx->coll) {
@@ -1322,12 +1345,23 @@ cr_status cr_partition_info(cr_ctx *ctx, cr_partition_stats *out) {
     const Layout &Ly = ctx->lay;
     *out = cr_partition_stats{};
     out->nbar = Ly.nbar;
+    out->timed_ms = ctx->bp_ms;
+    out->timed_launches = ctx->bp_launches;
     if (Ly.nbar > 1 && Ly.Ns > 0) {
         const int64_t nb = Ly.Ns / Ly.nbar;
         std::vector<int32_t> it((size_t)(8 * nb));
         CK(cudaMemcpyAsync(it.data(), ctx->at<int>(Ly.ipm_it), it.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         out->blocks = nb;
+        std::vector<unsigned long long> wk((size_t)(3 * nb));
+        CK(cudaMemcpyAsync(wk.data(), ctx->at<unsigned long long>(Ly.ipm_work), wk.size() * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int64_t b = 0; b < nb; ++b) {
+            out->factorizations += (int64_t)wk[3 * b];
+            out->solves += (int64_t)wk[3 * b + 1];
+            out->products += (int64_t)wk[3 * b + 2];
+        }
         for (int64_t b = 0; b < nb; ++b) {
             out->ipm_iters_max = std::max(out->ipm_iters_max, it[8 * b]);
             out->polish_rounds_max = std::max(out->polish_rounds_max, it[8 * b + 1]);
@@ -1483,6 +1517,14 @@ cr_status cr_pass_timing(cr_ctx *ctx, double *total_ms, int64_t *launches) {
     if (launches) *launches = ctx->ev_iters;
     ctx->ev_used = 0;
     ctx->ev_iters = 0;
+    ctx->bp_ms = 0.0;
+    for (size_t i = 0; i + 1 < ctx->bp_ev_used; i += 2) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->bp_ev[i], ctx->bp_ev[i + 1]));
+        ctx->bp_ms += ms;
+    }
+    ctx->bp_launches = (int64_t)(ctx->bp_ev_used / 2);
+    ctx->bp_ev_used = 0;
     return CR_OK;
 }
 
@@ -1493,6 +1535,7 @@ void cr_destroy(cr_ctx *ctx) {
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->trace) cudaFree(ctx->trace);
     for (auto e : ctx->ev) cudaEventDestroy(e);
+    for (auto e : ctx->bp_ev) cudaEventDestroy(e);
     if (ctx->comm.nccl) ncclCommDestroy(ctx->comm.nccl);
     delete ctx;
 }

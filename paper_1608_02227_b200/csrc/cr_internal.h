@@ -277,6 +277,7 @@ struct BlockIpmParams {
     int smem;                       // dynamic shared memory bytes
     int lgroup;                     // points factored concurrently (block_ipm_group)
     unsigned long long *prof;       // optional [nblocks][8] clock64 phase totals (CR_IPM_PROF)
+    unsigned long long *work;       // [nblocks][3] cumulative factorizations, solves, A / A^T products
 };
 size_t block_ipm_scratch_per_block(int nbar, int n);   // doubles
 int block_ipm_group(int nbar, int n, size_t smem_max);  // 0: does not fit

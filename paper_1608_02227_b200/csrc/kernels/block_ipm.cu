@@ -333,10 +333,12 @@ __device__ void solve(const Blk &B, double *by, double *bxi, double *t) {
 __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p) {
     extern __shared__ double bsm[];
     // optional phase timing (thread 0, clock64): [0] factor, [1] solve, [2] A, [3] A^T, [4] total
+    // and call counts (factorizations, solves, A / A^T products) for the work model
     unsigned long long pt[5] = {0, 0, 0, 0, 0}, pt0 = 0;
+    unsigned cnt[4] = {0, 0, 0, 0};
     const unsigned long long tk0 = clock64();
 #define PROF_BEGIN() do { if (p.prof && threadIdx.x == 0) pt0 = clock64(); } while (0)
-#define PROF_END(c) do { if (p.prof && threadIdx.x == 0) pt[c] += clock64() - pt0; } while (0)
+#define PROF_END(c) do { ++cnt[c]; if (p.prof && threadIdx.x == 0) pt[c] += clock64() - pt0; } while (0)
     __shared__ double red[IT];
     const int nb = p.nbar, n = p.n, m = nb * (nb - 1);
     const int64_t blk = blockIdx.x;
@@ -555,6 +557,9 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
         p.iters[8 * blk + 2] = mult_iters;
         p.iters[8 * blk + 3] = !ipm_ok ? 1 : (!polished ? 2 : 0);
         p.iters[8 * blk + 4] = (warm && it == 0 && polished) ? 1 : 0;
+        p.work[3 * blk + 0] += cnt[0];                   // cumulative since cr_init
+        p.work[3 * blk + 1] += cnt[1];
+        p.work[3 * blk + 2] += cnt[2] + cnt[3];
     }
 }
 
