@@ -48,7 +48,11 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p)
     double *as = ys + N;                                        // [R]        a_i - y_i
     double *r1 = as + R, *r2 = r1 + R, *c1 = r2 + R, *c2 = c1 + R;   // sums of Theta^{k-1}, ^{k-2}
     double *P1 = c2 + R, *P2 = P1 + (size_t)R * n;
-    T *xT = reinterpret_cast<T *>(P2 + (size_t)R * n);         // [NMAX][N]  X transposed (conflict-free)
+    // B1 row groups: with N < RT, H column copies of the thread set split the rows (H N <= RT)
+    int H = 1;
+    while (H < 16 && 2 * H * N <= RT) H *= 2;
+    double *cph = P2 + (size_t)R * n;                           // [H][N]     column partials (H > 1)
+    T *xT = reinterpret_cast<T *>(cph + (N < RT ? RT : 0));    // [NMAX][N]  X transposed (conflict-free)
     T *xis = xT + (size_t)N * NMAX;                             // [R][NMAX]  xi of own rows
     T *thA = xis + (size_t)R * NMAX;                            // [R][ldS] Theta^{k-1}
     T *thB = thA + (size_t)R * ldS;                             // [R][ldS] Theta^{k-2} -> Theta^k
@@ -114,17 +118,23 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p)
         __syncthreads();
         RS_TRACE(3);
         // ---------------- B1: Steps 2 + 4, thread per column j (x_j in registers), own rows in
-        // groups of 4 (independent dot products); column partial of the CTA's rows in order
-        for (int64_t j = threadIdx.x; j < N; j += RT) {
+        // groups of 4 (independent dot products); column partial of the CTA's rows in order.
+        // Small N (H > 1): thread (h, j) takes rows h, h + H, ...; the H partials are combined
+        // in h order (fixed: bitwise reproducible)
+        for (int64_t t = threadIdx.x; t < (H > 1 ? (int64_t)H * N : N); t += RT) {
+            const int64_t j = H > 1 ? t % N : t;
+            const int h = H > 1 ? (int)(t / N) : 0;
             T x[NMAX];     // storage precision for the dot products (fp32 configs: as the streaming
                            // SIMT pass does), fp64 for the combine
 #pragma unroll
             for (int d = 0; d < NMAX; ++d) x[d] = xT[(size_t)d * N + j];
             const double yj = ys[j];
             double cs = 0.0;
-            for (int i0 = 0; i0 < rows; i0 += 4) {
+            for (int i0 = h; i0 < rows; i0 += 4 * H) {
                 T s[4] = {T(0), T(0), T(0), T(0)};
-                const int iq[4] = {i0, min(i0 + 1, rows - 1), min(i0 + 2, rows - 1), min(i0 + 3, rows - 1)};
+                int iq[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) iq[q] = min(i0 + q * H, rows - 1);
 #pragma unroll
                 for (int d = 0; d < NMAX; ++d) {
 #pragma unroll
@@ -132,7 +142,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p)
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const int i = i0 + q;
+                    const int i = i0 + q * H;
                     if (i < rows) {
                         // (C eta)_ij / L = (y_j - y_i + a_i)/L - (xi_i / L) . x_j
                         const double RL = (yj + as[i]) * invL - (double)s[q];
@@ -144,8 +154,18 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p)
                     }
                 }
             }
-            if (multi) p.cpart[(int64_t)blockIdx.x * N + j] = cs;
+            if (H > 1) cph[(size_t)h * N + j] = cs;
+            else if (multi) p.cpart[(int64_t)blockIdx.x * N + j] = cs;
             else ys[j] = cs;                                    // single CTA: c directly (y consumed)
+        }
+        if (H > 1) {
+            __syncthreads();
+            for (int64_t j = threadIdx.x; j < N; j += RT) {
+                double cs = 0.0;
+                for (int h = 0; h < H; ++h) cs += cph[(size_t)h * N + j];
+                if (multi) p.cpart[(int64_t)blockIdx.x * N + j] = cs;
+                else ys[j] = cs;
+            }
         }
         __syncthreads();
         RS_TRACE(4);
@@ -235,7 +255,7 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p)
 
 template <typename T, int NMAX>
 size_t smem_of(const ResidentParams &p) {
-    return sizeof(double) * ((size_t)p.N + 2 * (size_t)p.R * (size_t)p.n + 5 * (size_t)p.R) +
+    return sizeof(double) * ((size_t)p.N + 2 * (size_t)p.R * (size_t)p.n + 5 * (size_t)p.R + (p.N < RT ? RT : 0)) +
            sizeof(T) * ((size_t)p.N * NMAX + (size_t)p.R * NMAX + 2 * (size_t)p.R * p.ldS) + 16;
 }
 
