@@ -247,6 +247,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
 
+    # what the JSON line needs from the device-timed solver; then release it (its workspace
+    # returns to torch's cache, so the e2e solver below does not pay a fresh multi-GB cudaMalloc
+    # whose cost depends on what the previous process left for the driver to scrub)
+    s_rows, s_kernel = s.rows, s.kernel
+    ps1 = s.partition_info(check=False) if args.nbar > 1 else None
+    s.close()
+    torch.cuda.synchronize()
+
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -285,12 +293,12 @@ def main():
         return
     value = cfg.N * cfg.N * K / (t_ms / 1e3)
     bpp = 24 if prec == "fp64" else 12
-    per_launch_bytes = bpp * s.rows * cfg.N
+    per_launch_bytes = bpp * s_rows * cfg.N
     avg_pass_s = (pass_ms / max(pass_n, 1)) / 1e3
     peak, peak_kind = peaks()
     achieved = per_launch_bytes / avg_pass_s / 1e9
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}_{s.kernel}.json")
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}_{s_kernel}.json")
     if os.path.exists(tfile):
         try:
             traffic = json.load(open(tfile)).get("bytes_per_launch")
@@ -303,7 +311,7 @@ def main():
         "dtype": "f64" if prec == "fp64" else "f32", "data": "synthetic",
         "config": {"workload": workload(cfg),
                    "N": cfg.N, "n": cfg.n, "gamma": cfg.gamma, "iters_timed": K,
-                   "kernel": s.kernel, "parallelism": f"rows{world}", "step_rule": args.step,
+                   "kernel": s_kernel, "parallelism": f"rows{world}", "step_rule": args.step,
                    **({"nbar": args.nbar, "partition": f"K = N / {args.nbar} blocks; N^2 - N*nbar pairs dualized; "
                        "Step 1 = per-block fp64 projections (block_ipm, warm started)"} if args.nbar > 1 else {}),
                    "l2": f"inputs larger than L2: Theta state {2 * bpp // 3 * cfg.N * cfg.N / 2**30:.2f} GiB "
@@ -311,7 +319,7 @@ def main():
         "hbm_gbs_algorithmic": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": f"fused pair pass ({s.kernel})", "bytes_per_launch": per_launch_bytes,
+                     "kernel": f"fused pair pass ({s_kernel})", "bytes_per_launch": per_launch_bytes,
                      "avg_launch_ms": avg_pass_s * 1e3, "pass_share_of_step": pass_ms / max(t_ms, 1e-9)},
         "gpu_launches": launches,
         **({"adaptive": {"trials_per_iter": trials / K, "passes_timed": pass_n,
@@ -325,7 +333,6 @@ def main():
     if args.nbar > 1:
         # the dominant kernel is the per-block projection: fp64 CUDA-core arithmetic, counted
         # with the work model of DESIGN.md §9 (FMAs per factorization / solve / product)
-        ps1 = s.partition_info(check=False)
         nb_, n_ = args.nbar, cfg.n
         f_fact = nb_ * (n_ * n_ * nb_ + n_ * nb_ + n_ ** 3 / 6) + nb_ ** 3 * n_ / 2 + nb_ ** 3 / 6 + nb_ * nb_
         f_solve = 2 * nb_ * n_ * n_ + 3 * nb_ * nb_ * n_ + nb_ * nb_

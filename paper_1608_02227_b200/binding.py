@@ -401,6 +401,7 @@ class Solver:
         if getattr(self, "h", None):
             self.lib.cr_destroy(self.h)
             self.h = None
+        self.workspace = None          # back to torch's caching allocator
 
     def __del__(self):
         try:
