@@ -22,10 +22,13 @@ cap = int(sys.argv[4]) if len(sys.argv) > 4 else 200000
 X, ybar = crdata.paper_problem(N, n, f0)
 prec = "fp64" if n <= 24 else "fp32"
 out = {"N": N, "n": n, "f0": f0, "gamma": 1e-4, "prec": prec}
-for rule in ("constant", "adaptive", "backtrack"):
+rules = os.environ.get("RULES", "constant,adaptive,backtrack").split(",")
+for rule in rules:
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    s = crp.Solver(X, ybar, 1e-4, prec=prec, adaptive=rule != "constant")
+    # "partition": the paper's own configuration, K = N / 100 blocks, constant step
+    nbar = 100 if rule == "partition" else 1
+    s = crp.Solver(X, ybar, 1e-4, prec=prec, adaptive=rule in ("adaptive", "backtrack"), nbar=nbar)
     if rule == "adaptive":
         s.set_step_rule("adaptive", 2.0)
     elif rule == "backtrack":
@@ -37,5 +40,7 @@ for rule in ("constant", "adaptive", "backtrack"):
     out[rule] = {"seconds": dt, "iters": rep["iters"], "converged": rep["converged"],
                  "infeas_norm": last["infeas_norm"], "gap_norm": abs(last["gap"]) / (N * N - N),
                  "r_gamma": last["r_gamma"], "s_over_L": s.step_info()["s"] / s.L}
+    if nbar > 1:
+        out[rule]["partition_stats"] = s.partition_info(check=False)
     s.close()
 print(json.dumps(out))
