@@ -13,6 +13,7 @@
 //                sum Theta R (gap), sum (R_-)^2 and max (-R)_+ (P:1106).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <algorithm>
 #include "../cr_internal.h"
 
 namespace cr {
@@ -21,44 +22,91 @@ namespace {
 // One warp per row (grid-stride), lanes over the n features: coalesced fp64 reads of the
 // sums, coalesced writes of xi; a_i by a fixed-order warp reduction.  Per-block partials of
 // |u|^2, u.ybar, |xi|^2 and a nonfinite flag go to statpart (fixed order: deterministic).
-template <typename T>
-__global__ void __launch_bounds__(256, 4) prologue_kernel(const SmallParams p) {
+// Latency: the row's static inputs (x_i, ybar_i) and the sums of Theta^{k-2} (written three
+// launches back) are loaded before the programmatic-dependency wait, and each warp keeps the
+// next row's loads in flight while it computes the current one.
+// kPQ feature chunks of 32 per lane: n <= 32 kPQ (instantiated for 1, 2, 3: cr_max_dim 80)
+template <int kPQ>
+struct ProRow {
+    double r1, r2, c1, c2, yb;
+    double P1[kPQ], P2[kPQ], x[kPQ];
+};
+
+template <typename T, int kPQ>
+__global__ void __launch_bounds__(256, kPQ == 1 ? 3 : 2) prologue_kernel(const SmallParams p) {
     __shared__ double red[4][8];
-    pdl_wait();
-    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double beta = p.use_beta ? (p.ts->t_prev - 1.0) / p.ts->t_cur : 0.0;
-    const double scale = p.s_dev ? 1.0 / *p.s_dev : p.scale;
+    const int n = p.n;
+    const int64_t stride = (int64_t)gridDim.x * 8;
+    int64_t i = (int64_t)blockIdx.x * 8 + warp;
     double u2 = 0.0, uy = 0.0, xi2 = 0.0, bad = 0.0;
     T *XiT = static_cast<T *>(p.XiT);
-    for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < p.Ns; i += (int64_t)gridDim.x * 8) {
+    auto load_static = [&](int64_t r, ProRow<kPQ> &d) {          // inputs final before this launch
+        const int64_t gr = p.row0 + r;
+        d.yb = p.ybar[gr];
+        if (!p.from_eta) { d.r2 = p.r2[r]; d.c2 = p.c2[r]; }
+#pragma unroll
+        for (int q = 0; q < kPQ; ++q) {
+            const int dd = lane + 32 * q;
+            d.x[q] = dd < n ? p.X64[gr * n + dd] : 0.0;
+            d.P2[q] = (!p.from_eta && dd < n) ? p.P2[r * n + dd] : 0.0;
+        }
+    };
+    auto load_fresh = [&](int64_t r, ProRow<kPQ> &d) {           // written by the preceding reduce
+        if (p.from_eta) {
+            d.r1 = p.y64[p.row0 + r];
+#pragma unroll
+            for (int q = 0; q < kPQ; ++q) {
+                const int dd = lane + 32 * q;
+                d.P1[q] = dd < n ? p.Xi64[r * n + dd] : 0.0;
+            }
+            return;
+        }
+        d.r1 = p.r1[r];
+        d.c1 = p.c1[r];
+#pragma unroll
+        for (int q = 0; q < kPQ; ++q) {
+            const int dd = lane + 32 * q;
+            d.P1[q] = dd < n ? p.P1[r * n + dd] : 0.0;
+        }
+    };
+    ProRow<kPQ> cur, nxt;
+    if (i < p.Ns) load_static(i, cur);
+    pdl_wait();
+    pdl_trigger();
+    const double beta = p.use_beta ? (p.ts->t_prev - 1.0) / p.ts->t_cur : 0.0;
+    const double scale = p.s_dev ? 1.0 / *p.s_dev : p.scale;
+    if (i < p.Ns) load_fresh(i, cur);
+    for (; i < p.Ns; i += stride) {
+        const int64_t in = i + stride;
+        if (in < p.Ns) { load_static(in, nxt); load_fresh(in, nxt); }     // next row in flight
         const int64_t gi = p.row0 + i;
         double rt = 0.0, y, u;
         if (p.from_eta) {                               // projected Step-1 point (partition K < N)
-            y = p.y64[gi];
-            u = y - p.ybar[gi];
+            y = cur.r1;
+            u = y - cur.yb;
         } else {
-            const double r1 = p.r1[i], r2 = p.r2[i], c1 = p.c1[i], c2 = p.c2[i];
-            rt = r1 + beta * (r1 - r2);
-            const double ct = c1 + beta * (c1 - c2);
+            rt = cur.r1 + beta * (cur.r1 - cur.r2);
+            const double ct = cur.c1 + beta * (cur.c1 - cur.c2);
             u = ct - rt;                                // (A1^T theta~)_i
-            y = p.ybar[gi] + u;
+            y = cur.yb + u;
         }
-        const double *x = p.X64 + gi * p.n;
         double a = 0.0, q2 = 0.0;
-        for (int d = lane; d < p.n; d += 32) {
+#pragma unroll
+        for (int q = 0; q < kPQ; ++q) {
+            const int d = lane + 32 * q;
+            if (d >= n) continue;
             double xi;
             if (p.from_eta) {
-                xi = p.Xi64[i * p.n + d];
+                xi = cur.P1[q];
             } else {
-                const double P1 = p.P1[i * p.n + d], P2 = p.P2[i * p.n + d];
-                const double Pt = P1 + beta * (P1 - P2);
-                xi = (rt * x[d] - Pt) / p.gamma;        // (A2^T theta~)_i / gamma
-                p.Xi64[i * p.n + d] = xi;
+                const double Pt = cur.P1[q] + beta * (cur.P1[q] - cur.P2[q]);
+                xi = (rt * cur.x[q] - Pt) / p.gamma;    // (A2^T theta~)_i / gamma
+                p.Xi64[i * n + d] = xi;
             }
             if (XiT) XiT[(int64_t)d * p.Rp + i] = T(xi * scale);
             if (p.XiR) p.XiR[i * p.NK + d] = (float)(xi * scale);
-            a += xi * x[d];
+            a += xi * cur.x[q];
             q2 += xi * xi;
         }
 #pragma unroll
@@ -72,10 +120,11 @@ __global__ void __launch_bounds__(256, 4) prologue_kernel(const SmallParams p) {
             static_cast<T *>(p.yv)[gi] = T(y * scale);
             static_cast<T *>(p.bv)[i] = T((a - y) * scale);
             u2 += u * u;
-            uy += u * p.ybar[gi];
+            uy += u * cur.yb;
             xi2 += q2;
             bad += (isfinite(y) && isfinite(a)) ? 0.0 : 1.0;
         }
+        cur = nxt;
     }
     if (lane == 0) { red[0][warp] = u2; red[1][warp] = uy; red[2][warp] = xi2; red[3][warp] = bad; }
     __syncthreads();
@@ -417,12 +466,42 @@ inline unsigned nblk(int64_t work, int bs) { return (unsigned)((work + bs - 1) /
 
 }  // namespace
 
+// One resident wave: the grid-stride loop keeps two rows in flight per warp, so more CTAs than
+// fit at once only add waves of latency.
+template <typename T, int Q>
+int prologue_wave() {
+    static int wave = 0;                       // per instantiation; the device does not change
+    if (wave == 0) {
+        int dev = 0, nsm = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prologue_kernel<T, Q>, 256, 0);
+        wave = std::max(1, nsm * std::max(occ, 1));
+    }
+    return wave;
+}
+
 cudaError_t launch_prologue(const SmallParams &p, int fp64, cudaStream_t s, int *nb_out) {
     int64_t nb = (p.Ns + 7) / 8;
     if (nb < 1) nb = 1;
+    const int q = (p.n + 31) / 32;
+    const int wave = q <= 1 ? (fp64 ? prologue_wave<double, 1>() : prologue_wave<float, 1>())
+                   : q == 2 ? (fp64 ? prologue_wave<double, 2>() : prologue_wave<float, 2>())
+                            : (fp64 ? prologue_wave<double, 3>() : prologue_wave<float, 3>());
+    if (nb > wave) nb = wave;
     if (nb > kStatBlocks) nb = kStatBlocks;
-    cudaError_t e = fp64 ? pdl_launch(prologue_kernel<double>, dim3((unsigned)nb), dim3(256), 0, s, p)
-                         : pdl_launch(prologue_kernel<float>, dim3((unsigned)nb), dim3(256), 0, s, p);
+    cudaError_t e;
+    if (q <= 1)
+        e = fp64 ? pdl_launch(prologue_kernel<double, 1>, dim3((unsigned)nb), dim3(256), 0, s, p)
+                 : pdl_launch(prologue_kernel<float, 1>, dim3((unsigned)nb), dim3(256), 0, s, p);
+    else if (q == 2)
+        e = fp64 ? pdl_launch(prologue_kernel<double, 2>, dim3((unsigned)nb), dim3(256), 0, s, p)
+                 : pdl_launch(prologue_kernel<float, 2>, dim3((unsigned)nb), dim3(256), 0, s, p);
+    else if (q == 3)
+        e = fp64 ? pdl_launch(prologue_kernel<double, 3>, dim3((unsigned)nb), dim3(256), 0, s, p)
+                 : pdl_launch(prologue_kernel<float, 3>, dim3((unsigned)nb), dim3(256), 0, s, p);
+    else
+        return cudaErrorInvalidValue;
     if (e != cudaSuccess) return e;
     if (nb_out) *nb_out = (int)nb;
     return cudaGetLastError();
