@@ -191,45 +191,59 @@ __device__ void factor(const Blk &B) {
     }
     // Per point l (independent across l): Mll = gamma I + sum_l' D_ll' delta delta^T, its
     // Cholesky factor Lll (kept in Lf), and Z_l = Lll^{-1} M0l^T (n x nb), M0l^T's column l' =
-    // D_ll' delta_ll' (l' != l), column l = -(sum of the others).  G warps take G points at a
-    // time (warp-private smem Drow / Mll / Z); then S -= sum_l Z_l^T Z_l for the G points.
+    // D_ll' delta_ll' (l' != l), column l = -(sum of the others).  G points at a time (smem Drow /
+    // Mll / Z per point), every phase spread over the whole block; then S -= sum_l Z_l^T Z_l.
     const int G = B.G, warp = threadIdx.x >> 5;
+    const int nlow = n * (n + 1) / 2;
     for (int l0 = 0; l0 < nb; l0 += G) {
-        const int l = l0 + warp;
-        if (warp < G && l < nb) {
-            double *Dr = B.Drow + warp * nb, *Ml = B.Mll + warp * n * n, *Zl = B.Z + (size_t)warp * n * nb;
-            for (int lp = lane; lp < nb; lp += 32) Dr[lp] = lp == l ? 0.0 : B.D[B.pid(l, lp)];
-            __syncwarp();
-            for (int e = lane; e < n * n; e += 32) {
-                const int d = e / n, f = e % n;
-                if (f > d) continue;
-                double v = d == f ? B.gamma : 0.0;
-                for (int lp = 0; lp < nb; ++lp) v += Dr[lp] * B.delta(l, lp, d) * B.delta(l, lp, f);
-                Ml[d * n + f] = v;
-            }
-            for (int e = lane; e < n * nb; e += 32) {
-                const int d = e / nb, lp = e % nb;
-                Zl[d * nb + lp] = Dr[lp] * B.delta(l, lp, d);           // Dr[l] = 0
-            }
-            __syncwarp();
-            for (int d = 0; d < n; ++d) {
-                double v = 0.0;
-                for (int lp = lane; lp < nb; lp += 32) v -= Zl[d * nb + lp];
-                v = warp_sum(v);
-                if (lane == 0) Zl[d * nb + l] = v;
-            }
-            chol_warp(Ml, n, n);                                         // (ends with __syncwarp)
-            for (int lp = lane; lp < nb; lp += 32)
-                for (int d = 0; d < n; ++d) {
-                    double s = Zl[d * nb + lp];
-                    for (int c = 0; c < d; ++c) s -= Ml[d * n + c] * Zl[c * nb + lp];
-                    Zl[d * nb + lp] = s * Ml[d * n + d];
-                }
-            for (int e = lane; e < n * n; e += 32) B.Lf[(size_t)l * n * n + e] = Ml[e];
+        const int gw = min(G, nb - l0);
+        for (int e = threadIdx.x; e < gw * nb; e += IT) {
+            const int g = e / nb, lp = e % nb, l = l0 + g;
+            B.Drow[g * nb + lp] = lp == l ? 0.0 : B.D[B.pid(l, lp)];
         }
         __syncthreads();
+        // Mll (lower triangle) and the unscaled M0l^T panels
+        for (int e = threadIdx.x; e < gw * nlow; e += IT) {
+            const int g = e / nlow, t = e % nlow, l = l0 + g;
+            int d = (int)((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
+            while (d * (d + 1) / 2 > t) --d;
+            while ((d + 1) * (d + 2) / 2 <= t) ++d;
+            const int f = t - d * (d + 1) / 2;
+            const double *Dr = B.Drow + g * nb;
+            double v = d == f ? B.gamma : 0.0;
+            for (int lp = 0; lp < nb; ++lp) v += Dr[lp] * B.delta(l, lp, d) * B.delta(l, lp, f);
+            B.Mll[g * n * n + d * n + f] = v;
+        }
+        for (int e = threadIdx.x; e < gw * n * nb; e += IT) {
+            const int g = e / (n * nb), r = e % (n * nb), d = r / nb, lp = r % nb;
+            B.Z[(size_t)g * n * nb + r] = B.Drow[g * nb + lp] * B.delta(l0 + g, lp, d);   // Drow[l] = 0
+        }
+        __syncthreads();
+        for (int gd = warp; gd < gw * n; gd += NW) {                 // column l of M0l^T
+            const int g = gd / n, d = gd % n;
+            double *zr = B.Z + (size_t)g * n * nb + d * nb;
+            double v = 0.0;
+            for (int lp = lane; lp < nb; lp += 32) v -= zr[lp];
+            v = warp_sum(v);
+            if (lane == 0) zr[l0 + g] = v;
+        }
+        for (int g = warp; g < gw; g += NW) chol_warp(B.Mll + g * n * n, n, n);
+        __syncthreads();
+        // Z_l <- Lll^{-1} M0l^T (forward substitution, threads over the (point, column) pairs)
+        for (int e = threadIdx.x; e < gw * nb; e += IT) {
+            const int g = e / nb, lp = e % nb;
+            const double *Ml = B.Mll + g * n * n;
+            double *zc = B.Z + (size_t)g * n * nb + lp;
+            for (int d = 0; d < n; ++d) {
+                double s = zc[d * nb];
+                for (int c = 0; c < d; ++c) s -= Ml[d * n + c] * zc[c * nb];
+                zc[d * nb] = s * Ml[d * n + d];
+            }
+        }
+        for (int e = threadIdx.x; e < gw * n * n; e += IT) B.Lf[(size_t)l0 * n * n + e] = B.Mll[e];
+        __syncthreads();
         // S -= sum_w Z_w^T Z_w on the lower triangle: 4 x 4 register tiles on a 16 x TY thread grid
-        const int gw = min(G, nb - l0), K = gw * n;
+        const int K = gw * n;
         const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
         for (int i0 = 4 * ty; i0 < nb; i0 += 4 * TY)
             for (int j0 = 4 * tx; j0 <= i0; j0 += 64) {
