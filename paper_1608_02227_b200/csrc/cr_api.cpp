@@ -1229,7 +1229,7 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
                 const int key = 3 * ctx->bA + ctx->bB;
                 if (!ctx->graph[key] && (st = build_graph(ctx, key)) != CR_OK) return st;
                 CK(cudaGraphLaunch(ctx->graph[key], ctx->stream));
-                ctx->launches += 3;
+                ctx->launches += ctx->lay.nbar > 1 ? 5 : 3;      // (+ block projections, prologue refresh)
             } else if ((st = enqueue_step(ctx, true, bo, 1.0 / ctx->L, true, false)) != CR_OK) {
                 return st;
             }
