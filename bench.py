@@ -237,7 +237,7 @@ def main():
     t_ms = e0.elapsed_time(e1)
     launches = s.launch_count - l0
     trials = s.step_info()["trials_total"] - tr0
-    Kp = min(K, 20 if adaptive else 50)
+    Kp = min(K, 20 if adaptive else 200)
     ps0 = s.partition_info(check=False) if args.nbar > 1 else None
     s.set_pass_timing(True)
     s.solve(Kp)
