@@ -29,7 +29,7 @@ struct CtC {
     CtC(int64_t N_, int n_, const double *X_) : N(N_), n(n_), X(X_), s(n_, 0.0), S2((size_t)n_ * n_, 0.0) {
         for (int64_t l = 0; l < N; ++l)
             for (int d = 0; d < n; ++d) s[d] += X[l * n + d];
-        #pragma omp parallel for
+        #pragma omp parallel for if ((int64_t)N * n * n > (1 << 20))   // small problems: no thread wake-ups
         for (int d = 0; d < n; ++d)
             for (int e = 0; e < n; ++e) {
                 double acc = 0.0;
@@ -50,7 +50,7 @@ struct CtC {
             for (int d = 0; d < n; ++d) { Sxi[d] += xi[k * n + d]; w[d] += y[k] * X[k * n + d]; }
         }
         const double Nd = (double)N;
-        #pragma omp parallel for schedule(static)
+        #pragma omp parallel for schedule(static) if ((int64_t)N * n * n > (1 << 20))
         for (int64_t k = 0; k < N; ++k) {
             const double *xk = X + k * n, *xik = xi + k * n;
             double xs = 0.0, sx = 0.0;
