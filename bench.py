@@ -127,9 +127,26 @@ def cpu_baseline(cfg, budget_s):
     oracle.papg(Xs, ys, cfg.gamma, L, iters, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"])
     t_used = time.perf_counter() - t0
     return {"value": Np * Np * iters / t_used, "unit": "pairs/s", "cores": oracle.max_threads(),
-            "kind": "oracle",
+            "kind": "oracle", "host": host_info(),
             "sample": f"{iters} full fp64 P-APG iterations on the first N'={Np} of {cfg.N} observations "
                       f"of {cfg.name} (n={cfg.n}), {t_used:.1f} s"}
+
+
+def host_info():
+    """CPU model and RAM of the host the oracle ran on (SURVEY.md §8(d) oracle timing)."""
+    model, ram = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu": model, "ram_gib": ram, "nproc": os.cpu_count()}
 
 
 def workload(cfg):
@@ -168,6 +185,7 @@ def run_reference(args, cfg, rank, world):
             "config": {"workload": workload(cfg), "N": cfg.N, "n": cfg.n, "gamma": cfg.gamma, "iters_timed": K,
                        "kernel": "oracle (fp64, CPU)", "sampled_N": Np},
             "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": oracle.max_threads(), "kind": "oracle",
+                             "host": host_info(),
                              "sample": f"{K} full fp64 P-APG iterations on the first N'={Np} of {cfg.N} "
                                        f"observations of {cfg.name}"},
             "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
