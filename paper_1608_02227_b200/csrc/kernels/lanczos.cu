@@ -176,9 +176,9 @@ __global__ void __launch_bounds__(LB) lz_dot_kernel(const double *a, const doubl
 
 // w -= alpha v + beta vprev, per-block partial of |w|^2
 __global__ void __launch_bounds__(LB) lz_update_kernel(double *w, const double *v, const double *vprev, int64_t m,
-                                                       const double *ab, double *part) {
+                                                       const double *alpha, const double *beta_prev, double *part) {
     __shared__ double sh[LB];
-    const double al = ab[0], bp = ab[1];
+    const double al = *alpha, bp = *beta_prev;
     double acc = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * LB + threadIdx.x; i < m; i += (int64_t)gridDim.x * LB) {
         const double t = w[i] - (al * v[i] + bp * vprev[i]);
@@ -190,16 +190,17 @@ __global__ void __launch_bounds__(LB) lz_update_kernel(double *w, const double *
 }
 
 // fixed-order sum of nb partials (one block of LB threads: strided partial sums, then a tree)
-__global__ void __launch_bounds__(LB) lz_final_kernel(const double *part, int nb, double *dst) {
+__global__ void __launch_bounds__(LB) lz_final_kernel(const double *part, int nb, double *dst, int take_sqrt) {
     __shared__ double sh[LB];
     double r = 0.0;
     for (int b = threadIdx.x; b < nb; b += LB) r += part[b];
     r = block_sum(r, sh);
-    if (threadIdx.x == 0) *dst = r;
+    if (threadIdx.x == 0) *dst = take_sqrt ? sqrt(r) : r;
 }
 
 // vprev <- v, v <- w / b
-__global__ void lz_shift_kernel(double *v, double *vprev, const double *w, int64_t m, double inv_b) {
+__global__ void lz_shift_kernel(double *v, double *vprev, const double *w, int64_t m, const double *b) {
+    const double inv_b = 1.0 / *b;
     for (int64_t i = (int64_t)blockIdx.x * LB + threadIdx.x; i < m; i += (int64_t)gridDim.x * LB) {
         vprev[i] = v[i];
         v[i] = w[i] * inv_b;
@@ -219,8 +220,9 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
     const int nbk = (int)((N + LROWS - 1) / LROWS);           // lz_sums blocks
     const int nba = (int)((N + LW - 1) / LW);                 // lz_apply blocks (warp per row)
     const int nbv = (int)std::min<int64_t>((m + LB - 1) / LB, 1024);
+    const int itmax = (int)std::min<int64_t>(max_iter, m);
     double *S2 = nullptr, *s = nullptr, *v = nullptr, *vp = nullptr, *w = nullptr, *a = nullptr, *part = nullptr,
-           *tot = nullptr, *sc = nullptr;
+           *tot = nullptr, *ab = nullptr;
     auto ok = [&](cudaError_t e) { if (e != cudaSuccess && *err == cudaSuccess) *err = e; return e == cudaSuccess; };
     *err = cudaSuccess;
     const size_t npart = std::max<size_t>((size_t)nbk * (2 + 2 * n), (size_t)nbv);
@@ -228,53 +230,58 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
     ok(cudaMallocAsync(&v, sizeof(double) * 3 * m, st));
     ok(cudaMallocAsync(&a, sizeof(double) * N, st));
     ok(cudaMallocAsync(&part, sizeof(double) * npart, st));
-    ok(cudaMallocAsync(&tot, sizeof(double) * (2 + 2 * n + 4), st));
+    ok(cudaMallocAsync(&tot, sizeof(double) * (2 + 2 * n), st));
+    ok(cudaMallocAsync(&ab, sizeof(double) * (2 * (size_t)itmax + 1), st));   // alpha[it], beta[it], 0
     double result = -1.0;
     if (*err == cudaSuccess) {
         s = S2 + (size_t)n * n;
         vp = v + m;
         w = vp + m;
-        sc = tot + 2 + 2 * n;                    // [alpha, beta_prev, |w|^2, spare]
+        double *al_d = ab, *be_d = ab + itmax, *zero_d = ab + 2 * itmax;
         ok(cudaMemcpyAsync(v, start.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
         ok(cudaMemsetAsync(vp, 0, sizeof(double) * m, st));
+        ok(cudaMemsetAsync(zero_d, 0, sizeof(double), st));
         lz_gram_kernel<<<n * (n + 1), LB, 0, st>>>(X, N, n, S2, s);
         ok(cudaGetLastError());
-        std::vector<double> al, be;
-        double prev = 0.0, bprev = 0.0;
-        int stable = 0;
-        for (int it = 0; it < std::min<int64_t>(max_iter, m) && *err == cudaSuccess; ++it) {
-            lz_sums_kernel<<<nbk, LB, 0, st>>>(X, N, n, v, a, part);
-            lz_sums_final_kernel<<<1, 256, 0, st>>>(part, nbk, n, tot);
-            lz_apply_kernel<<<nba, LB, 0, st>>>(X, N, n, S2, s, v, a, tot, w);
-            lz_dot_kernel<<<nbv, LB, 0, st>>>(w, v, m, part);
-            lz_final_kernel<<<1, LB, 0, st>>>(part, nbv, sc);
-            double hv[2];
-            ok(cudaMemcpyAsync(hv, sc, sizeof(double), cudaMemcpyDeviceToHost, st));
-            ok(cudaStreamSynchronize(st));
-            const double al_ = hv[0];
-            hv[0] = al_;
-            hv[1] = bprev;
-            ok(cudaMemcpyAsync(sc, hv, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
-            lz_update_kernel<<<nbv, LB, 0, st>>>(w, v, vp, m, sc, part);
-            lz_final_kernel<<<1, LB, 0, st>>>(part, nbv, sc + 2);
-            double b2 = 0.0;
-            ok(cudaMemcpyAsync(&b2, sc + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
-            ok(cudaStreamSynchronize(st));
-            const double b = std::sqrt(b2);
-            al.push_back(al_);
-            const double theta = lanczos_max_ritz(al.data(), be.data(), (int)al.size());
-            result = theta;
-            if (it > 2 && std::fabs(theta - prev) <= tol * std::fabs(theta)) {
-                if (++stable >= 3) break;
-            } else {
-                stable = 0;
+        // The recurrence runs on the device in chunks of kChunk iterations (alpha, beta kept in
+        // device memory); after each chunk the host replays the stopping logic of the host
+        // Lanczos iteration by iteration on the copied (alpha, beta), so L is the same as
+        // stepping with a host round trip per iteration (iterations past the stop are unused).
+        constexpr int kChunk = 8;
+        std::vector<double> al, be, hab(2 * (size_t)itmax);
+        double prev = 0.0;
+        int stable = 0, it = 0, done = 0;
+        bool stop = false;
+        while (!stop && it < itmax && *err == cudaSuccess) {
+            const int end = std::min(itmax, it + kChunk);
+            for (; it < end; ++it) {
+                lz_sums_kernel<<<nbk, LB, 0, st>>>(X, N, n, v, a, part);
+                lz_sums_final_kernel<<<1, 256, 0, st>>>(part, nbk, n, tot);
+                lz_apply_kernel<<<nba, LB, 0, st>>>(X, N, n, S2, s, v, a, tot, w);
+                lz_dot_kernel<<<nbv, LB, 0, st>>>(w, v, m, part);
+                lz_final_kernel<<<1, LB, 0, st>>>(part, nbv, al_d + it, 0);
+                lz_update_kernel<<<nbv, LB, 0, st>>>(w, v, vp, m, al_d + it, it > 0 ? be_d + it - 1 : zero_d, part);
+                lz_final_kernel<<<1, LB, 0, st>>>(part, nbv, be_d + it, 1);
+                lz_shift_kernel<<<nbv, LB, 0, st>>>(v, vp, w, m, be_d + it);
             }
-            prev = theta;
-            if (b <= 1e-14 * std::fabs(theta)) break;
-            be.push_back(b);
-            lz_shift_kernel<<<nbv, LB, 0, st>>>(v, vp, w, m, 1.0 / b);
             ok(cudaGetLastError());
-            bprev = b;
+            ok(cudaMemcpyAsync(hab.data(), al_d, sizeof(double) * it, cudaMemcpyDeviceToHost, st));
+            ok(cudaMemcpyAsync(hab.data() + itmax, be_d, sizeof(double) * it, cudaMemcpyDeviceToHost, st));
+            ok(cudaStreamSynchronize(st));
+            for (; done < it && !stop; ++done) {
+                al.push_back(hab[done]);
+                const double theta = lanczos_max_ritz(al.data(), be.data(), (int)al.size());
+                result = theta;
+                if (done > 2 && std::fabs(theta - prev) <= tol * std::fabs(theta)) {
+                    if (++stable >= 3) { stop = true; break; }
+                } else {
+                    stable = 0;
+                }
+                prev = theta;
+                const double b = hab[itmax + done];
+                if (b <= 1e-14 * std::fabs(theta)) { stop = true; break; }
+                be.push_back(b);
+            }
         }
     }
     cudaFreeAsync(S2, st);
@@ -282,6 +289,7 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
     cudaFreeAsync(a, st);
     cudaFreeAsync(part, st);
     cudaFreeAsync(tot, st);
+    cudaFreeAsync(ab, st);
     ok(cudaStreamSynchronize(st));
     return *err == cudaSuccess ? result : -1.0;
 }
