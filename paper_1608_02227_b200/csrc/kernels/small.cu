@@ -331,14 +331,18 @@ __global__ void adapt_finalize_kernel(const double *part, int nb, DevScalars *ts
 
 // Residual pass: 64 rows x 128 columns per tile, thread = 8 rows x 4 columns (register-blocked
 // fp64 outer products over d: 12 shared loads -- 8 of them warp broadcasts -- per 32 FMAs).
+// Feature chunks of kRDC: shared memory stays ~50 KB whatever n is, so several CTAs share an
+// SM (latency hiding for the fp64 FMA chains); the d loop is unrolled for load / FMA overlap.
+constexpr int kRDC = 32;
+
 template <typename T>
-__global__ void __launch_bounds__(256) residual_kernel(const ResidualParams p) {
+__global__ void __launch_bounds__(256, 2) residual_kernel(const ResidualParams p) {
     constexpr int RBM = 64, RBN = 128;
     extern __shared__ double rsm[];
-    double *xs = rsm;                        // [n][RBN]   x_j[d]
-    double *xis = xs + p.n * RBN;            // [n][RBM]   xi_i[d]
-    double *ab = xis + RBM * p.n;            // [RBM]      a_i - y_i
-    double *yj = ab + RBM;                   // [RBN]      y_j
+    double *xs = rsm;                        // [kRDC][RBN]   x_j[d] of the current feature chunk
+    double *xis = xs + kRDC * RBN;           // [kRDC][RBM]   xi_i[d]
+    double *ab = xis + RBM * kRDC;           // [RBM]         a_i - y_i
+    double *yj = ab + RBM;                   // [RBN]         y_j
     __shared__ double red[3][256];
     const int nrb = (int)((p.Ns + RBM - 1) / RBM), ncb = (int)((p.N + RBN - 1) / RBN);
     const int64_t ntiles = (int64_t)nrb * ncb;
@@ -348,16 +352,6 @@ __global__ void __launch_bounds__(256) residual_kernel(const ResidualParams p) {
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t rb = t / ncb, cb = t % ncb;
         __syncthreads();
-        for (int f = threadIdx.x; f < p.n * RBN; f += blockDim.x) {      // contiguous rows of X
-            const int cc = f / p.n, d = f % p.n;
-            const int64_t j = cb * RBN + cc;
-            xs[d * RBN + cc] = j < p.N ? p.X64[j * p.n + d] : 0.0;
-        }
-        for (int e = threadIdx.x; e < RBM * p.n; e += blockDim.x) {
-            const int ii = e / p.n, d = e % p.n;
-            const int64_t i = rb * RBM + ii;
-            xis[d * RBM + ii] = i < p.Ns ? p.Xi64[i * p.n + d] : 0.0;
-        }
         for (int e = threadIdx.x; e < RBM; e += blockDim.x) {
             const int64_t i = rb * RBM + e;
             ab[e] = i < p.Ns ? p.a64[i] - p.y64[p.row0 + i] : 0.0;
@@ -366,27 +360,42 @@ __global__ void __launch_bounds__(256) residual_kernel(const ResidualParams p) {
             const int64_t j = cb * RBN + e;
             yj[e] = j < p.N ? p.y64[j] : 0.0;
         }
-        __syncthreads();
         double acc[8][4];
 #pragma unroll
         for (int r = 0; r < 8; ++r)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-        for (int d = 0; d < p.n; ++d) {
-            const double2 x01 = *reinterpret_cast<const double2 *>(xs + d * RBN + tx * 4);
-            const double2 x23 = *reinterpret_cast<const double2 *>(xs + d * RBN + tx * 4 + 2);
-            const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
-            double xi[8];
-#pragma unroll
-            for (int r = 0; r < 8; r += 2) {
-                const double2 q = *reinterpret_cast<const double2 *>(xis + d * RBM + ty * 8 + r);
-                xi[r] = q.x;
-                xi[r + 1] = q.y;
+        for (int d0 = 0; d0 < p.n; d0 += kRDC) {
+            const int dc = min(kRDC, p.n - d0);
+            if (d0 > 0) __syncthreads();
+            for (int f = threadIdx.x; f < dc * RBN; f += blockDim.x) {      // rows of X, chunk columns
+                const int cc = f / dc, d = f % dc;
+                const int64_t j = cb * RBN + cc;
+                xs[d * RBN + cc] = j < p.N ? p.X64[j * p.n + d0 + d] : 0.0;
             }
+            for (int e = threadIdx.x; e < RBM * dc; e += blockDim.x) {
+                const int ii = e / dc, d = e % dc;
+                const int64_t i = rb * RBM + ii;
+                xis[d * RBM + ii] = i < p.Ns ? p.Xi64[i * p.n + d0 + d] : 0.0;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int d = 0; d < dc; ++d) {
+                const double2 x01 = *reinterpret_cast<const double2 *>(xs + d * RBN + tx * 4);
+                const double2 x23 = *reinterpret_cast<const double2 *>(xs + d * RBN + tx * 4 + 2);
+                const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
+                double xi[8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
+                for (int r = 0; r < 8; r += 2) {
+                    const double2 q = *reinterpret_cast<const double2 *>(xis + d * RBM + ty * 8 + r);
+                    xi[r] = q.x;
+                    xi[r + 1] = q.y;
+                }
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = fma(xi[r], xv[c], acc[r][c]);
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[r][c] = fma(xi[r], xv[c], acc[r][c]);
+            }
         }
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -535,7 +544,7 @@ cudaError_t launch_residual(const ResidualParams &p, int fp64, cudaStream_t s, i
     const int64_t nrb = (p.Ns + 63) / 64, ncb = (p.N + 127) / 128;
     int64_t tiles = nrb * ncb;
     int nb = (int)(tiles < kStatBlocks ? (tiles > 0 ? tiles : 1) : kStatBlocks);
-    const size_t smem = sizeof(double) * ((size_t)p.n * 128 + 64 * (size_t)p.n + 64 + 128);
+    const size_t smem = sizeof(double) * ((size_t)kRDC * 128 + 64 * (size_t)kRDC + 64 + 128);
     cudaError_t e;
     if (fp64) {
         e = cudaFuncSetAttribute(residual_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
