@@ -88,6 +88,16 @@ typedef enum {
 } cr_step_rule;
 
 /* cr_config.flags */
+#define CR_FLAG_P2P 2       /* multi-GPU (NCCL mode): reduce-scatter the column sums over NVLink
+                               peer memory instead of ncclReduceScatter -- the reduce kernel
+                               stores each column sum straight into its owner rank's receive slab
+                               (CUDA IPC, mapped once in cr_init over the NCCL communicator) and
+                               releases a per-source arrival counter (system scope); the owner's
+                               gather kernel acquires the W counters and sums the slabs in rank
+                               order.  Requires world <= 8 and shard rows S % 128 == 0 (32 for
+                               fp64); CR_ERR_UNSUPPORTED otherwise.  Verified on one GPU through
+                               cr_selftest_p2p (all ranks in one cooperative launch) and a 1-rank
+                               communicator (CR_FORCE_NCCL); not yet run across GPUs.          */
 #define CR_FLAG_ADAPTIVE 1  /* reserve a third Theta buffer + sums slot so cr_set_step_rule can
                                select CR_STEP_ADAPTIVE (a rejected trial must not overwrite
                                Theta^{k-2}); +1 Theta matrix of workspace                       */
@@ -235,6 +245,14 @@ cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, doubl
 /* s_k of the last accepted step (L for the constant rule), trials l_k + 1 of the last
  * adaptive iteration and the total number of adaptive trials; any pointer may be NULL. */
 cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *trials_total);
+
+/* Self-test of the CR_FLAG_P2P protocol on the current device: `world` virtual ranks, each with
+ * nrb rows of fp32 column partials (HOST colpart[world][nrb][N], the fused pass's layout), run
+ * the production column-sum blocks (push into the owners' slabs + release) and owner gathers
+ * (acquire + rank-order sum) in ONE cooperative launch; c (HOST, N) receives every owner's
+ * slice = the column sums over all ranks and rows.  1 <= world <= 8, ceil(N/world) % 128 == 0
+ * (else CR_ERR_UNSUPPORTED); CR_ERR_CUDA on a CUDA error. */
+cr_status cr_selftest_p2p(int32_t world, int64_t N, int32_t nrb, const float *colpart, double *c);
 
 /* Partition diagnostics (cr_config.nbar) of the block projections of this rank's LAST Step 1. */
 typedef struct {

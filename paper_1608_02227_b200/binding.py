@@ -21,6 +21,7 @@ KERNEL = {"auto": 0, "simt": 1, "tc": 2}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
 STEP_RULE = {"constant": 0, "adaptive": 1, "backtrack": 2}
 CR_FLAG_ADAPTIVE = 1
+CR_FLAG_P2P = 2
 
 # Symbols include/cr.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -29,7 +30,7 @@ EXPORTS = (
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
     "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info", "cr_set_gamma",
     "cr_continuation", "cr_local_group_create", "cr_local_group_destroy", "cr_predict", "cr_workspace_size_ex",
-    "cr_partition_info",
+    "cr_partition_info", "cr_selftest_p2p",
 )
 
 
@@ -97,6 +98,7 @@ def load(path: str = LIB_PATH):
         "cr_workspace_size": (C.c_size_t, [i64, i32, C.c_int, C.c_int, i32, i32, i32]),
         "cr_workspace_size_ex": (C.c_size_t, [i64, i32, C.c_int, C.c_int, i32, i32, i32, i64]),
         "cr_partition_info": (C.c_int, [vp, C.POINTER(CrPartitionStats)]),
+        "cr_selftest_p2p": (C.c_int, [i32, i64, i32, vp, vp]),
         "cr_max_dim": (i32, []),
         "cr_nccl_get_unique_id": (C.c_int, [vp]),
         "cr_init": (C.c_int, [C.POINTER(CrConfig), C.POINTER(vp)]),
@@ -143,6 +145,18 @@ def _f64(a, shape=None):
 def workspace_size(N, n, prec="fp32", kernel="auto", rank=0, world=1, flags=0, nbar=1) -> int:
     return int(load().cr_workspace_size_ex(int(N), int(n), PREC[prec], KERNEL[kernel], int(rank), int(world),
                                            int(flags), int(nbar)))
+
+
+def selftest_p2p(colpart) -> np.ndarray:
+    """cr_selftest_p2p: colpart [world][nrb][N] fp32 -> the column sums over all ranks and rows,
+    computed by the CR_FLAG_P2P push / gather kernels for `world` virtual ranks on this GPU."""
+    cp = np.ascontiguousarray(colpart, dtype=np.float32)
+    W, nrb, N = cp.shape
+    out = np.empty(N)
+    st = load().cr_selftest_p2p(int(W), int(N), int(nrb), cp.ctypes.data, out.ctypes.data)
+    if st != 0:
+        raise CrError(f"cr_selftest_p2p: {load().cr_status_string(st).decode()}")
+    return out
 
 
 def lipschitz_host(X, gamma) -> float:
@@ -219,7 +233,7 @@ class Solver:
     """
 
     def __init__(self, X, ybar, gamma, L=0.0, prec="fp32", kernel="auto", device=None, stream=None,
-                 group=None, adaptive=False, rank=None, nbar=1):
+                 group=None, adaptive=False, rank=None, nbar=1, p2p=False):
         import torch
         if not torch.cuda.is_available():
             raise CrError("libcr needs a CUDA device (no CPU fallback)")
@@ -245,7 +259,7 @@ class Solver:
                 uid = (C.c_char * 128).from_buffer_copy(broadcast_unique_id(group, dev))
         self._uid = uid
         self.row0, self.rows = shard_range(self.N, self.rank, self.world)
-        flags = CR_FLAG_ADAPTIVE if adaptive else 0
+        flags = (CR_FLAG_ADAPTIVE if adaptive else 0) | (CR_FLAG_P2P if p2p else 0)
         self.nbar = int(nbar)
         nbytes = workspace_size(self.N, self.n, prec, kernel, self.rank, self.world, flags, self.nbar)
         if nbytes == 0:

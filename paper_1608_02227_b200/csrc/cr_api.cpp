@@ -76,7 +76,7 @@ bool use_tc(int n, cr_precision prec, cr_kernel kernel) {
 bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank, int world, int flags,
                  int64_t nbar, Layout *L) {
     if (N < 2 || n < 1 || world < 1 || rank < 0 || rank >= world) return false;
-    if (flags & ~CR_FLAG_ADAPTIVE) return false;
+    if (flags & ~(CR_FLAG_ADAPTIVE | CR_FLAG_P2P)) return false;
     if (nbar < 0) return false;
     L->nbar = std::max<int64_t>(nbar, 1);
     if (L->nbar > 1) {
@@ -242,6 +242,13 @@ struct cr_ctx {
     int64_t T_tc = 0;
     unsigned long long *trace = nullptr;   // debug timeline buffer (CR_TC_TRACE=<file>)
     Comm comm;           // NCCL communicator or in-process local group (world > 1)
+    // CR_FLAG_P2P: peer-memory reduce-scatter of the column sums (receive slab + flags + epoch
+    // in p2p_buf, IPC-mapped by the other ranks; p2p_tab = device table of every rank's slab
+    // and flag array)
+    bool p2p = false;
+    double *p2p_buf = nullptr;
+    void **p2p_tab = nullptr;
+    std::vector<void *> p2p_opened;
     bool coll = false;   // collectives active: world > 1, or a 1-rank NCCL comm (CR_FORCE_NCCL test mode)
 
     template <typename P> P *at(size_t off) { return reinterpret_cast<P *>(ws + off); }
@@ -330,6 +337,12 @@ ReduceParams reduce_params(cr_ctx *ctx, int slot, int advance, bool tc = false, 
     q.r = ctx->r[slot];
     q.P = ctx->P[slot];
     q.c_out = ctx->coll ? ctx->at<double>(Ly.cfull) : ctx->c[slot];
+    if (ctx->p2p) {
+        q.p2p_recv = reinterpret_cast<double *const *>(ctx->p2p_tab);
+        q.p2p_flag = reinterpret_cast<unsigned long long *const *>(ctx->p2p_tab + kP2PTab);
+        q.p2p_rank = ctx->rank;
+        q.p2p_S = Ly.S;
+    }
     q.ts = ctx->at<DevScalars>(Ly.ts);
     q.advance_t = advance;
     return q;
@@ -430,6 +443,30 @@ cudaEvent_t next_event(cr_ctx *ctx) {
     return ctx->ev[ctx->ev_used++];
 }
 
+// The column sums of slot s for this rank's rows from every rank's partials: NCCL / local
+// reduce-scatter of cfull, or (CR_FLAG_P2P) the owner-side gather of the peer-memory slabs the
+// reduce kernels of all ranks stored into.
+cr_status reduce_scatter_c(cr_ctx *ctx, int s) {
+    const Layout &Ly = ctx->lay;
+    if (ctx->p2p) {
+        P2PGather g{};
+        g.W = ctx->world;
+        g.S = Ly.S;
+        g.Ns = Ly.Ns;
+        g.slab = ctx->p2p_buf;
+        g.flag = reinterpret_cast<unsigned long long *>(ctx->p2p_buf + (size_t)ctx->world * Ly.S);
+        g.epoch = g.flag + ctx->world;
+        const int cbw = reduce_col_block(Ly.fp64);
+        g.nblk = (Ly.Ns + cbw - 1) / cbw;
+        g.c_out = ctx->c[s];
+        CK(launch_p2p_gather(g, ctx->stream));
+        ctx->launches += 1;
+        return CR_OK;
+    }
+    CM(comm_reduce_scatter_f64(ctx->comm, ctx->at<double>(Ly.cfull), ctx->c[s], (size_t)Ly.S, ctx->stream));
+    return CR_OK;
+}
+
 // Sums (r, c, Theta X) of buffer b into slot s, read-only pass.
 cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
     const Layout &Ly = ctx->lay;
@@ -438,8 +475,10 @@ cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
     ReduceParams q = reduce_params(ctx, s, 0);
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
     ctx->launches += 2;
-    if (ctx->coll)
-        CM(comm_reduce_scatter_f64(ctx->comm, ctx->at<double>(Ly.cfull), ctx->c[s], (size_t)Ly.S, ctx->stream));
+    if (ctx->coll) {
+        cr_status st = reduce_scatter_c(ctx, s);
+        if (st != CR_OK) return st;
+    }
     return CR_OK;
 }
 
@@ -520,8 +559,10 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     }
     ReduceParams q = reduce_params(ctx, bo, advance_t ? 1 : 0, Ly.tc, adapt);
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
-    if (ctx->coll)
-        CM(comm_reduce_scatter_f64(ctx->comm, ctx->at<double>(Ly.cfull), ctx->c[bo], (size_t)Ly.S, ctx->stream));
+    if (ctx->coll) {
+        cr_status st = reduce_scatter_c(ctx, bo);
+        if (st != CR_OK) return st;
+    }
     ctx->launches += 3;
     return CR_OK;
 }
@@ -859,6 +900,8 @@ cr_status cr_lipschitz_host(int64_t N, int32_t n, const double *X, double gamma,
     return CR_OK;
 }
 
+static cr_status p2p_setup(cr_ctx *ctx);   // CR_FLAG_P2P (below)
+
 cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     if (!out) return CR_ERR_INVALID_ARG;
     *out = nullptr;
@@ -1052,7 +1095,63 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
             return bail(CR_ERR_NCCL);
         }
     }
+    if (cfg->flags & CR_FLAG_P2P) {
+        cr_status st = p2p_setup(ctx);
+        if (st != CR_OK) return bail(st);
+    }
     *out = ctx;
+    return CR_OK;
+}
+
+// CR_FLAG_P2P: this rank's receive slab [W][S] + arrival flags [W] + epoch in one cudaMalloc
+// (IPC-exportable), the handles exchanged once over the NCCL communicator and the peers' slabs
+// mapped (cudaIpcOpenMemHandle, NVLink peer access); the device table lists every rank's slab
+// and flags.  NCCL mode only; S must be a multiple of the column-sum block.
+static cr_status p2p_setup(cr_ctx *ctx) {
+    const Layout &Ly = ctx->lay;
+    const int W = ctx->world;
+    if (!ctx->coll || ctx->comm.local || !ctx->comm.nccl)
+        return fail(ctx, CR_ERR_UNSUPPORTED, "CR_FLAG_P2P needs the NCCL path (world > 1, or CR_FORCE_NCCL)");
+    if (W > kP2PTab || Ly.S % reduce_col_block(Ly.fp64))
+        return fail(ctx, CR_ERR_UNSUPPORTED, "CR_FLAG_P2P: world <= %d and shard rows %% %d == 0 required", kP2PTab,
+                    reduce_col_block(Ly.fp64));
+    const size_t per = (size_t)W * Ly.S + W + 1;
+    CK(cudaMalloc(&ctx->p2p_buf, per * sizeof(double)));
+    CK(cudaMemset(ctx->p2p_buf, 0, per * sizeof(double)));
+    CK(cudaMalloc(&ctx->p2p_tab, 2 * kP2PTab * sizeof(void *)));
+    std::vector<void *> base(W, nullptr);
+    base[ctx->rank] = ctx->p2p_buf;
+    if (W > 1) {
+        cudaIpcMemHandle_t h{};
+        CK(cudaIpcGetMemHandle(&h, ctx->p2p_buf));
+        char *dev = nullptr;
+        CK(cudaMalloc(&dev, (size_t)W * sizeof h));
+        CK(cudaMemcpy(dev + (size_t)ctx->rank * sizeof h, &h, sizeof h, cudaMemcpyHostToDevice));
+        ncclResult_t r = ncclAllGather(dev + (size_t)ctx->rank * sizeof h, dev, sizeof h, ncclChar, ctx->comm.nccl,
+                                       ctx->stream);
+        if (r != ncclSuccess) {
+            cudaFree(dev);
+            return fail(ctx, CR_ERR_NCCL, "CR_FLAG_P2P handle exchange: %s", ncclGetErrorString(r));
+        }
+        std::vector<cudaIpcMemHandle_t> all(W);
+        CK(cudaMemcpyAsync(all.data(), dev, (size_t)W * sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(dev);
+        for (int q = 0; q < W; ++q) {
+            if (q == ctx->rank) continue;
+            void *ptr = nullptr;
+            CK(cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess));
+            ctx->p2p_opened.push_back(ptr);
+            base[q] = ptr;
+        }
+    }
+    void *tab[2 * kP2PTab] = {};
+    for (int q = 0; q < W; ++q) {
+        tab[q] = base[q];
+        tab[kP2PTab + q] = static_cast<double *>(base[q]) + (size_t)W * Ly.S;
+    }
+    CK(cudaMemcpy(ctx->p2p_tab, tab, sizeof tab, cudaMemcpyHostToDevice));
+    ctx->p2p = true;
     return CR_OK;
 }
 
@@ -1383,6 +1482,29 @@ cr_status cr_partition_info(cr_ctx *ctx, cr_partition_stats *out) {
     return CR_OK;
 }
 
+cr_status cr_selftest_p2p(int32_t world, int64_t N, int32_t nrb, const float *colpart, double *c) {
+    if (world < 1 || world > kP2PTab || N < 1 || nrb < 1 || !colpart || !c) return CR_ERR_INVALID_ARG;
+    const int64_t S = (N + world - 1) / world;
+    if (S % 128) return CR_ERR_UNSUPPORTED;
+    const int64_t ldT = (N + 3) / 4 * 4;
+    float *dcp = nullptr;
+    double *dc = nullptr;
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&dcp, sizeof(float) * (size_t)world * nrb * ldT);
+    if (e == cudaSuccess) e = cudaMalloc(&dc, sizeof(double) * (size_t)N);
+    if (e == cudaSuccess) e = cudaMemset(dcp, 0, sizeof(float) * (size_t)world * nrb * ldT);
+    if (e == cudaSuccess)
+        e = cudaMemcpy2D(dcp, ldT * sizeof(float), colpart, N * sizeof(float), N * sizeof(float),
+                         (size_t)world * nrb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = p2p_selftest(world, N, nrb, dcp, ldT, dc, st);
+    if (e == cudaSuccess) e = cudaMemcpy(c, dc, sizeof(double) * N, cudaMemcpyDeviceToHost);
+    if (dcp) cudaFree(dcp);
+    if (dc) cudaFree(dc);
+    if (st) cudaStreamDestroy(st);
+    return e == cudaSuccess ? CR_OK : CR_ERR_CUDA;
+}
+
 cr_status cr_set_gamma(cr_ctx *ctx, double gamma, double L) {
     cr_status st = check_ctx(ctx);
     if (st != CR_OK) return st;
@@ -1537,6 +1659,9 @@ void cr_destroy(cr_ctx *ctx) {
     for (auto e : ctx->ev) cudaEventDestroy(e);
     for (auto e : ctx->bp_ev) cudaEventDestroy(e);
     if (ctx->comm.nccl) ncclCommDestroy(ctx->comm.nccl);
+    for (void *ptr : ctx->p2p_opened) cudaIpcCloseMemHandle(ptr);
+    if (ctx->p2p_buf) cudaFree(ctx->p2p_buf);
+    if (ctx->p2p_tab) cudaFree(ctx->p2p_tab);
     delete ctx;
 }
 

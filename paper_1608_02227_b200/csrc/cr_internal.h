@@ -47,6 +47,7 @@ constexpr int64_t kIpmMaxNbar = 128;         // partition block size limit (bloc
 constexpr size_t kIpmMaxSmem = 220 * 1024;
 constexpr int kIpmMaxIter = 100;             // interior-point iterations per projection
 constexpr double kIpmTol = 1e-9;             // relative residuals / max complementarity (then the polish)
+constexpr int kP2PTab = 8;                   // CR_FLAG_P2P: largest world (pointer table size)
 constexpr int64_t kLanczosHostMax = 1 << 14;   // N (n + 1) at or below: L by the host Lanczos in cr_init
 constexpr int64_t kResidentMaxN = 4096;   // SMEM-resident small-N solver: eligible sizes
 constexpr int kResidentMaxCTAs = 256;
@@ -150,9 +151,34 @@ struct ReduceParams {
     double *c_out;         // column sums for all N columns (shard partial)
     DevScalars *ts;
     int advance_t;         // 1: t_prev <- t_cur, t_cur <- (1 + sqrt(1 + 4 t^2)) / 2
+    // Peer-memory reduce-scatter (CR_FLAG_P2P): non-null -> column j's partial goes straight to
+    // its owner q = j / S, at p2p_recv[q][p2p_rank * S + j - q S] (NVLink peer store), and each
+    // column block then bumps p2p_flag[q][p2p_rank] with a system-scope release (S % block = 0)
+    double *const *p2p_recv;
+    unsigned long long *const *p2p_flag;
+    int p2p_rank;
+    int64_t p2p_S;
 };
 
 cudaError_t launch_reduce(const ReduceParams &p, int prec_fp64, cudaStream_t s);
+int reduce_col_block(int prec_fp64);   // columns per column-sum CTA (128 fp32 partials, 32 fp64)
+
+// Owner side of the peer-memory reduce-scatter: one CTA waits (acquire, system scope) until
+// every source rank's column blocks for this epoch have landed in the local slab, then sums
+// the W contributions in rank order (deterministic) into c_out.
+struct P2PGather {
+    const double *slab;          // [W][S] this rank's receive slab
+    unsigned long long *flag;    // [W]    arrivals per source (monotonic)
+    unsigned long long *epoch;   // [1]    gathers completed (this rank)
+    int W;
+    int64_t S, Ns, nblk;         // nblk: column blocks each source sends per epoch
+    double *c_out;               // [Ns]
+};
+cudaError_t launch_p2p_gather(const P2PGather &g, cudaStream_t s);
+// Self-test: W virtual ranks' column sums + reduce-scatter in ONE cooperative launch on one
+// GPU (push blocks and owner blocks co-resident, so the owners' waits cannot deadlock).
+cudaError_t p2p_selftest(int W, int64_t N, int nRB, const float *colpart_dev /* [W][nRB][ldT] */, int64_t ldT,
+                         double *c_dev /* [N] */, cudaStream_t s);
 
 // Adaptive step: Eq. (adaptive-check) in its quadratic form (R15),
 //   Q = ||A1^T D||^2 + ||A2^T D||^2 / gamma   vs   s ||D||^2,   D = Theta^k - theta~^k,

@@ -140,68 +140,94 @@ __global__ void __launch_bounds__(256, kPQ == 1 ? 3 : 2) prologue_kernel(const S
 // (fixed chunks, combined in order).  Remaining blocks: one warp per row, lanes over d <= n (+1),
 // summing that row's run slots in a fixed order.  Every pass rewrites every column of the slots
 // it owns, so the partials are read-only here.
+// Column j's sum of this rank's partials: into c_out (NCCL / local reduce-scatter follows), or
+// straight into its owner's receive slab over peer memory (CR_FLAG_P2P).
+__device__ __forceinline__ void col_store(const ReduceParams &p, int64_t j, double v) {
+    if (p.p2p_recv) {
+        const int64_t q = j / p.p2p_S;
+        p.p2p_recv[q][p.p2p_rank * p.p2p_S + (j - q * p.p2p_S)] = v;
+    } else {
+        p.c_out[j] = v;
+    }
+}
+
+// One column block (128 columns of fp32 partials / 32 of fp64): fixed-order sums; with P2P the
+// block then releases its arrival to the owner (system scope: the owner is another GPU).
+template <typename Tc>
+__device__ void colsum_block(const ReduceParams &p, int64_t cb) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rb0 = (int)((int64_t)p.nRB * warp / 8), rb1 = (int)((int64_t)p.nRB * (warp + 1) / 8);
+    if constexpr (sizeof(Tc) == 4) {
+        // fp32 partials: 128 columns per block, a float4 of 4 columns per lane, 4 row blocks
+        // of loads in flight per lane
+        __shared__ double cs4[8][128];
+        const int64_t j = (int64_t)cb * 128 + 4 * lane;      // ldT % 4 == 0: in bounds
+        const float *cp = static_cast<const float *>(p.colpart);
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        if (j < p.N) {
+            int rb = rb0;
+            for (; rb + 4 <= rb1; rb += 4) {
+                float4 v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4 *>(cp + (int64_t)(rb + k) * p.ldT + j);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    s[0] += (double)v[k].x; s[1] += (double)v[k].y; s[2] += (double)v[k].z; s[3] += (double)v[k].w;
+                }
+            }
+            for (; rb < rb1; ++rb) {
+                const float4 v = *reinterpret_cast<const float4 *>(cp + (int64_t)rb * p.ldT + j);
+                s[0] += (double)v.x; s[1] += (double)v.y; s[2] += (double)v.z; s[3] += (double)v.w;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cs4[warp][4 * lane + q] = s[q];
+        __syncthreads();
+        if (threadIdx.x < 128) {
+            const int64_t jj = (int64_t)cb * 128 + threadIdx.x;
+            double t = 0.0;
+            for (int w = 0; w < 8; ++w) t += cs4[w][threadIdx.x];
+            if (jj < p.N) col_store(p, jj, t);
+        }
+    } else {
+        __shared__ double cs[8][32];
+        const int64_t j = (int64_t)cb * 32 + lane;
+        const Tc *cp = static_cast<const Tc *>(p.colpart);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (j < p.N) {
+            int rb = rb0;
+            for (; rb + 4 <= rb1; rb += 4) {
+                s0 += (double)cp[(int64_t)rb * p.ldT + j];
+                s1 += (double)cp[(int64_t)(rb + 1) * p.ldT + j];
+                s2 += (double)cp[(int64_t)(rb + 2) * p.ldT + j];
+                s3 += (double)cp[(int64_t)(rb + 3) * p.ldT + j];
+            }
+            for (; rb < rb1; ++rb) s0 += (double)cp[(int64_t)rb * p.ldT + j];
+        }
+        cs[warp][lane] = (s0 + s1) + (s2 + s3);
+        __syncthreads();
+        if (warp == 0 && j < p.N) {
+            double t = 0.0;
+            for (int w = 0; w < 8; ++w) t += cs[w][lane];
+            col_store(p, j, t);
+        }
+    }
+    if (p.p2p_recv) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int64_t q = cb * (sizeof(Tc) == 4 ? 128 : 32) / p.p2p_S;
+            __threadfence_system();
+            atomicAdd_system(p.p2p_flag[q] + p.p2p_rank, 1ULL);
+        }
+    }
+}
+
 template <typename Tc>
 __global__ void __launch_bounds__(256, 4) reduce_kernel(const ReduceParams p, int ncolb) {
     pdl_wait();
     pdl_trigger();
     if ((int)blockIdx.x < ncolb) {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        const int rb0 = (int)((int64_t)p.nRB * warp / 8), rb1 = (int)((int64_t)p.nRB * (warp + 1) / 8);
-        if constexpr (sizeof(Tc) == 4) {
-            // fp32 partials: 128 columns per block, a float4 of 4 columns per lane, 4 row blocks
-            // of loads in flight per lane
-            __shared__ double cs4[8][128];
-            const int64_t j = (int64_t)blockIdx.x * 128 + 4 * lane;      // ldT % 4 == 0: in bounds
-            const float *cp = static_cast<const float *>(p.colpart);
-            double s[4] = {0.0, 0.0, 0.0, 0.0};
-            if (j < p.N) {
-                int rb = rb0;
-                for (; rb + 4 <= rb1; rb += 4) {
-                    float4 v[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4 *>(cp + (int64_t)(rb + k) * p.ldT + j);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        s[0] += (double)v[k].x; s[1] += (double)v[k].y; s[2] += (double)v[k].z; s[3] += (double)v[k].w;
-                    }
-                }
-                for (; rb < rb1; ++rb) {
-                    const float4 v = *reinterpret_cast<const float4 *>(cp + (int64_t)rb * p.ldT + j);
-                    s[0] += (double)v.x; s[1] += (double)v.y; s[2] += (double)v.z; s[3] += (double)v.w;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) cs4[warp][4 * lane + q] = s[q];
-            __syncthreads();
-            if (threadIdx.x < 128) {
-                const int64_t jj = (int64_t)blockIdx.x * 128 + threadIdx.x;
-                double t = 0.0;
-                for (int w = 0; w < 8; ++w) t += cs4[w][threadIdx.x];
-                if (jj < p.N) p.c_out[jj] = t;
-            }
-        } else {
-            __shared__ double cs[8][32];
-            const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-            const Tc *cp = static_cast<const Tc *>(p.colpart);
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            if (j < p.N) {
-                int rb = rb0;
-                for (; rb + 4 <= rb1; rb += 4) {
-                    s0 += (double)cp[(int64_t)rb * p.ldT + j];
-                    s1 += (double)cp[(int64_t)(rb + 1) * p.ldT + j];
-                    s2 += (double)cp[(int64_t)(rb + 2) * p.ldT + j];
-                    s3 += (double)cp[(int64_t)(rb + 3) * p.ldT + j];
-                }
-                for (; rb < rb1; ++rb) s0 += (double)cp[(int64_t)rb * p.ldT + j];
-            }
-            cs[warp][lane] = (s0 + s1) + (s2 + s3);
-            __syncthreads();
-            if (warp == 0 && j < p.N) {
-                double t = 0.0;
-                for (int w = 0; w < 8; ++w) t += cs[w][lane];
-                p.c_out[j] = t;
-            }
-        }
+        colsum_block<Tc>(p, blockIdx.x);
     } else {
         // one warp per row, lanes over d <= n (32-bit index math: Ns < 2^31)
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -473,6 +499,73 @@ __global__ void unconvert_rows_kernel(const T *src, int64_t rows, int64_t N, int
 
 inline unsigned nblk(int64_t work, int bs) { return (unsigned)((work + bs - 1) / bs); }
 
+// Owner side of the peer-memory reduce-scatter (one CTA): acquire every source's arrivals for
+// this epoch, then sum the W contributions in rank order.
+__device__ void p2p_gather_block(const double *slab, unsigned long long *flag, unsigned long long *epoch, int W,
+                                 int64_t S, int64_t Ns, int64_t nblk, double *c_out) {
+    __shared__ unsigned long long target;
+    if (threadIdx.x == 0) {
+        const unsigned long long e = *epoch + 1;
+        target = e * (unsigned long long)nblk;
+        for (int r = 0; r < W; ++r) {
+            unsigned long long v;
+            while (true) {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag + r) : "memory");
+                if (v >= target) break;
+                __nanosleep(64);
+            }
+        }
+        *epoch = e;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < Ns; i += blockDim.x) {
+        double t = 0.0;
+        for (int r = 0; r < W; ++r) t += slab[(int64_t)r * S + i];
+        c_out[i] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) p2p_gather_kernel(const P2PGather g) {
+    pdl_wait();
+    p2p_gather_block(g.slab, g.flag, g.epoch, g.W, g.S, g.Ns, g.nblk, g.c_out);
+}
+
+// Self-test kernel: blocks [0, W ncolb) are rank (b / ncolb)'s column-sum blocks pushing into
+// the owners' slabs; the last W blocks are the owners gathering.  A cooperative launch, so all
+// blocks are resident and the owners' waits always see their sources run.
+constexpr int kP2PMaxWorld = kP2PTab;
+struct P2PEmu {
+    int W, nRB;
+    int64_t N, S, ncolb, ldT;
+    const float *colpart[kP2PMaxWorld];
+    double *c_out[kP2PMaxWorld];
+    unsigned long long *epoch[kP2PMaxWorld];
+    double *const *recv;
+    unsigned long long *const *flag;
+};
+
+__global__ void __launch_bounds__(256) p2p_emulate_kernel(const P2PEmu em) {
+    const int64_t b = blockIdx.x;
+    if (b < em.W * em.ncolb) {
+        const int r = (int)(b / em.ncolb);
+        ReduceParams p{};
+        p.N = em.N;
+        p.ldT = em.ldT;
+        p.nRB = em.nRB;
+        p.colpart = em.colpart[r];
+        p.p2p_recv = em.recv;
+        p.p2p_flag = em.flag;
+        p.p2p_rank = r;
+        p.p2p_S = em.S;
+        colsum_block<float>(p, b % em.ncolb);
+    } else {
+        const int q = (int)(b - em.W * em.ncolb);
+        const int64_t Ns = min(em.S, em.N - q * em.S);
+        const int64_t nblk = (Ns + 127) / 128;
+        p2p_gather_block(em.recv[q], em.flag[q], em.epoch[q], em.W, em.S, Ns, nblk, em.c_out[q]);
+    }
+}
+
 }  // namespace
 
 // One resident wave: the grid-stride loop keeps two rows in flight per warp, so more CTAs than
@@ -514,6 +607,56 @@ cudaError_t launch_prologue(const SmallParams &p, int fp64, cudaStream_t s, int 
     if (e != cudaSuccess) return e;
     if (nb_out) *nb_out = (int)nb;
     return cudaGetLastError();
+}
+
+int reduce_col_block(int fp64) { return fp64 ? 32 : 128; }
+
+cudaError_t launch_p2p_gather(const P2PGather &g, cudaStream_t s) {
+    p2p_gather_kernel<<<1, 1024, 0, s>>>(g);
+    return cudaGetLastError();
+}
+
+cudaError_t p2p_selftest(int W, int64_t N, int nRB, const float *colpart, int64_t ldT, double *c, cudaStream_t s) {
+    if (W < 1 || W > kP2PMaxWorld || N < 1) return cudaErrorInvalidValue;
+    const int64_t S = (N + W - 1) / W;
+    if (S % 128) return cudaErrorInvalidValue;                 // column blocks may not straddle owners
+    const int64_t ncolb = (N + 127) / 128;
+    // per virtual rank: a receive slab [W][S] + flags [W] + epoch, one allocation
+    const size_t per = (size_t)W * S + W + 1;
+    double *buf = nullptr;
+    cudaError_t e = cudaMallocAsync(&buf, sizeof(double) * per * W + sizeof(void *) * 2 * kP2PMaxWorld, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(buf, 0, sizeof(double) * per * W, s);
+    P2PEmu em{};
+    em.W = W;
+    em.N = N;
+    em.S = S;
+    em.ncolb = ncolb;
+    double *hr[kP2PMaxWorld];
+    unsigned long long *hf[kP2PMaxWorld];
+    for (int q = 0; q < W; ++q) {
+        hr[q] = buf + per * q;
+        hf[q] = reinterpret_cast<unsigned long long *>(hr[q] + (size_t)W * S);
+        em.epoch[q] = hf[q] + W;
+        em.colpart[q] = colpart + (size_t)q * nRB * ldT;
+        em.c_out[q] = c + q * S;
+    }
+    double **tab = reinterpret_cast<double **>(buf + per * W);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tab, hr, sizeof(void *) * W, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(tab + kP2PMaxWorld, hf, sizeof(void *) * W, cudaMemcpyHostToDevice, s);
+    em.recv = tab;
+    em.flag = reinterpret_cast<unsigned long long *const *>(tab + kP2PMaxWorld);
+    em.nRB = nRB;
+    em.ldT = ldT;
+    if (e == cudaSuccess) {
+        void *args[] = {&em};
+        e = cudaLaunchCooperativeKernel((const void *)p2p_emulate_kernel, dim3((unsigned)(W * ncolb + W)), dim3(256),
+                                        args, 0, s);
+    }
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaFreeAsync(buf, s);
+    return e != cudaSuccess ? e : e2;
 }
 
 cudaError_t launch_reduce(const ReduceParams &p, int fp64, cudaStream_t s) {

@@ -44,7 +44,8 @@ def test_workspace_sizes_and_unsupported(lib):
     # CR_FLAG_ADAPTIVE reserves one more Theta matrix (+ sums slot); unknown flags are rejected
     extra = crp.workspace_size(16384, 40, "fp32", flags=1) - n4
     assert 16384 * 16384 * 4 <= extra < 16384 * 16384 * 4 * 1.1
-    assert crp.workspace_size(16384, 40, "fp32", flags=2) == 0
+    assert crp.workspace_size(16384, 40, "fp32", flags=2) == n4          # CR_FLAG_P2P: no workspace change
+    assert crp.workspace_size(16384, 40, "fp32", flags=4) == 0
     assert crp.workspace_size(100, 0) == 0                # n < 1
     assert crp.workspace_size(100, 500) == 0              # n beyond the compiled buckets
     assert crp.workspace_size(100, 4, rank=3, world=2) == 0
