@@ -40,6 +40,8 @@ def parse():
                     help="step rule of Step 2: constant 1/L (Fig. 2, the headline) or adaptive (P:400-407)")
     ap.add_argument("--nbar", type=int, default=1,
                     help="partition block size (K = N / nbar < N, per-block projections in Step 1); 1 = all pairs")
+    ap.add_argument("--p2p", action="store_true",
+                    help="N > 1: reduce-scatter the column sums over NVLink peer memory (CR_FLAG_P2P)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
@@ -220,7 +222,9 @@ def main():
     prec = cfg.prec
 
     adaptive = args.step == "adaptive"
-    s = crp.Solver(X, ybar, cfg.gamma, prec=prec, kernel=args.kernel, group=group, adaptive=adaptive, nbar=args.nbar)
+    p2p = args.p2p and world > 1
+    s = crp.Solver(X, ybar, cfg.gamma, prec=prec, kernel=args.kernel, group=group, adaptive=adaptive, nbar=args.nbar,
+                   p2p=p2p)
     if adaptive:
         s.set_step_rule("adaptive", 2.0)
     stream = s.stream
@@ -284,7 +288,7 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         s2 = crp.Solver(Xp, yp, cfg.gamma, prec=prec, kernel=args.kernel, group=group, adaptive=adaptive,
-                        nbar=args.nbar)
+                        nbar=args.nbar, p2p=p2p)
         if adaptive:
             s2.set_step_rule("adaptive", 2.0)
         torch.cuda.synchronize()
@@ -331,6 +335,7 @@ def main():
         "config": {"workload": workload(cfg),
                    "N": cfg.N, "n": cfg.n, "gamma": cfg.gamma, "iters_timed": K,
                    "kernel": s_kernel, "parallelism": f"rows{world}", "step_rule": args.step,
+                   "column_reduce_scatter": "peer-memory (CR_FLAG_P2P)" if p2p else ("nccl" if world > 1 else "none"),
                    **({"nbar": args.nbar, "partition": f"K = N / {args.nbar} blocks; N^2 - N*nbar pairs dualized; "
                        "Step 1 = per-block fp64 projections (block_ipm, warm started)"} if args.nbar > 1 else {}),
                    "l2": f"inputs larger than L2: Theta state {2 * bpp // 3 * cfg.N * cfg.N / 2**30:.2f} GiB "
