@@ -88,8 +88,11 @@ typedef enum {
 } cr_step_rule;
 
 /* cr_config.flags */
-#define CR_FLAG_P2P 2       /* multi-GPU (NCCL mode): reduce-scatter the column sums over NVLink
-                               peer memory instead of ncclReduceScatter -- the reduce kernel
+#define CR_FLAG_P2P 2       /* multi-GPU (NCCL mode): the per-iteration exchanges over NVLink peer
+                               memory instead of NCCL.  y' all-gather: the prologue stores each
+                               row's y' into every rank's receive array and releases a per-source
+                               row counter; a one-CTA acquire kernel copies it into the pass
+                               operand.  Column-sum reduce-scatter: the reduce kernel
                                stores each column sum straight into its owner rank's receive slab
                                (CUDA IPC, mapped once in cr_init over the NCCL communicator) and
                                releases a per-source arrival counter (system scope); the owner's
@@ -253,6 +256,12 @@ cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *
  * slice = the column sums over all ranks and rows.  1 <= world <= 8, ceil(N/world) % 128 == 0
  * (else CR_ERR_UNSUPPORTED); CR_ERR_CUDA on a CUDA error. */
 cr_status cr_selftest_p2p(int32_t world, int64_t N, int32_t nrb, const float *colpart, double *c);
+
+/* Self-test of the CR_FLAG_P2P y' all-gather on the current device: `world` virtual ranks each
+ * push their rows [r S, min(N, (r+1) S)) of y (HOST, N) to every rank's receive array with
+ * per-CTA release counters (the prologue's code path) and each rank acquires all and copies
+ * them out, in ONE cooperative launch; out (HOST, world x N) = every rank's gathered vector. */
+cr_status cr_selftest_p2p_allgather(int32_t world, int64_t N, const float *y, float *out);
 
 /* Partition diagnostics (cr_config.nbar) of the block projections of this rank's LAST Step 1. */
 typedef struct {

@@ -6,8 +6,9 @@ ctypes layer over it.  See DESIGN.md.
 """
 from . import binding  # noqa: F401
 from .binding import (  # noqa: F401
-    CrError, LocalGroup, Solver, load, lipschitz_host, nccl_unique_id, selftest_p2p, workspace_size, EXPORTS,
+    CrError, LocalGroup, Solver, load, lipschitz_host, nccl_unique_id, selftest_p2p, selftest_p2p_allgather,
+    workspace_size, EXPORTS,
 )
 
 __all__ = ["CrError", "LocalGroup", "Solver", "load", "lipschitz_host", "nccl_unique_id", "selftest_p2p",
-           "workspace_size", "EXPORTS"]
+           "selftest_p2p_allgather", "workspace_size", "EXPORTS"]

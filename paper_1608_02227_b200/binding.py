@@ -30,7 +30,7 @@ EXPORTS = (
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
     "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info", "cr_set_gamma",
     "cr_continuation", "cr_local_group_create", "cr_local_group_destroy", "cr_predict", "cr_workspace_size_ex",
-    "cr_partition_info", "cr_selftest_p2p",
+    "cr_partition_info", "cr_selftest_p2p", "cr_selftest_p2p_allgather",
 )
 
 
@@ -99,6 +99,7 @@ def load(path: str = LIB_PATH):
         "cr_workspace_size_ex": (C.c_size_t, [i64, i32, C.c_int, C.c_int, i32, i32, i32, i64]),
         "cr_partition_info": (C.c_int, [vp, C.POINTER(CrPartitionStats)]),
         "cr_selftest_p2p": (C.c_int, [i32, i64, i32, vp, vp]),
+        "cr_selftest_p2p_allgather": (C.c_int, [i32, i64, vp, vp]),
         "cr_max_dim": (i32, []),
         "cr_nccl_get_unique_id": (C.c_int, [vp]),
         "cr_init": (C.c_int, [C.POINTER(CrConfig), C.POINTER(vp)]),
@@ -156,6 +157,16 @@ def selftest_p2p(colpart) -> np.ndarray:
     st = load().cr_selftest_p2p(int(W), int(N), int(nrb), cp.ctypes.data, out.ctypes.data)
     if st != 0:
         raise CrError(f"cr_selftest_p2p: {load().cr_status_string(st).decode()}")
+    return out
+
+
+def selftest_p2p_allgather(y, world) -> np.ndarray:
+    """cr_selftest_p2p_allgather: y [N] fp32 -> [world][N], every virtual rank's gathered copy."""
+    yy = np.ascontiguousarray(y, dtype=np.float32)
+    out = np.empty((int(world), yy.shape[0]), dtype=np.float32)
+    st = load().cr_selftest_p2p_allgather(int(world), int(yy.shape[0]), yy.ctypes.data, out.ctypes.data)
+    if st != 0:
+        raise CrError(f"cr_selftest_p2p_allgather: {load().cr_status_string(st).decode()}")
     return out
 
 

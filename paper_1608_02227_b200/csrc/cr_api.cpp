@@ -246,8 +246,9 @@ struct cr_ctx {
     // in p2p_buf, IPC-mapped by the other ranks; p2p_tab = device table of every rank's slab
     // and flag array)
     bool p2p = false;
-    double *p2p_buf = nullptr;
-    void **p2p_tab = nullptr;
+    double *p2p_buf = nullptr;       // [W S] c slab | c flags [W] | c epoch | y flags [W] | y epoch | (256-B) y' receive [W S]
+    void **p2p_tab = nullptr;        // [4][kP2PTab]: every rank's c slab, c flags, y' receive, y flags
+    size_t p2p_yf = 0, p2p_yr = 0;   // byte offsets of the y flags and the y' receive array in p2p_buf
     std::vector<void *> p2p_opened;
     bool coll = false;   // collectives active: world > 1, or a 1-rank NCCL comm (CR_FORCE_NCCL test mode)
 
@@ -376,6 +377,12 @@ SmallParams small_params(cr_ctx *ctx, int sa, int sb, int use_beta, double scale
     p.use_beta = use_beta;
     p.XiR = Ly.tc ? ctx->at<float>(Ly.XiR) : nullptr;
     p.NK = Ly.NK;
+    if (ctx->p2p) {
+        p.p2p_yrecv = ctx->p2p_tab + 2 * kP2PTab;
+        p.p2p_yflag = reinterpret_cast<unsigned long long *const *>(ctx->p2p_tab + 3 * kP2PTab);
+        p.p2p_rank = ctx->rank;
+        p.p2p_W = ctx->world;
+    }
     return p;
 }
 
@@ -485,7 +492,7 @@ cr_status enqueue_sums(cr_ctx *ctx, int b, int s) {
 // Partition K < N (Assumption 1): Step 1 = the closed-form point just written by the prologue
 // projected per block onto the intra-block constraints (block_ipm), then the prologue again in
 // from_eta mode to refresh a, the pass operands and (stats) the objective partials.
-cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro, bool allow_timing = false) {
+cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro, bool allow_timing = false, bool push = false) {
     const Layout &Ly = ctx->lay;
     BlockIpmParams bp{};
     bp.nbar = (int)Ly.nbar;
@@ -516,6 +523,7 @@ cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro, bool allow_ti
     CK(launch_block_ipm(bp, ctx->stream));
     if (e1) CK(cudaEventRecord(e1, ctx->stream));
     sp.from_eta = 1;
+    sp.p2p_push = push ? 1 : 0;                 // the step's final y' (partition): sent to the peers
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nb_pro));
     ctx->launches += 2;
     return CR_OK;
@@ -531,12 +539,26 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     const int bA = ctx->bA, bB = ctx->bB;
     SmallParams sp = small_params(ctx, bA, bB, 1, scale, false);
     sp.s_dev = s_dev;
+    sp.p2p_push = (ctx->p2p && Ly.nbar == 1) ? 1 : 0;
     CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
     if (Ly.nbar > 1) {
-        cr_status st = project_blocks(ctx, sp, nullptr, allow_timing);
+        sp.p2p_push = 0;
+        cr_status st = project_blocks(ctx, sp, nullptr, allow_timing, ctx->p2p);
         if (st != CR_OK) return st;
     }
-    if (ctx->coll) {
+    if (ctx->p2p) {
+        // y' all-gather over peer memory: every rank's prologue pushed its rows; acquire + copy
+        P2PYGather g{};
+        g.yrecv = reinterpret_cast<char *>(ctx->p2p_buf) + ctx->p2p_yr;
+        g.flag = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ctx->p2p_buf) + ctx->p2p_yf);
+        g.epoch = g.flag + ctx->world;
+        g.W = ctx->world;
+        g.N = Ly.N;
+        g.S = Ly.S;
+        g.yv = ctx->ws + Ly.yv;
+        CK(launch_p2p_ygather(g, Ly.fp64, ctx->stream));
+        ctx->launches += 1;
+    } else if (ctx->coll) {
         CM(comm_allgather(ctx->comm, ctx->ws + Ly.yv, (size_t)Ly.S, (int)Ly.es, ctx->stream));
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1115,10 +1137,13 @@ static cr_status p2p_setup(cr_ctx *ctx) {
     if (W > kP2PTab || Ly.S % reduce_col_block(Ly.fp64))
         return fail(ctx, CR_ERR_UNSUPPORTED, "CR_FLAG_P2P: world <= %d and shard rows %% %d == 0 required", kP2PTab,
                     reduce_col_block(Ly.fp64));
-    const size_t per = (size_t)W * Ly.S + W + 1;
-    CK(cudaMalloc(&ctx->p2p_buf, per * sizeof(double)));
-    CK(cudaMemset(ctx->p2p_buf, 0, per * sizeof(double)));
-    CK(cudaMalloc(&ctx->p2p_tab, 2 * kP2PTab * sizeof(void *)));
+    const size_t cbytes = ((size_t)W * Ly.S + W + 1) * 8;          // c slab, c flags, c epoch
+    ctx->p2p_yf = cbytes;                                            // y flags [W], y epoch
+    ctx->p2p_yr = (cbytes + ((size_t)W + 1) * 8 + 255) / 256 * 256;  // y' receive [W S]
+    const size_t bytes = ctx->p2p_yr + (size_t)W * Ly.S * Ly.es;
+    CK(cudaMalloc(&ctx->p2p_buf, bytes));
+    CK(cudaMemset(ctx->p2p_buf, 0, bytes));
+    CK(cudaMalloc(&ctx->p2p_tab, 4 * kP2PTab * sizeof(void *)));
     std::vector<void *> base(W, nullptr);
     base[ctx->rank] = ctx->p2p_buf;
     if (W > 1) {
@@ -1145,10 +1170,13 @@ static cr_status p2p_setup(cr_ctx *ctx) {
             base[q] = ptr;
         }
     }
-    void *tab[2 * kP2PTab] = {};
+    void *tab[4 * kP2PTab] = {};
     for (int q = 0; q < W; ++q) {
-        tab[q] = base[q];
-        tab[kP2PTab + q] = static_cast<double *>(base[q]) + (size_t)W * Ly.S;
+        char *b = static_cast<char *>(base[q]);
+        tab[q] = b;                                                  // c slab
+        tab[kP2PTab + q] = b + (size_t)W * Ly.S * 8;                 // c flags
+        tab[2 * kP2PTab + q] = b + ctx->p2p_yr;                      // y' receive
+        tab[3 * kP2PTab + q] = b + ctx->p2p_yf;                      // y flags
     }
     CK(cudaMemcpy(ctx->p2p_tab, tab, sizeof tab, cudaMemcpyHostToDevice));
     ctx->p2p = true;
@@ -1501,6 +1529,22 @@ cr_status cr_selftest_p2p(int32_t world, int64_t N, int32_t nrb, const float *co
     if (e == cudaSuccess) e = cudaMemcpy(c, dc, sizeof(double) * N, cudaMemcpyDeviceToHost);
     if (dcp) cudaFree(dcp);
     if (dc) cudaFree(dc);
+    if (st) cudaStreamDestroy(st);
+    return e == cudaSuccess ? CR_OK : CR_ERR_CUDA;
+}
+
+cr_status cr_selftest_p2p_allgather(int32_t world, int64_t N, const float *y, float *out) {
+    if (world < 1 || world > kP2PTab || N < 1 || !y || !out) return CR_ERR_INVALID_ARG;
+    float *dy = nullptr, *dout = nullptr;
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&dy, sizeof(float) * (size_t)N);
+    if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(float) * (size_t)world * N);
+    if (e == cudaSuccess) e = cudaMemcpy(dy, y, sizeof(float) * (size_t)N, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = p2p_selftest_y(world, N, dy, dout, st);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(float) * (size_t)world * N, cudaMemcpyDeviceToHost);
+    if (dy) cudaFree(dy);
+    if (dout) cudaFree(dout);
     if (st) cudaStreamDestroy(st);
     return e == cudaSuccess ? CR_OK : CR_ERR_CUDA;
 }

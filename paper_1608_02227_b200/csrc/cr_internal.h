@@ -133,6 +133,12 @@ struct SmallParams {
     int NK;
     int from_eta;          // 1: take (y, xi) from y64 / Xi64 (after the block projections) instead of
                            //    the closed form; refreshes a64, the pass operands and the stat partials
+    // CR_FLAG_P2P all-gather of y': with p2p_push, every row's y' also goes to each rank q's
+    // receive array p2p_yrecv[q][global row] (peer stores), and each CTA then adds its row count to
+    // p2p_yflag[q][p2p_rank] (system-scope release)
+    void *const *p2p_yrecv;
+    unsigned long long *const *p2p_yflag;
+    int p2p_rank, p2p_W, p2p_push;
 };
 
 cudaError_t launch_prologue(const SmallParams &p, int prec_fp64, cudaStream_t s, int *nblocks_out);
@@ -175,6 +181,21 @@ struct P2PGather {
     double *c_out;               // [Ns]
 };
 cudaError_t launch_p2p_gather(const P2PGather &g, cudaStream_t s);
+// Receiving side of the y' all-gather: acquire every source's rows for this epoch, then copy the
+// receive array (all N rows) into the pass operand yv.
+struct P2PYGather {
+    const void *yrecv;           // [N] storage precision, written by every rank's prologue
+    unsigned long long *flag;    // [W] rows received per source (monotonic)
+    unsigned long long *epoch;   // [1]
+    int W;
+    int64_t N, S;
+    void *yv;                    // [>= N] storage precision
+};
+cudaError_t launch_p2p_ygather(const P2PYGather &g, int prec_fp64, cudaStream_t s);
+// Self-test of the y' all-gather protocol: W virtual ranks' row pushes and receivers in ONE
+// cooperative launch; out[q][j] = rank q's gathered y'_j.
+cudaError_t p2p_selftest_y(int W, int64_t N, const float *y_dev /* [N] */, float *out_dev /* [W][N] */,
+                           cudaStream_t s);
 // Self-test: W virtual ranks' column sums + reduce-scatter in ONE cooperative launch on one
 // GPU (push blocks and owner blocks co-resident, so the owners' waits cannot deadlock).
 cudaError_t p2p_selftest(int W, int64_t N, int nRB, const float *colpart_dev /* [W][nRB][ldT] */, int64_t ldT,

@@ -19,6 +19,17 @@
 namespace cr {
 namespace {
 
+// CR_FLAG_P2P all-gather of y': one row's value to every rank's receive array (peer stores) ...
+template <typename T>
+__device__ __forceinline__ void p2p_ypush_row(void *const *yrecv, int W, int64_t gi, T v) {
+    for (int q = 0; q < W; ++q) static_cast<T *>(yrecv[q])[gi] = v;
+}
+// ... and, once per CTA after its rows, the row count to every rank's arrival counter
+__device__ __forceinline__ void p2p_ysignal(unsigned long long *const *yflag, int W, int rank, unsigned long long cnt) {
+    __threadfence_system();
+    for (int q = 0; q < W; ++q) atomicAdd_system(yflag[q] + rank, cnt);
+}
+
 // One warp per row (grid-stride), lanes over the n features: coalesced fp64 reads of the
 // sums, coalesced writes of xi; a_i by a fixed-order warp reduction.  Per-block partials of
 // |u|^2, u.ybar, |xi|^2 and a nonfinite flag go to statpart (fixed order: deterministic).
@@ -71,6 +82,7 @@ __global__ void __launch_bounds__(256, kPQ == 1 ? 3 : 2) prologue_kernel(const S
         }
     };
     ProRow<kPQ> cur, nxt;
+    unsigned rows_pushed = 0;                               // (lane 0: rows sent over peer memory)
     if (i < p.Ns) load_static(i, cur);
     pdl_wait();
     pdl_trigger();
@@ -118,6 +130,10 @@ __global__ void __launch_bounds__(256, kPQ == 1 ? 3 : 2) prologue_kernel(const S
             if (!p.from_eta) p.y64[gi] = y;
             p.a64[i] = a;
             static_cast<T *>(p.yv)[gi] = T(y * scale);
+            if (p.p2p_push) {
+                p2p_ypush_row<T>(p.p2p_yrecv, p.p2p_W, gi, T(y * scale));
+                ++rows_pushed;
+            }
             static_cast<T *>(p.bv)[i] = T((a - y) * scale);
             u2 += u * u;
             uy += u * cur.yb;
@@ -126,8 +142,14 @@ __global__ void __launch_bounds__(256, kPQ == 1 ? 3 : 2) prologue_kernel(const S
         }
         cur = nxt;
     }
-    if (lane == 0) { red[0][warp] = u2; red[1][warp] = uy; red[2][warp] = xi2; red[3][warp] = bad; }
+    __shared__ unsigned pushed[8];
+    if (lane == 0) { red[0][warp] = u2; red[1][warp] = uy; red[2][warp] = xi2; red[3][warp] = bad; pushed[warp] = rows_pushed; }
     __syncthreads();
+    if (p.p2p_push && threadIdx.x == 0) {
+        unsigned long long cnt = 0;
+        for (int w = 0; w < 8; ++w) cnt += pushed[w];
+        if (cnt) p2p_ysignal(p.p2p_yflag, p.p2p_W, p.p2p_rank, cnt);
+    }
     if (threadIdx.x < 4 && p.statpart) {
         double t = 0.0;
         for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
@@ -499,6 +521,69 @@ __global__ void unconvert_rows_kernel(const T *src, int64_t rows, int64_t N, int
 
 inline unsigned nblk(int64_t work, int bs) { return (unsigned)((work + bs - 1) / bs); }
 
+// Receiving side of the y' all-gather (one CTA): acquire each source's rows for this epoch
+// (source r sends min(S, N - r S) rows per epoch), then copy all N rows into yv.
+template <typename T>
+__device__ void p2p_ygather_block(const T *yrecv, unsigned long long *flag, unsigned long long *epoch, int W,
+                                  int64_t N, int64_t S, T *yv) {
+    if (threadIdx.x == 0) {
+        const unsigned long long e = *epoch + 1;
+        for (int r = 0; r < W; ++r) {
+            const int64_t rows = max((int64_t)0, min(S, N - (int64_t)r * S));
+            const unsigned long long target = e * (unsigned long long)rows;
+            unsigned long long v;
+            while (true) {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag + r) : "memory");
+                if (v >= target) break;
+                __nanosleep(64);
+            }
+        }
+        *epoch = e;
+    }
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < N; j += blockDim.x) yv[j] = yrecv[j];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) p2p_ygather_kernel(const P2PYGather g) {
+    pdl_wait();
+    p2p_ygather_block<T>(static_cast<const T *>(g.yrecv), g.flag, g.epoch, g.W, g.N, g.S, static_cast<T *>(g.yv));
+}
+
+// y' self-test: blocks [0, W nbp) push rank (b / nbp)'s rows (256 per block), the last W blocks
+// receive.  Cooperative launch: all resident.
+struct P2PYEmu {
+    int W;
+    int64_t N, S, nbp;
+    const float *y;
+    float *out;                              // [W][N]
+    void *const *yrecv;
+    unsigned long long *const *yflag;
+    unsigned long long *epoch;               // [W]
+};
+
+__global__ void __launch_bounds__(256) p2p_yemulate_kernel(const P2PYEmu em) {
+    const int64_t b = blockIdx.x;
+    if (b < em.W * em.nbp) {
+        const int r = (int)(b / em.nbp);
+        const int64_t r0 = (int64_t)r * em.S, r1 = min(em.N, r0 + em.S);
+        const int64_t gi = r0 + (b % em.nbp) * 256 + threadIdx.x;
+        __shared__ unsigned cnt;
+        if (threadIdx.x == 0) cnt = 0;
+        __syncthreads();
+        if (gi < r1) {
+            p2p_ypush_row<float>(em.yrecv, em.W, gi, em.y[gi]);
+            atomicAdd(&cnt, 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && cnt) p2p_ysignal(em.yflag, em.W, r, cnt);
+    } else {
+        const int q = (int)(b - em.W * em.nbp);
+        p2p_ygather_block<float>(static_cast<const float *>(em.yrecv[q]), em.yflag[q], em.epoch + q, em.W, em.N, em.S,
+                                 em.out + (int64_t)q * em.N);
+    }
+}
+
 // Owner side of the peer-memory reduce-scatter (one CTA): acquire every source's arrivals for
 // this epoch, then sum the W contributions in rank order.
 __device__ void p2p_gather_block(const double *slab, unsigned long long *flag, unsigned long long *epoch, int W,
@@ -610,6 +695,48 @@ cudaError_t launch_prologue(const SmallParams &p, int fp64, cudaStream_t s, int 
 }
 
 int reduce_col_block(int fp64) { return fp64 ? 32 : 128; }
+
+cudaError_t launch_p2p_ygather(const P2PYGather &g, int fp64, cudaStream_t s) {
+    if (fp64) p2p_ygather_kernel<double><<<1, 1024, 0, s>>>(g);
+    else p2p_ygather_kernel<float><<<1, 1024, 0, s>>>(g);
+    return cudaGetLastError();
+}
+
+cudaError_t p2p_selftest_y(int W, int64_t N, const float *y, float *out, cudaStream_t s) {
+    if (W < 1 || W > kP2PTab || N < 1) return cudaErrorInvalidValue;
+    const int64_t S = (N + W - 1) / W, nbp = (S + 255) / 256;
+    char *buf = nullptr;
+    const size_t yb = (sizeof(float) * (size_t)N + 255) / 256 * 256, fb = sizeof(unsigned long long) * (size_t)W;
+    const size_t per = (yb + fb + 255) / 256 * 256;     // y' receive, then the (8-B aligned) flags
+    cudaError_t e = cudaMallocAsync(&buf, per * W + sizeof(void *) * 2 * kP2PTab + sizeof(unsigned long long) * W, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(buf, 0, per * W + sizeof(void *) * 2 * kP2PTab + sizeof(unsigned long long) * W, s);
+    void *tab[2 * kP2PTab] = {};
+    for (int q = 0; q < W; ++q) {
+        tab[q] = buf + per * q;
+        tab[kP2PTab + q] = buf + per * q + yb;
+    }
+    void **dtab = reinterpret_cast<void **>(buf + per * W);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dtab, tab, sizeof tab, cudaMemcpyHostToDevice, s);
+    P2PYEmu em{};
+    em.W = W;
+    em.N = N;
+    em.S = S;
+    em.nbp = nbp;
+    em.y = y;
+    em.out = out;
+    em.yrecv = dtab;
+    em.yflag = reinterpret_cast<unsigned long long *const *>(dtab + kP2PTab);
+    em.epoch = reinterpret_cast<unsigned long long *>(dtab + 2 * kP2PTab);
+    if (e == cudaSuccess) {
+        void *args[] = {&em};
+        e = cudaLaunchCooperativeKernel((const void *)p2p_yemulate_kernel, dim3((unsigned)(W * nbp + W)), dim3(256),
+                                        args, 0, s);
+    }
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaFreeAsync(buf, s);
+    return e != cudaSuccess ? e : e2;
+}
 
 cudaError_t launch_p2p_gather(const P2PGather &g, cudaStream_t s) {
     p2p_gather_kernel<<<1, 1024, 0, s>>>(g);

@@ -35,6 +35,14 @@ def test_selftest_protocol_matches_column_sums(crp, W, N, nrb):
     np.testing.assert_allclose(c, want, rtol=1e-13, atol=0)
 
 
+@pytest.mark.parametrize("W,N", [(1, 300), (2, 1000), (3, 1001), (5, 4097), (8, 20000)])
+def test_selftest_allgather_protocol(crp, W, N):
+    y = np.random.default_rng(W + N).random(N, dtype=np.float32)
+    out = crp.selftest_p2p_allgather(y, W)
+    for q in range(W):
+        np.testing.assert_array_equal(out[q], y)
+
+
 def test_selftest_rejects_straddling_blocks(crp):
     with pytest.raises(crp.CrError):
         crp.selftest_p2p(np.zeros((3, 2, 1000), dtype=np.float32))      # ceil(1000/3) % 128 != 0
@@ -58,6 +66,28 @@ def test_p2p_one_rank_nccl_equals_nccl_reduce_scatter(crp, monkeypatch, N, n, pr
         s.close()
     for a, b in zip(out[0], out[1]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "partition"])
+def test_p2p_one_rank_nccl_adaptive_and_partition(crp, monkeypatch, mode):
+    """The adaptive rule's trial prologues and the partition's refreshed prologue push y' too."""
+    monkeypatch.setenv("CR_FORCE_NCCL", "1")
+    N, n = 256, 3
+    X, ybar = crdata.random_problem(N, n, seed=3)
+    gamma = 1e-2
+    L = ref.lipschitz(X, gamma)
+    out = []
+    for p2p in (False, True):
+        if mode == "adaptive":
+            s = crp.Solver(X, ybar, gamma, L=L, prec="fp64", adaptive=True, p2p=p2p)
+            s.set_step_rule("adaptive", 2.0)
+        else:
+            s = crp.Solver(X, ybar, gamma, L=L, prec="fp64", nbar=16, p2p=p2p)
+        s.solve(6)
+        s.step()
+        out.append(s.get_theta()[0])
+        s.close()
+    np.testing.assert_array_equal(out[0], out[1])
 
 
 def test_p2p_flag_needs_nccl(crp):
