@@ -365,6 +365,9 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
     double *eta = w + m, *eta0 = eta + ne, *rhs = eta0 + ne, *ds = rhs + ne, *tv = ds + ne;
     double *Lf = tv + ne;
     double *wact = Lf + (size_t)nb * n * n, *wla = wact + m, *wflag = wla + m;   // warm start (persists)
+    // the last settled polish's factorization: [0] valid, [1] rho, [2] gamma, [3..) the Schur factor
+    // S (its Mll factors are still in Lf unless a factorization ran since)
+    double *fsave = wflag + 1;
     for (int e = threadIdx.x; e < nb * n; e += IT) Xs[e] = p.X64[(p.row0 + row0) * n + e];
     for (int k = threadIdx.x; k < nb; k += IT) {
         eta0[k] = p.y64[p.row0 + row0 + k];
@@ -391,16 +394,29 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
     // dla, multipliers in dsa (set by the caller); eta is overwritten only on success.
     bool polished = false;
     int rounds = 0, mult_iters = 0;
-    auto polish = [&]() {
+    double rho_last = 0.0;
+    // reuse: the warm start's active set is exactly the one the saved factorization was made for
+    // (a settled polish ends on an unchanged active set), so with the same rho and gamma the
+    // first round needs no factorization
+    auto polish = [&](bool reuse) {
+        int a0 = 0;
+        if (reuse) a0 = fsave[1] == 10.0 * kRho ? 1 : (fsave[1] == 100.0 * kRho ? 2 : 0);
         for (int round = 0; round < kPolishRounds && !polished; ++round) {
             rounds = round + 1;
             double lmax = 0.0;
             // penalty rho = kRho, escalated x10 (refactor) while the multiplier iteration stalls
-            for (int attempt = 0; attempt < kRhoAttempts; ++attempt) {
+            for (int attempt = round == 0 ? a0 : 0; attempt < kRhoAttempts; ++attempt) {
                 const double rho = kRho * (attempt == 0 ? 1.0 : attempt == 1 ? 10.0 : 100.0);
+                rho_last = rho;
                 for (int q = threadIdx.x; q < m; q += IT) D[q] = rho * dla[q];
-                __syncthreads();
-                PROF_BEGIN(); factor(B); PROF_END(0);
+                if (reuse && round == 0 && attempt == a0) {
+                    for (int e = threadIdx.x; e < nb * nb; e += IT) S[e] = fsave[3 + e];
+                    __syncthreads();
+                } else {
+                    __syncthreads();
+                    if (threadIdx.x == 0) fsave[0] = 0.0;                // Lf is about to change
+                    PROF_BEGIN(); factor(B); PROF_END(0);
+                }
                 bool conv = false;
                 for (int r = 0; r < kPolishIters; ++r) {
                     PROF_BEGIN(); apply_AT(B, dsa, ry, rxi); PROF_END(3);
@@ -443,9 +459,11 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
     //    P-APG iterations), verified by the polish itself
     const bool warm = p.warm && wflag[0] != 0.0;
     if (warm) {
+        const bool reuse = fsave[0] != 0.0 && fsave[2] == p.gamma &&
+                           (fsave[1] == kRho || fsave[1] == 10.0 * kRho || fsave[1] == 100.0 * kRho);
         for (int q = threadIdx.x; q < m; q += IT) { dla[q] = wact[q]; dsa[q] = wla[q]; }
         __syncthreads();
-        polish();
+        polish(reuse);
     }
     // 2) otherwise the interior point method from s = max(A eta0, 0) + sc, lambda = sc / 100, then
     //    the polish from its active set {lambda > s}
@@ -549,12 +567,22 @@ __global__ void __launch_bounds__(IT, 1) block_ipm_kernel(const BlockIpmParams p
                 dsa[q] = act ? lam[q] : 0.0;
             }
             __syncthreads();
-            polish();
+            polish(false);
         }
     }
     if (polished && p.warm) {
         for (int q = threadIdx.x; q < m; q += IT) { wact[q] = dla[q]; wla[q] = dsa[q]; }
-        if (threadIdx.x == 0) wflag[0] = 1.0;
+        // smem S / Lf hold the factorization of the final (unchanged) active set at rho_last
+        for (int e = threadIdx.x; e < nb * nb; e += IT) fsave[3 + e] = S[e];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            wflag[0] = 1.0;
+            fsave[1] = rho_last;
+            fsave[2] = p.gamma;
+            fsave[0] = 1.0;
+        }
+    } else if (threadIdx.x == 0) {
+        fsave[0] = 0.0;
     }
     for (int k = threadIdx.x; k < nb; k += IT) p.y64[p.row0 + row0 + k] = eta[k];
     for (int e = threadIdx.x; e < nb * n; e += IT) p.Xi64[row0 * n + e] = eta[nb + e];
@@ -592,7 +620,7 @@ size_t block_ipm_smem(int nbar, int n, int G) {
 
 size_t block_ipm_scratch_per_block(int nbar, int n) {
     const size_t m = (size_t)nbar * (nbar - 1);
-    return 7 * m + 5 * (size_t)nbar * (n + 1) + (size_t)nbar * n * n + 2 * m + 1;
+    return 7 * m + 5 * (size_t)nbar * (n + 1) + (size_t)nbar * n * n + 2 * m + 1 + 3 + (size_t)nbar * nbar;
 }
 
 cudaError_t block_ipm_prepare(int smem) {
