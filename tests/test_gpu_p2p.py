@@ -90,6 +90,13 @@ def test_p2p_one_rank_nccl_adaptive_and_partition(crp, monkeypatch, mode):
     np.testing.assert_array_equal(out[0], out[1])
 
 
+def test_p2p_rejects_unaligned_shards(crp, monkeypatch):
+    monkeypatch.setenv("CR_FORCE_NCCL", "1")
+    X, ybar = crdata.random_problem(300, 3, seed=2, fp32=True)      # S = 300: not a multiple of 128
+    with pytest.raises(crp.CrError):
+        crp.Solver(X, ybar, 1e-3, L=1.0, prec="fp32", p2p=True)
+
+
 def test_p2p_flag_needs_nccl(crp):
     X, ybar = crdata.random_problem(256, 3, seed=1)
     with pytest.raises(crp.CrError):
