@@ -293,6 +293,7 @@ def main():
             s2.set_step_rule("adaptive", 2.0)
         torch.cuda.synchronize()
         t_init = time.perf_counter() - t0
+        init_detail = getattr(s2, "init_ms", None)
         s2.solve(K)
         torch.cuda.synchronize()
         t_solve = time.perf_counter() - t0 - t_init
@@ -308,7 +309,8 @@ def main():
                "h2d_bytes_per_step": (X.nbytes + ybar.nbytes) / K,
                "d2h_bytes_per_step": (y.nbytes + xi.nbytes + 64) / K,
                "timed": "Solver(X, ybar) [H2D + Lanczos L + init] + solve(K) + primal() [D2H y, xi]",
-               "split_ms": {"init": 1e3 * t_init, "solve": 1e3 * t_solve, "primal": 1e3 * (te - t_init - t_solve)}}
+               "split_ms": {"init": 1e3 * t_init, "solve": 1e3 * t_solve, "primal": 1e3 * (te - t_init - t_solve),
+                            "init_detail": init_detail}}
 
     if rank != 0:
         if group is not None:

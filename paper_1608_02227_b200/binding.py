@@ -276,7 +276,10 @@ class Solver:
         if nbytes == 0:
             raise CrError(f"unsupported shape/precision: N={self.N} n={self.n} prec={prec} kernel={kernel} "
                           f"nbar={self.nbar}")
+        import time as _time
+        _t0 = _time.perf_counter()
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.init_ms = {"workspace_alloc": 1e3 * (_time.perf_counter() - _t0)}
         self.stream = torch.cuda.current_stream(dev) if stream is None else stream
         cfg = CrConfig(N=self.N, n=self.n, X=self.X.ctypes.data, ybar=self.ybar.ctypes.data, gamma=self.gamma,
                        L=float(L), prec=PREC[prec], kernel=KERNEL[kernel], rank=self.rank, world=self.world,
@@ -285,7 +288,9 @@ class Solver:
                        workspace=self.workspace.data_ptr(), workspace_bytes=nbytes, flags=flags,
                        local_group=local.h if local is not None else None, nbar=self.nbar)
         h = C.c_void_p()
+        _t1 = _time.perf_counter()
         st = self.lib.cr_init(C.byref(cfg), C.byref(h))
+        self.init_ms["cr_init"] = 1e3 * (_time.perf_counter() - _t1)     # (host-synchronous: includes L)
         if st != CR_OK:
             raise CrError(f"cr_init failed: {self.lib.cr_status_string(st).decode()}")
         self.h = h
