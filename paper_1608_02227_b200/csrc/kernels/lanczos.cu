@@ -96,20 +96,15 @@ __global__ void __launch_bounds__(LB) lz_sums_kernel(const double *X, int64_t N,
     }
 }
 
-// fixed-order sum of the block partials -> tot [2 + 2n]
-__global__ void lz_sums_final_kernel(const double *part, int nb, int n, double *tot) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= 2 + 2 * n) return;
-    double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
-    int b = 0;
-    for (; b + 4 <= nb; b += 4) {
-        r0 += part[(size_t)b * (2 + 2 * n) + q];
-        r1 += part[(size_t)(b + 1) * (2 + 2 * n) + q];
-        r2 += part[(size_t)(b + 2) * (2 + 2 * n) + q];
-        r3 += part[(size_t)(b + 3) * (2 + 2 * n) + q];
-    }
-    for (; b < nb; ++b) r0 += part[(size_t)b * (2 + 2 * n) + q];
-    tot[q] = (r0 + r1) + (r2 + r3);
+// fixed-order sum of the block partials -> tot [2 + 2n]: one block per output value, threads
+// over the partials (strided), then a fixed tree
+__global__ void __launch_bounds__(LB) lz_sums_final_kernel(const double *part, int nb, int n, double *tot) {
+    __shared__ double sh[LB];
+    const int q = blockIdx.x;
+    double r = 0.0;
+    for (int b = threadIdx.x; b < nb; b += LB) r += part[(size_t)b * (2 + 2 * n) + q];
+    r = block_sum(r, sh);
+    if (threadIdx.x == 0) tot[q] = r;
 }
 
 // out = C^T C v (lanczos.cpp CtC::apply), warp per row k (lanes over d); S2 is symmetric, so
@@ -256,7 +251,7 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
             const int end = std::min(itmax, it + kChunk);
             for (; it < end; ++it) {
                 lz_sums_kernel<<<nbk, LB, 0, st>>>(X, N, n, v, a, part);
-                lz_sums_final_kernel<<<1, 256, 0, st>>>(part, nbk, n, tot);
+                lz_sums_final_kernel<<<2 + 2 * n, LB, 0, st>>>(part, nbk, n, tot);
                 lz_apply_kernel<<<nba, LB, 0, st>>>(X, N, n, S2, s, v, a, tot, w);
                 lz_dot_kernel<<<nbv, LB, 0, st>>>(w, v, m, part);
                 lz_final_kernel<<<1, LB, 0, st>>>(part, nbv, al_d + it, 0);
