@@ -236,6 +236,7 @@ struct cr_ctx {
     int res_G = 0, res_R = 0, res_ldS = 0;
     // constant-step graphs per (bA, bB) assignment
     cudaGraphExec_t graph[9] = {};
+    cudaGraphExec_t graph_multi[9] = {};   // kMultiIters constant-step iterations per replay
     cudaStream_t cap_stream = nullptr;   // private stream used only to record graphs
     // tensor-core pass
     int G_tc = 0, stages = 0, g1stages = 0, g2stages = 0, window = 64, smem_tc = 0;
@@ -775,8 +776,44 @@ cr_status check_ctx(cr_ctx *ctx) {
 void drop_graphs(cr_ctx *ctx) {
     for (auto &g : ctx->graph)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    for (auto &g : ctx->graph_multi)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     for (auto &g : ctx->graph_ad)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
+// kMultiIters (even: the buffer roles repeat with period 2, so the graph starts and ends in the
+// same assignment) constant-step iterations in one graph: the PDL chain then also spans the
+// iteration boundaries and the host launches one graph per kMultiIters iterations.
+constexpr int kMultiIters = 8;
+
+cr_status build_graph_multi(cr_ctx *ctx, int key) {
+    cudaGraph_t g = nullptr;
+    const int bA = ctx->bA, bB = ctx->bB;
+    const int64_t k = ctx->k, launches = ctx->launches;
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->cap_stream;
+    cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        ctx->stream = user;
+        return fail(ctx, CR_ERR_CUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(e));
+    }
+    cr_status st = CR_OK;
+    for (int i = 0; i < kMultiIters && st == CR_OK; ++i) {
+        const int bo = ctx->bB;
+        st = enqueue_step(ctx, false, bo, 1.0 / ctx->L, true, false);
+        advance_host(ctx, bo);
+    }
+    e = cudaStreamEndCapture(ctx->stream, &g);
+    ctx->stream = user;
+    ctx->bA = bA; ctx->bB = bB; ctx->k = k; ctx->launches = launches;
+    if (st != CR_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&ctx->graph_multi[key], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    return CR_OK;
 }
 
 cr_status build_graph(cr_ctx *ctx, int key) {
@@ -1352,15 +1389,26 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
             if ((st = adaptive_step(ctx)) != CR_OK) return st;
         } else {
             const int bo = ctx->bB;
-            if (use_graph) {
+            const int per_iter = ctx->lay.nbar > 1 ? 5 : 3;     // (+ block projections, prologue refresh)
+            int64_t room = max_iters - it;                      // iterations before the end / next stop test
+            if (stop) room = std::min<int64_t>(room, stop->report_every - it % stop->report_every);
+            if (use_graph && room >= kMultiIters) {
+                const int key = 3 * ctx->bA + ctx->bB;
+                if (!ctx->graph_multi[key] && (st = build_graph_multi(ctx, key)) != CR_OK) return st;
+                CK(cudaGraphLaunch(ctx->graph_multi[key], ctx->stream));
+                ctx->launches += (int64_t)per_iter * kMultiIters;
+                for (int i = 0; i < kMultiIters; ++i) advance_host(ctx, ctx->bB);
+                it += kMultiIters - 1;
+            } else if (use_graph) {
                 const int key = 3 * ctx->bA + ctx->bB;
                 if (!ctx->graph[key] && (st = build_graph(ctx, key)) != CR_OK) return st;
                 CK(cudaGraphLaunch(ctx->graph[key], ctx->stream));
-                ctx->launches += ctx->lay.nbar > 1 ? 5 : 3;      // (+ block projections, prologue refresh)
-            } else if ((st = enqueue_step(ctx, true, bo, 1.0 / ctx->L, true, false)) != CR_OK) {
-                return st;
+                ctx->launches += per_iter;
+                advance_host(ctx, bo);
+            } else {
+                if ((st = enqueue_step(ctx, true, bo, 1.0 / ctx->L, true, false)) != CR_OK) return st;
+                advance_host(ctx, bo);
             }
-            advance_host(ctx, bo);
         }
         ++it;
         if (stop && (it % stop->report_every == 0 || it == max_iters)) {
