@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -1021,10 +1022,24 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
             return bail(CR_ERR_CUDA);                                                              \
         }                                                                                          \
     } while (0)
+    // CR_INIT_PROF=1: host-synchronous phase timings of cr_init on stderr (diagnostics)
+    const bool iprof = std::getenv("CR_INIT_PROF") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto t_prev = tnow();
+    auto mark = [&](const char *what) {
+        if (!iprof) return;
+        cudaStreamSynchronize(ctx->stream);
+        const auto t = tnow();
+        std::fprintf(stderr, "cr_init %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_prev).count());
+        t_prev = t;
+    };
+    mark("enter");
     IK(cudaMemsetAsync(ctx->ws, 0, Ly.total, ctx->stream));
+    mark("memset");
     if (Ly.nbar > 1) IK(block_ipm_prepare(Ly.ipm_smem));
     IK(cudaMemcpyAsync(ctx->ws + Ly.X64, cfg->X, (size_t)N * n * 8, cudaMemcpyHostToDevice, ctx->stream));
     IK(cudaMemcpyAsync(ctx->ws + Ly.ybar, cfg->ybar, (size_t)N * 8, cudaMemcpyHostToDevice, ctx->stream));
+    mark("h2d");
     if (!(cfg->L > 0.0)) {
         // L = sigma_max(C)^2 / gamma by the device Lanczos (the host cr_lipschitz_host computes
         // the same iteration; fixed-order reductions, so every rank gets the same L)
@@ -1042,6 +1057,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         ctx->L = s2 / cfg->gamma;
     }
     ctx->sigma2 = ctx->L * cfg->gamma;
+    mark("lanczos");
     IK(launch_fill_inputs(ctx->at<double>(Ly.X64), N, n, Ly.NB, Ly.NBP, Ly.ldT, Ly.fp64, ctx->ws + Ly.XT,
                           ctx->ws + Ly.Xh, ctx->stream));
     ctx->launches += 1;
@@ -1132,6 +1148,7 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         }
     }
     IK(cudaStreamSynchronize(ctx->stream));   // host vectors go out of scope
+    mark("setup");
 #undef IK
     ctx->comm.rank = ctx->rank;
     ctx->comm.world = ctx->world;
