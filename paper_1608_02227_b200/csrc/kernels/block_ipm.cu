@@ -278,11 +278,13 @@ __device__ void factor(const Blk &B) {
 // areas) so the substitution chains run from shared memory.
 __device__ void solve(const Blk &B, double *by, double *bxi, double *t) {
     const int nb = B.nb, n = B.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool has = warp < B.G;                          // warps with private smem
-    double *Mw = B.Mll + warp * n * n, *vw = B.Z + (size_t)warp * n * nb;
+    // per-warp (Lll, rhs) staging areas carved from the factor's contiguous Mll + Z panels
+    const int Ws = min(NW, (int)(((size_t)B.G * ((size_t)n * n + (size_t)n * nb)) / ((size_t)n * n + n)));
+    const bool has = warp < Ws;
+    double *Mw = B.Mll + (size_t)warp * (n * n + n), *vw = Mw + n * n;
     // t_l = Mll^{-1} b_l
     if (has)
-        for (int l = warp; l < nb; l += B.G) {
+        for (int l = warp; l < nb; l += Ws) {
             for (int e = lane; e < n * n; e += 32) Mw[e] = B.Lf[(size_t)l * n * n + e];
             for (int d = lane; d < n; d += 32) vw[d] = bxi[l * n + d];
             __syncwarp();
@@ -317,7 +319,7 @@ __device__ void solve(const Blk &B, double *by, double *bxi, double *t) {
     __syncthreads();
     // dxi_l = Mll^{-1} (b_l - M0l^T dy);  (M0l^T dy)_d = sum_l' D_ll' delta_d (dy_l' - dy_l)
     if (has)
-        for (int l = warp; l < nb; l += B.G) {
+        for (int l = warp; l < nb; l += Ws) {
             double wv[kMaxPerLane];
             const double byl = by[l];
 #pragma unroll
