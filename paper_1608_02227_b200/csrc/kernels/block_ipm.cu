@@ -173,6 +173,51 @@ __device__ void chol_solve_warp(const double *Lm, int k, double *v) {
     }
 }
 
+// in place: v <- (L L^T)^{-1} v for the k x k factor in smem (row-major, ld k, diagonal stored
+// inverted), v in smem; the whole block: 32-row diagonal blocks by warp 0 in registers (shuffle
+// broadcast), the off-diagonal updates by all threads.
+__device__ void chol_solve_block(const double *Lm, int k, double *v) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int kb = 0; kb < k; kb += 32) {                  // forward: L y = v
+        const int bs = min(32, k - kb);
+        if (warp == 0) {
+            double x = lane < bs ? v[kb + lane] : 0.0;
+            for (int c = 0; c < bs; ++c) {
+                if (lane == c) x *= Lm[(kb + c) * k + kb + c];
+                const double yc = __shfl_sync(0xffffffffu, x, c);
+                if (lane > c && lane < bs) x -= Lm[(kb + lane) * k + kb + c] * yc;
+            }
+            if (lane < bs) v[kb + lane] = x;
+        }
+        __syncthreads();
+        for (int i = kb + bs + threadIdx.x; i < k; i += IT) {
+            double s = 0.0;
+            for (int c = 0; c < bs; ++c) s += Lm[i * k + kb + c] * v[kb + c];
+            v[i] -= s;
+        }
+        __syncthreads();
+    }
+    for (int kb = ((k - 1) / 32) * 32; kb >= 0; kb -= 32) {   // backward: L^T x = y
+        const int bs = min(32, k - kb);
+        if (warp == 0) {
+            double x = lane < bs ? v[kb + lane] : 0.0;
+            for (int c = bs - 1; c >= 0; --c) {
+                if (lane == c) x *= Lm[(kb + c) * k + kb + c];
+                const double xc = __shfl_sync(0xffffffffu, x, c);
+                if (lane < c) x -= Lm[(kb + c) * k + kb + lane] * xc;
+            }
+            if (lane < bs) v[kb + lane] = x;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kb; i += IT) {
+            double s = 0.0;
+            for (int c = 0; c < bs; ++c) s += Lm[(kb + c) * k + i] * v[kb + c];
+            v[i] -= s;
+        }
+        __syncthreads();
+    }
+}
+
 // Form the Schur complement S and the Mll factors for the current D (= lambda / s).
 __device__ void factor(const Blk &B) {
     const int nb = B.nb, n = B.n, lane = threadIdx.x & 31;
@@ -309,12 +354,12 @@ __device__ void solve(const Blk &B, double *by, double *bxi, double *t) {
         if (lane == 0) by[k] -= s;
     }
     __syncthreads();
-    if (warp == 0) {
+    {
         double *v = B.Drow;                               // [>= nb] smem
-        for (int k = lane; k < nb; k += 32) v[k] = by[k];
-        __syncwarp();
-        chol_solve_warp(B.S, nb, v);
-        for (int k = lane; k < nb; k += 32) by[k] = v[k];
+        for (int k = threadIdx.x; k < nb; k += IT) v[k] = by[k];
+        __syncthreads();
+        chol_solve_block(B.S, nb, v);
+        for (int k = threadIdx.x; k < nb; k += IT) by[k] = v[k];
     }
     __syncthreads();
     // dxi_l = Mll^{-1} (b_l - M0l^T dy);  (M0l^T dy)_d = sum_l' D_ll' delta_d (dy_l' - dy_l)
