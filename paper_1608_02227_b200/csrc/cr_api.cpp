@@ -1047,8 +1047,12 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         // work beat ~100 device round trips; deterministic either way.
         cudaError_t le = cudaSuccess;
         const bool host = (int64_t)N * (n + 1) <= kLanczosHostMax;
+        // device scratch: the Theta buffers (contiguous, not used yet; re-zeroed below)
+        const size_t th_bytes = (size_t)Ly.nbuf * Ly.Rp * Ly.ldT * Ly.es;
         const double s2 = host ? sigma_max_sq_lanczos(N, n, cfg->X, 1e-13, 2000)
-                               : sigma_max_sq_lanczos_device(N, n, ctx->at<double>(Ly.X64), 1e-13, 2000, ctx->stream, &le);
+                               : sigma_max_sq_lanczos_device(N, n, ctx->at<double>(Ly.X64), 1e-13, 2000, ctx->stream, &le,
+                                                             ctx->ws + Ly.th[0], th_bytes);
+        if (!host) IK(cudaMemsetAsync(ctx->ws + Ly.th[0], 0, th_bytes, ctx->stream));
         if (le != cudaSuccess) {
             fail(ctx, CR_ERR_CUDA, "cr_init Lanczos: %s", cudaGetErrorString(le));
             return bail(CR_ERR_CUDA);

@@ -289,7 +289,7 @@ cudaError_t launch_resident(const ResidentParams &p, int fp64, cudaStream_t s);
 double lanczos_max_ritz(const double *al, const double *be, int m);
 void lanczos_start(int64_t N, int n, double *v);
 double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol, int max_iter, cudaStream_t st,
-                                   cudaError_t *err);
+                                   cudaError_t *err, void *scratch = nullptr, size_t scratch_bytes = 0);
 
 // Max-affine estimator f_hat(z) = max_i (y_i - a_i) + xi_i . z over this shard's rows
 // (kernels/predict.cu); fp64.

@@ -208,7 +208,7 @@ __global__ void lz_shift_kernel(double *v, double *vprev, const double *w, int64
 // (cudaMallocAsync).  start: host start vector of length N (n + 1), unit norm.  Returns < 0 on
 // a CUDA error (then *err holds it).
 double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol, int max_iter, cudaStream_t st,
-                                   cudaError_t *err) {
+                                   cudaError_t *err, void *scratch, size_t scratch_bytes) {
     std::vector<double> start((size_t)N * (n + 1));
     lanczos_start(N, n, start.data());
     const int64_t m = N * (int64_t)(n + 1);
@@ -221,12 +221,28 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
     auto ok = [&](cudaError_t e) { if (e != cudaSuccess && *err == cudaSuccess) *err = e; return e == cudaSuccess; };
     *err = cudaSuccess;
     const size_t npart = std::max<size_t>((size_t)nbk * (2 + 2 * n), (size_t)nbv);
-    ok(cudaMallocAsync(&S2, sizeof(double) * ((size_t)n * n + n), st));
-    ok(cudaMallocAsync(&v, sizeof(double) * 3 * m, st));
-    ok(cudaMallocAsync(&a, sizeof(double) * N, st));
-    ok(cudaMallocAsync(&part, sizeof(double) * npart, st));
-    ok(cudaMallocAsync(&tot, sizeof(double) * (2 + 2 * n), st));
-    ok(cudaMallocAsync(&ab, sizeof(double) * (2 * (size_t)itmax + 1), st));   // alpha[it], beta[it], 0
+    // the caller's scratch when it is large enough (cr_init passes the not-yet-used Theta
+    // buffers: no allocation in the init path), else stream-ordered allocations
+    const size_t nS2 = (size_t)n * n + n, nv = 3 * (size_t)m, na = (size_t)N, ntot = 2 + 2 * (size_t)n,
+                 nab = 2 * (size_t)itmax + 1;
+    const size_t need = sizeof(double) * (nS2 + nv + na + npart + ntot + nab);
+    const bool own = !(scratch && scratch_bytes >= need);
+    if (!own) {
+        double *q = static_cast<double *>(scratch);
+        S2 = q; q += nS2;
+        v = q; q += nv;
+        a = q; q += na;
+        part = q; q += npart;
+        tot = q; q += ntot;
+        ab = q;
+    } else {
+        ok(cudaMallocAsync(&S2, sizeof(double) * nS2, st));
+        ok(cudaMallocAsync(&v, sizeof(double) * nv, st));
+        ok(cudaMallocAsync(&a, sizeof(double) * na, st));
+        ok(cudaMallocAsync(&part, sizeof(double) * npart, st));
+        ok(cudaMallocAsync(&tot, sizeof(double) * ntot, st));
+        ok(cudaMallocAsync(&ab, sizeof(double) * nab, st));   // alpha[it], beta[it], 0
+    }
     double result = -1.0;
     if (*err == cudaSuccess) {
         s = S2 + (size_t)n * n;
@@ -279,12 +295,14 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
             }
         }
     }
-    cudaFreeAsync(S2, st);
-    cudaFreeAsync(v, st);
-    cudaFreeAsync(a, st);
-    cudaFreeAsync(part, st);
-    cudaFreeAsync(tot, st);
-    cudaFreeAsync(ab, st);
+    if (own) {
+        cudaFreeAsync(S2, st);
+        cudaFreeAsync(v, st);
+        cudaFreeAsync(a, st);
+        cudaFreeAsync(part, st);
+        cudaFreeAsync(tot, st);
+        cudaFreeAsync(ab, st);
+    }
     ok(cudaStreamSynchronize(st));
     return *err == cudaSuccess ? result : -1.0;
 }
