@@ -27,6 +27,7 @@ namespace {
 
 constexpr int RT = 512;         // threads per CTA (16 warps: latency hiding at 1 CTA per SM)
 constexpr int NW = RT / 32;
+constexpr int kB2Chunks = 8;    // small-N B2: column chunks per row
 
 template <typename T, int NMAX>
 __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p) {
@@ -52,7 +53,9 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p)
     int H = 1;
     while (H < 16 && 2 * H * N <= RT) H *= 2;
     double *cph = P2 + (size_t)R * n;                           // [H][N]     column partials (H > 1)
-    T *xT = reinterpret_cast<T *>(cph + (N < RT ? RT : 0));    // [NMAX][N]  X transposed (conflict-free)
+    // small N: B2 runs over (row, column chunk) pairs; their partial records
+    double *b2s = cph + (N < RT ? RT : 0);                      // [R][kB2Chunks][1 + NMAX] (N < RT)
+    T *xT = reinterpret_cast<T *>(b2s + (N < RT ? (size_t)R * kB2Chunks * (1 + NMAX) : 0));   // [NMAX][N]
     T *xis = xT + (size_t)N * NMAX;                             // [R][NMAX]  xi of own rows
     T *thA = xis + (size_t)R * NMAX;                            // [R][ldS] Theta^{k-1}
     T *thB = thA + (size_t)R * ldS;                             // [R][ldS] Theta^{k-2} -> Theta^k
@@ -169,7 +172,37 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p)
         }
         __syncthreads();
         RS_TRACE(4);
-        // ---------------- B2: r_i^k and (Theta^k X)_i, warp per row, lanes over j (d independent)
+        // ---------------- B2: r_i^k and (Theta^k X)_i
+        if (N < RT) {
+            // small N: thread per (row, column chunk), chunks combined in order (fixed)
+            for (int t = threadIdx.x; t < rows * kB2Chunks; t += RT) {
+                const int i = t / kB2Chunks, ch = t % kB2Chunks;
+                const int64_t ja = N * ch / kB2Chunks, jb = N * (ch + 1) / kB2Chunks;
+                T racc_t = T(0), pacc_t[NMAX];
+#pragma unroll
+                for (int d = 0; d < NMAX; ++d) pacc_t[d] = T(0);
+                const T *row = thB + (size_t)i * ldS;
+                for (int64_t j = ja; j < jb; ++j) {
+                    const T th = row[j];
+                    racc_t += th;
+#pragma unroll
+                    for (int d = 0; d < NMAX; ++d) pacc_t[d] = fma(th, xT[(size_t)d * N + j], pacc_t[d]);
+                }
+                double *rec = b2s + (size_t)t * (1 + NMAX);
+                rec[0] = (double)racc_t;
+#pragma unroll
+                for (int d = 0; d < NMAX; ++d) rec[1 + d] = (double)pacc_t[d];
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < rows * (1 + n); e += RT) {
+                const int i = e / (1 + n), d = e % (1 + n);          // d = 0: r, d >= 1: (Theta X)_{d-1}
+                double v = 0.0;
+                for (int ch = 0; ch < kB2Chunks; ++ch) v += b2s[((size_t)i * kB2Chunks + ch) * (1 + NMAX) + d];
+                if (d == 0) { r2[i] = r1[i]; r1[i] = v; }
+                else { P2[i * n + d - 1] = P1[i * n + d - 1]; P1[i * n + d - 1] = v; }
+            }
+        } else
+        // warp per row, lanes over j (d independent)
         for (int i = warp; i < rows; i += NW) {
             // per-lane sums in the storage precision (fp32 within a lane's <= N/32 terms, as the
             // streaming pass sums within a tile), fp64 across lanes
@@ -255,7 +288,8 @@ __global__ void __launch_bounds__(RT, 1) resident_kernel(const ResidentParams p)
 
 template <typename T, int NMAX>
 size_t smem_of(const ResidentParams &p) {
-    return sizeof(double) * ((size_t)p.N + 2 * (size_t)p.R * (size_t)p.n + 5 * (size_t)p.R + (p.N < RT ? RT : 0)) +
+    return sizeof(double) * ((size_t)p.N + 2 * (size_t)p.R * (size_t)p.n + 5 * (size_t)p.R + (p.N < RT ? RT : 0) +
+                             (p.N < RT ? (size_t)p.R * kB2Chunks * (1 + NMAX) : 0)) +
            sizeof(T) * ((size_t)p.N * NMAX + (size_t)p.R * NMAX + 2 * (size_t)p.R * p.ldS) + 16;
 }
 
