@@ -95,6 +95,8 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
+        self.t.join(timeout=2)
+        time.sleep(0.5)          # let nvidia-smi's NVML session close before anything else is timed
         rows = [l.split(", ") for l in self.lines[since:] if l.count(",") >= 7] or \
                [l.split(", ") for l in self.lines if l.count(",") >= 7]
         sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
