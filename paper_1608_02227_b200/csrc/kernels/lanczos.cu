@@ -107,56 +107,80 @@ __global__ void __launch_bounds__(LB) lz_sums_final_kernel(const double *part, i
     if (threadIdx.x == 0) tot[q] = r;
 }
 
-// out = C^T C v (lanczos.cpp CtC::apply), warp per row k (lanes over d); S2 is symmetric, so
-// lane d reads S2[e][d] (coalesced) for t_d = sum_e S2[d][e] xi_k[e]
+// out = C^T C v (lanczos.cpp CtC::apply), warp per LR rows (lanes over d); S2 is symmetric, so
+// lane d reads S2[e][d] (coalesced) for t_d = sum_e S2[d][e] xi_k[e], each S2 element serving
+// the warp's LR rows
+constexpr int LR = 4;
 __global__ void __launch_bounds__(LB) lz_apply_kernel(const double *X, int64_t N, int n, const double *S2,
                                                       const double *s, const double *v, const double *a,
                                                       const double *tot, double *out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t k = (int64_t)blockIdx.x * LW + warp;
-    if (k >= N) return;
+    const int64_t k0 = ((int64_t)blockIdx.x * LW + warp) * LR;
+    if (k0 >= N) return;
     const double *y = v, *xi = v + N;
     const double Y = tot[0], Sa = tot[1];
     const double *Sxi = tot + 2, *w = tot + 2 + n;
-    double xk[LQ], xik[LQ], sd[LQ];
-    double xs = 0.0, sx = 0.0;
+    const double Nd = (double)N;
+    double xik[LR][LQ], t[LR][LQ], sd[LQ];
 #pragma unroll
     for (int q = 0; q < LQ; ++q) {
         const int d = lane + 32 * q;
-        xk[q] = d < n ? X[k * n + d] : 0.0;
-        xik[q] = d < n ? xi[k * n + d] : 0.0;
         sd[q] = d < n ? s[d] : 0.0;
-        xs += xik[q] * sd[q];
-        sx += (d < n ? Sxi[d] : 0.0) * xk[q];
     }
-    xs = warp_sum(xs);
-    sx = warp_sum(sx);
-    const double Nd = (double)N, yk = y[k], ak = a[k];
-    const double rho = Y - Nd * yk + Nd * ak - xs;
-    if (lane == 0) out[k] = 2.0 * Nd * yk - 2.0 * Y + Sa - sx - Nd * ak + xs;
-    double t[LQ];
 #pragma unroll
-    for (int q = 0; q < LQ; ++q) t[q] = 0.0;
+    for (int r = 0; r < LR; ++r) {
+        const int64_t k = k0 + r;
+#pragma unroll
+        for (int q = 0; q < LQ; ++q) {
+            const int d = lane + 32 * q;
+            xik[r][q] = (k < N && d < n) ? xi[k * n + d] : 0.0;
+            t[r][q] = 0.0;
+        }
+    }
 #pragma unroll
     for (int qe = 0; qe < LQ; ++qe) {
         if (32 * qe >= n) break;
         for (int src = 0; src < 32; ++src) {
             const int e = 32 * qe + src;
-            const double xe = __shfl_sync(0xffffffffu, xik[qe], src);
             if (e >= n) break;
+            double xe[LR];
+#pragma unroll
+            for (int r = 0; r < LR; ++r) xe[r] = __shfl_sync(0xffffffffu, xik[r][qe], src);
             const double *row = S2 + (size_t)e * n;
 #pragma unroll
             for (int q = 0; q < LQ; ++q) {
                 const int d = lane + 32 * q;
-                if (d < n) t[q] += row[d] * xe;
+                if (d < n) {
+                    const double sv = row[d];
+#pragma unroll
+                    for (int r = 0; r < LR; ++r) t[r][q] += sv * xe[r];
+                }
             }
         }
     }
-    double *ok = out + N + k * n;
 #pragma unroll
-    for (int q = 0; q < LQ; ++q) {
-        const int d = lane + 32 * q;
-        if (d < n) ok[d] = xk[q] * rho - w[d] + (yk - ak) * sd[q] + t[q];
+    for (int r = 0; r < LR; ++r) {
+        const int64_t k = k0 + r;
+        if (k >= N) break;
+        double xk[LQ], xs = 0.0, sx = 0.0;
+#pragma unroll
+        for (int q = 0; q < LQ; ++q) {
+            const int d = lane + 32 * q;
+            xk[q] = d < n ? X[k * n + d] : 0.0;
+            xs += xik[r][q] * sd[q];
+            sx += (d < n ? Sxi[d] : 0.0) * xk[q];
+        }
+        xs = warp_sum(xs);
+        sx = warp_sum(sx);
+        const double yk = y[k], ak = a[k];
+        const double rho = Y - Nd * yk + Nd * ak - xs;
+        if (lane == 0) out[k] = 2.0 * Nd * yk - 2.0 * Y + Sa - sx - Nd * ak + xs;
+        double *ok = out + N + k * n;
+#pragma unroll
+        for (int q = 0; q < LQ; ++q) {
+            const int d = lane + 32 * q;
+            if (d < n) ok[d] = xk[q] * rho - w[d] + (yk - ak) * sd[q] + t[r][q];
+        }
     }
 }
 
@@ -213,7 +237,7 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
     lanczos_start(N, n, start.data());
     const int64_t m = N * (int64_t)(n + 1);
     const int nbk = (int)((N + LROWS - 1) / LROWS);           // lz_sums blocks
-    const int nba = (int)((N + LW - 1) / LW);                 // lz_apply blocks (warp per row)
+    const int nba = (int)((N + (int64_t)LW * LR - 1) / ((int64_t)LW * LR));   // lz_apply blocks (warp per LR rows)
     const int nbv = (int)std::min<int64_t>((m + LB - 1) / LB, 1024);
     const int itmax = (int)std::min<int64_t>(max_iter, m);
     double *S2 = nullptr, *s = nullptr, *v = nullptr, *vp = nullptr, *w = nullptr, *a = nullptr, *part = nullptr,
