@@ -369,12 +369,41 @@ __global__ void adapt_decide_kernel(DevScalars *ts, cudaGraphConditionalHandle c
     if (has_cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
 }
 
-__global__ void adapt_finalize_kernel(const double *part, int nb, DevScalars *ts) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Fixed-order block reductions for the finalize kernels (256 threads: strided partial sums in
+// a fixed assignment, then a fixed tree)
+__device__ __forceinline__ double fin_sum(double v, double *sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st) sh[threadIdx.x] += sh[threadIdx.x + st];
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+__device__ __forceinline__ double fin_max(double v, double *sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + st]);
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(256) adapt_finalize_kernel(const double *part, int nb, DevScalars *ts) {
+    __shared__ double sh[256];
     double q = 0.0, d = 0.0;
-    for (int b = 0; b < nb; ++b) { q += part[b * 8]; d += part[b * 8 + 1]; }
-    ts->stats[8] = q;
-    ts->stats[9] = d;
+    for (int b = threadIdx.x; b < nb; b += 256) { q += part[b * 8]; d += part[b * 8 + 1]; }
+    q = fin_sum(q, sh);
+    d = fin_sum(d, sh);
+    if (threadIdx.x == 0) {
+        ts->stats[8] = q;
+        ts->stats[9] = d;
+    }
 }
 
 // Residual pass: 64 rows x 128 columns per tile, thread = 8 rows x 4 columns (register-blocked
@@ -478,19 +507,22 @@ __global__ void __launch_bounds__(256, 2) residual_kernel(const ResidualParams p
     }
 }
 
-__global__ void stats_finalize_kernel(const double *pro, int nb_pro, const double *res, int nb_res,
-                                      DevScalars *ts) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(256) stats_finalize_kernel(const double *pro, int nb_pro, const double *res,
+                                                             int nb_res, DevScalars *ts) {
+    __shared__ double sh[256];
     double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int b = 0; b < nb_pro; ++b)
+    for (int b = threadIdx.x; b < nb_pro; b += 256)
         for (int q = 0; q < 4; ++q) s[q] += pro[b * 8 + q];
-    for (int b = 0; b < nb_res; ++b) {
+    for (int b = threadIdx.x; b < nb_res; b += 256) {
         s[4] += res[b * 8 + 4];
         s[5] += res[b * 8 + 5];
         s[6] = fmax(s[6], res[b * 8 + 6]);
         s[7] += res[b * 8 + 7];
     }
-    for (int q = 0; q < 8; ++q) ts->stats[q] = s[q];
+    double r[8];
+    for (int q = 0; q < 8; ++q) r[q] = q == 6 ? fin_max(s[q], sh) : fin_sum(s[q], sh);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 8; ++q) ts->stats[q] = r[q];
 }
 
 template <typename T>
@@ -801,7 +833,7 @@ cudaError_t launch_adapt_check(const AdaptParams &p, cudaStream_t s) {
     if (nb < 1) nb = 1;
     if (nb > kStatBlocks) nb = kStatBlocks;
     adapt_check_kernel<<<(unsigned)nb, 256, 0, s>>>(p);
-    adapt_finalize_kernel<<<1, 32, 0, s>>>(p.statpart, (int)nb, p.ts);
+    adapt_finalize_kernel<<<1, 256, 0, s>>>(p.statpart, (int)nb, p.ts);
     return cudaGetLastError();
 }
 
@@ -831,7 +863,7 @@ cudaError_t launch_residual(const ResidualParams &p, int fp64, cudaStream_t s, i
 
 cudaError_t launch_stats_finalize(const double *pro, int nb_pro, const double *res, int nb_res,
                                   DevScalars *ts, cudaStream_t s) {
-    stats_finalize_kernel<<<1, 32, 0, s>>>(pro, nb_pro, res, nb_res, ts);
+    stats_finalize_kernel<<<1, 256, 0, s>>>(pro, nb_pro, res, nb_res, ts);
     return cudaGetLastError();
 }
 
