@@ -99,8 +99,9 @@ typedef enum {
                                gather kernel acquires the W counters and sums the slabs in rank
                                order.  Requires world <= 8 and shard rows S % 128 == 0 (32 for
                                fp64); CR_ERR_UNSUPPORTED otherwise.  Verified on one GPU through
-                               cr_selftest_p2p (all ranks in one cooperative launch) and a 1-rank
-                               communicator (CR_FORCE_NCCL); not yet run across GPUs.          */
+                               cr_selftest_p2p / cr_selftest_p2p_allgather (all ranks in one
+                               cooperative launch) and a 1-rank communicator (CR_FORCE_NCCL);
+                               not yet run across GPUs.                                          */
 #define CR_FLAG_ADAPTIVE 1  /* reserve a third Theta buffer + sums slot so cr_set_step_rule can
                                select CR_STEP_ADAPTIVE (a rejected trial must not overwrite
                                Theta^{k-2}); +1 Theta matrix of workspace                       */
