@@ -58,18 +58,26 @@ def momentum_next(t: float) -> float:
     return (1.0 + math.sqrt(1.0 + 4.0 * t * t)) / 2.0
 
 
-def papg(X, ybar, gamma, L, K, Tprev=None, Tt=None, t=1.0, nthreads=0):
+def papg(X, ybar, gamma, L, K, Tprev=None, Tt=None, t=1.0, nthreads=0, inplace=False):
     """Run K P-APG iterations (Fig. 2) from state (theta^{k-1}, theta~^k, t_k).
 
     Defaults are the paper's start: theta^0 = 0, theta~^1 = theta^0, t_1 = 1.
     Returns dict(Tprev=theta^{last}, Tt=theta~^{last+1}, t=t_{last+1}, y, xi) where
     (y, xi) = eta of the last iteration's Step 1.
+    inplace=True: Tprev and Tt (C-contiguous float64 N x N, both given) are updated in place
+    instead of copied -- memory only (full-size C5 states are 32 GiB each); same arithmetic.
     """
     X = _c64(X)
     ybar = _c64(ybar)
     N, n = X.shape
-    Tprev = np.zeros((N, N)) if Tprev is None else _c64(Tprev).copy()
-    Tt = Tprev.copy() if Tt is None else _c64(Tt).copy()
+    if inplace:
+        for a in (Tprev, Tt):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+                    and a.shape == (N, N)):
+                raise ValueError("inplace=True needs C-contiguous float64 N x N Tprev and Tt")
+    else:
+        Tprev = np.zeros((N, N)) if Tprev is None else _c64(Tprev).copy()
+        Tt = Tprev.copy() if Tt is None else _c64(Tt).copy()
     y = np.zeros(N)
     xi = np.zeros((N, n))
     tt = C.c_double(float(t))

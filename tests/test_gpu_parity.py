@@ -37,6 +37,24 @@ def rnd32(a):
     return np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
 
 
+def elementwise(got, want, tol, band=None):
+    """Element-wise criterion beside the Frobenius one: max_ij |dTheta| <= tol *
+    max|Theta_oracle|, and the zero pattern of Step 2's projection (.)_+  agrees away from
+    ties: an entry may be 0 on one side and positive on the other only if the positive value is
+    within `band` * max|Theta_oracle| of 0 (a pre-projection value at the rounding level)."""
+    got, want = np.asarray(got), np.asarray(want)
+    scale = max(float(np.abs(want).max()), 1e-300)
+    dmax = float(np.abs(got - want).max()) / scale
+    band = tol / 10 if band is None else band
+    mism = (got > 0) != (want > 0)
+    worst = float(np.maximum(got[mism], want[mism]).max()) / scale if mism.any() else 0.0
+    out = dict(max_abs=dmax, support_mismatch=int(mism.sum()), worst_mismatch=worst,
+               nnz_oracle=int(np.count_nonzero(want)), nnz_gpu=int(np.count_nonzero(got)))
+    assert dmax <= tol, out
+    assert worst <= band, out
+    return out
+
+
 def single_step_case(crp, X, ybar, gamma, K, prec, tol, kernel="auto"):
     """State after K oracle iterations (rounded to the storage precision) -> one GPU step
     vs one oracle step from the identical state."""
@@ -52,10 +70,11 @@ def single_step_case(crp, X, ybar, gamma, K, prec, tol, kernel="auto"):
     y, xi = s.get_eta()
     errs = dict(theta=rel(Tg, want["Tprev"]), y=rel(y, want["y"]), xi=rel(xi, want["xi"]))
     assert np.all(Tg >= 0) and np.all(np.diag(Tg) == 0)
+    errs["elementwise"] = elementwise(Tg, want["Tprev"], tol)
     np.testing.assert_array_equal(Tg1, Tk if prec == "fp64" else rnd32(Tk))
     assert tk == st["t_kp1"] and tk1 == oracle.momentum_next(st["t_kp1"])
-    for k_, v in errs.items():
-        assert v <= tol, (k_, v, errs)
+    for k_ in ("theta", "y", "xi"):
+        assert errs[k_] <= tol, (k_, errs)
     s.close()
     return errs
 
@@ -151,6 +170,27 @@ def test_K_iterations_C2_fp64_storage(crp):
     k_iteration_case(crp, "C2", "fp64")
 
 
+def _storage_floor(cfg_name, K):
+    """The fp32-storage floor of the max violation (tests/numerics/fp32_storage_floor.py, written
+    by that script from oracle/ only; tests/golden/fp32_storage_floor.json)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "fp32_storage_floor.json")
+    for r in json.load(open(path))["records"]:
+        if r["config"] == cfg_name and r["K"] == K and r["N"] == crdata.CONFIGS[cfg_name].N:
+            return r["max_violation"]
+    raise KeyError((cfg_name, K))
+
+
+def test_K_iterations_C3_full(crp):
+    """C3 at full size (N=4000, n=20, fp32) for its full 2000 iterations.
+    Objective within the north star's 1e-4; the max violation within max(1e-4, 3 x the fp32-storage
+    floor at K = 2000) -- the floor is what rounding Theta^k to fp32 once per iteration (the storage
+    precision BASELINE.json fixes), with every other operation exact, does to that quantity."""
+    tol_viol = max(1e-4, 3.0 * _storage_floor("C3", 2000))
+    print(k_iteration_case(crp, "C3", "fp32", tol_viol=tol_viol), tol_viol)
+
+
 def test_K_iterations_C3_reduced(crp):
     """C3 laws at N=1500 (fp32, 300 iterations): several tiles and a ragged tail."""
     k_iteration_case(crp, "C3", "fp32", K=300, N=1500)
@@ -244,7 +284,6 @@ def test_lipschitz_computed_by_library(crp):
     assert abs(s.L - ref.lipschitz(X, 1e-3)) <= 1e-10 * s.L
 
 
-@pytest.mark.slow
 def _theta1_rows(ybar, L, rows):
     """P1 (exact step from theta^0 = 0): Theta^1_ij = (ybar_i - ybar_j)_+ / L, zero diagonal."""
     T = np.maximum(ybar[rows][:, None] - ybar[None, :], 0.0) / L
@@ -252,36 +291,93 @@ def _theta1_rows(ybar, L, rows):
     return T
 
 
-def test_full_size_C4_two_steps(crp):
-    """C4 at full size (N=16384, n=40) in the bench's launch configuration.  Step 1 against the
-    closed form P1 on sampled rows; step 2 against the oracle started from that closed form:
-    eta^2 = eta(Theta^1) on all rows and Theta^2 on sampled rows (no oracle input comes from
-    the GPU)."""
-    cfg = crdata.CONFIGS["C4"]
+def _host_gib_available():
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 2**30
+    except Exception:
+        return float("inf")
+
+
+def _round32_inplace(A, chunk=1024):
+    for a in range(0, A.shape[0], chunk):
+        A[a:a + chunk] = A[a:a + chunk].astype(np.float32)
+
+
+def full_size_beta_step(crp, cfg_name, row_blocks=None):
+    """Full-size single step with momentum (beta != 0), in the bench's launch configuration.
+
+    The oracle runs Fig. 2 from theta^0 = 0 for two iterations IN PLACE (two N x N
+    fp64 arrays: 64 GiB at C5), giving (Theta^2, Theta^1, t_2, t_3); the state is rounded to the
+    fp32 storage precision and loaded into libcr (cr_set_theta); both sides then take iteration 3,
+    whose extrapolation weight beta_2 = (t_2 - 1)/t_3 = 0.28 makes GEMM1 (Xi' X^T) and GEMM2
+    (Theta^k X, the A2^T theta sums of Def. A1A2 P:103-128 feeding Step 1 P:386) both non-trivial.
+    Compared: Theta^3 (all rows, or `row_blocks` = [(row0, nrows)] at C5) and eta^3 = (y, xi)
+    of Step 1 at theta~^3 on all rows.  No oracle input comes from the GPU."""
+    cfg = crdata.CONFIGS[cfg_name]
     X, ybar = crdata.make_problem(cfg)
-    L = ref.lipschitz(X, cfg.gamma)
     N = cfg.N
-    rows = np.array([0, 1, 777, 8191, 8192, 12345, 16383])
-    s = crp.Solver(X, ybar, cfg.gamma, L=L)
+    L = ref.lipschitz(X, cfg.gamma)
+    P = np.zeros((N, N))
+    Q = np.zeros((N, N))
+    o1 = oracle.papg(X, ybar, cfg.gamma, L, 1, Tprev=P, Tt=Q, t=1.0, inplace=True)      # P = Q = Theta^1
+    R = P.astype(np.float32)                                                          # fp32 Theta^1
+    o2 = oracle.papg(X, ybar, cfg.gamma, L, 1, Tprev=P, Tt=Q, t=o1["t"], inplace=True)  # P = Theta^2
+    t2, t3 = o1["t"], o2["t"]
+    _round32_inplace(P)                                                               # stored Theta^2
+    for a in range(0, N, 1024):
+        Q[a:a + 1024] = R[a:a + 1024]                                                 # stored Theta^1
+    del R
+    s = crp.Solver(X, ybar, cfg.gamma, L=L, prec=cfg.prec)
     assert s.kernel == "tc"
+    s.set_theta(P, Q, t2, t3)
+    beta = (t2 - 1.0) / t3
+    assert 0.2 < beta < 0.4
+    for a in range(0, N, 1024):                    # theta~^3 (Step 4, P:389) from the stored iterates
+        Pa = P[a:a + 1024]
+        Q[a:a + 1024] = Pa + beta * (Pa - Q[a:a + 1024])
+    o3 = oracle.papg(X, ybar, cfg.gamma, L, 1, Tprev=P, Tt=Q, t=t3, inplace=True)       # P = Theta^3
+    del Q
     s.step()
-    got1 = np.concatenate([s.get_theta_rows(0, int(r), 1) for r in rows])
-    assert rel(got1, _theta1_rows(ybar, L, rows)) <= 1e-6
-    s.step()                                                    # theta~^2 = Theta^1 (beta_1 = 0)
     y, xi = s.get_eta()
-    T1 = _theta1_rows(ybar, L, np.arange(N))
-    yo, xio = oracle.eta(X, ybar, cfg.gamma, T1)
-    assert rel(y, yo) <= 1e-5 and rel(xi, xio) <= 1e-5
-    want = oracle.project_rows(X, yo, xio, L, rows, T1[rows])
-    del T1
-    got2 = np.concatenate([s.get_theta_rows(0, int(r), 1) for r in rows])
-    assert rel(got2, want) <= 1e-5
+    out = dict(y=rel(y, o3["y"]), xi=rel(xi, o3["xi"]))
+    assert out["y"] <= 1e-5 and out["xi"] <= 1e-5, out
+    if row_blocks is None:
+        Tg = s.get_theta()[0]
+        Tw = P
+    else:
+        Tg = np.concatenate([s.get_theta_rows(0, int(r0), int(nr)) for r0, nr in row_blocks])
+        Tw = np.concatenate([P[r0:r0 + nr] for r0, nr in row_blocks])
+    out["theta"] = rel(Tg, Tw)
+    out["rows"] = Tg.shape[0]
+    assert np.all(Tg >= 0)
+    assert out["theta"] <= 1e-5, out
+    out["elementwise"] = elementwise(Tg, Tw, 1e-5)
     s.close()
+    return out
+
+
+def test_full_size_C4_beta_step(crp):
+    """C4 at full size (N=16384, n=40): iteration 3 from the oracle's (Theta^2, Theta^1), every
+    row of Theta^3 plus y and Xi."""
+    print(full_size_beta_step(crp, "C4"))
+
+
+def test_full_size_C5_beta_step(crp):
+    """C5 at full size (N=65536, n=80, 2 x 16 GiB of state on one GPU): iteration 3 from the
+    oracle's (Theta^2, Theta^1); 4096 rows of Theta^3 (32 blocks of 128, tile-aligned and not,
+    spread over the matrix, both ends included) plus all of y and Xi -- GEMM2's Theta X at
+    n = 80 enters through Xi.  Needs ~100 GiB of host memory for the in-place fp64 oracle."""
+    if _host_gib_available() < 110:
+        pytest.skip(f"C5 oracle needs ~100 GiB of host RAM; {_host_gib_available():.0f} GiB available")
+    N = 65536
+    starts = sorted(set([0, N - 128] + [int(v) for v in np.linspace(128, N - 256, 30).astype(np.int64) + 61 % 128]))
+    blocks = [(r0, 128) for r0 in starts][:32]
+    print(full_size_beta_step(crp, "C5", blocks))
 
 
 def test_full_size_C5_first_step(crp):
-    """C5 at full size (N=65536, n=80, 2 x 16 GiB of state on one GPU) in the bench's launch
-    configuration: Theta^1 on sampled rows against the closed form P1."""
+    """C5 first step: Theta^1 on sampled rows against the closed form P1, eta^1 = (ybar, 0)."""
     cfg = crdata.CONFIGS["C5"]
     X, ybar = crdata.make_problem(cfg)
     L = ref.lipschitz(X, cfg.gamma)
@@ -290,8 +386,10 @@ def test_full_size_C5_first_step(crp):
     assert s.kernel == "tc"
     s.step()
     got = np.concatenate([s.get_theta_rows(0, int(r), 1) for r in rows])
-    assert rel(got, _theta1_rows(ybar, L, rows)) <= 1e-6
-    y, xi = s.get_eta()                                         # eta^1 = eta(0) = (ybar, 0)
+    want = _theta1_rows(ybar, L, rows)
+    assert rel(got, want) <= 1e-6
+    elementwise(got, want, 1e-6)
+    y, xi = s.get_eta()
     np.testing.assert_array_equal(y, ybar)
     assert np.all(xi == 0)
     s.close()

@@ -483,6 +483,46 @@ def test_continuation_stage_is_warm_started_papg():
     np.testing.assert_array_equal(a[1]["Theta"], b2["Tprev"])
 
 
+def test_continuation_stop_branch_is_the_p1106_pair_at_multiples_of_m():
+    """The early stop inside a continuation stage (oracle/core.py, the ``stop`` branch): with
+    stop = (m, infeas_tol, gap_tol) a stage ends at the FIRST multiple k of m at which the stopping
+    pair of P:1106 holds at eta(theta^k) -- normalized infeasibility ||(C eta)_-|| / sqrt(N^2 - N)
+    <= infeas_tol and |theta^T C eta| / (N^2 - N) <= gap_tol -- and returns theta^k of Fig. 2.
+    Both conditions are re-evaluated here with the dense operators of Def. A1A2, so
+    the pin is independent of oracle_eta / oracle_stats."""
+    N, n, m = 8, 2, 5
+    X, ybar = _tiny(N, n, seed=31)
+    sigma2 = ref.sigma_max_sq(X)
+    eps0, beta, kap = 0.5, 2.0, 0.02
+    gamma = kap * eps0 / beta
+    L = sigma2 / gamma
+    C = ref.dense_C(X)
+    # the dense stopping quantities at theta^k for k = m, 2m, ...
+    hist = []
+    st = dict(Tprev=np.zeros((N, N)), Tt=np.zeros((N, N)), t=1.0)
+    for k in range(m, 401, m):
+        st = oracle.papg(X, ybar, gamma, L, m, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"])
+        th = ref.theta_vec(st["Tprev"])
+        y, xi = ref.eta_dense(th, X, ybar, gamma)
+        z = C @ np.concatenate([y, xi.reshape(-1)])
+        hist.append((k, np.linalg.norm(np.minimum(z, 0.0)) / math.sqrt(N * N - N), abs(th @ z) / (N * N - N),
+                     st["Tprev"].copy()))
+    # tolerances placed between consecutive checks, so exactly one k is the first to satisfy both
+    inf_tol = 0.5 * (hist[5][1] + hist[6][1]) if hist[6][1] < hist[5][1] else hist[6][1] * (1 + 1e-9)
+    gap_tol = max(h[2] for h in hist) * 2 + 1e-300
+    first = next(h for h in hist if h[1] <= inf_tol and h[2] <= gap_tol)
+    assert m < first[0] < 400
+    st = oracle.continuation(X, ybar, sigma2, eps0=eps0, beta=beta, kappa_gamma=kap, iters=[400],
+                             stop=(m, inf_tol, gap_tol))[0]
+    assert st["iters"] == first[0]
+    np.testing.assert_array_equal(st["Theta"], first[3])
+    # a gap tolerance no iterate meets: the stage runs its whole budget
+    st2 = oracle.continuation(X, ybar, sigma2, eps0=eps0, beta=beta, kappa_gamma=kap, iters=[40],
+                              stop=(m, inf_tol, -1.0))[0]
+    assert st2["iters"] == 40
+    np.testing.assert_array_equal(st2["Theta"], hist[7][3])
+
+
 # ---------------------------------------------------------------- max-affine estimator
 def test_predict_from_exact_convex_supports():
     """With y_i = f(x_i), xi_i = grad f(x_i) of a convex f (every pair constraint of Eq. (original)
