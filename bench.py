@@ -25,7 +25,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DEFAULT_CONFIG = "C4"
+DEFAULT_CONFIG = "C5"   # the largest BASELINE.json config that fits one B200 (north star N >= 16384)
 
 
 def parse():
@@ -58,17 +58,51 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region: an NVML thread
+    polling every ~2 ms (a 12 ms C4 window still gets several samples); nvidia-smi -lms 50 as
+    the fallback when NVML is unavailable."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, device_index):
         self.dev = device_index
         self.proc = None
+        self.nvml = None
+        self.rows = []            # (sm_mhz, max_mhz, {reason names})
         self.lines = []
+        self.active = False
+        self.stop_ev = threading.Event()
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            uuid = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(self.dev).uuid)
+            except Exception:
+                pass
+            h = None
+            if uuid:
+                try:
+                    h = nv.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+                except Exception:
+                    h = None
+            if h is None:
+                h = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            self.nvml = (nv, h)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            self.bits = bits
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
@@ -79,61 +113,120 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nvml
+        while not self.stop_ev.is_set():
+            try:
+                if self.active:
+                    mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((mhz, self.max_mhz, {n for n, b in zip(self.NAMES, self.bits) if r & b}))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def mark(self):
+        self.active = True
         return len(self.lines)
 
     def stop(self, since=0):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.1)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        time.sleep(0.5)          # let nvidia-smi's NVML session close before anything else is timed
-        rows = [l.split(", ") for l in self.lines[since:] if l.count(",") >= 7] or \
-               [l.split(", ") for l in self.lines if l.count(",") >= 7]
-        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].strip() == "Active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        self.active = False
+        if self.nvml is not None:
+            self.stop_ev.set()
+            self.t.join(timeout=2)
+            rows = self.rows
+            src = "nvml (2 ms polling)"
+        elif self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+            time.sleep(0.5)      # let nvidia-smi's NVML session close before anything else is timed
+            raw = [l.split(", ") for l in self.lines[since:] if l.count(",") >= 7] or \
+                  [l.split(", ") for l in self.lines if l.count(",") >= 7]
+            rows = [(float(r[0]), float(r[1]), {self.NAMES[i] for i in range(4) if r[4 + i].strip() == "Active"})
+                    for r in raw if r[0].replace(".", "").isdigit() and r[1].replace(".", "").isdigit()]
+            src = "nvidia-smi -lms 50"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = sorted(r[0] for r in rows)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max((r[1] for r in rows), default=None),
+                "reasons": sorted(set().union(*[r[2] for r in rows])) if rows else [], "samples": len(rows),
+                "sm_mhz_min": sm[0] if sm else None, "source": src}
+
+
+def _mem_available_gib():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable"):
+                return int(line.split()[1]) / 2**20
+    except OSError:
+        pass
+    return 0.0
 
 
 def cpu_baseline(cfg, budget_s):
     """The fp64 oracle as it stands, on this host's cores, on a bounded sample of the workload:
-    full P-APG iterations on the first N' observations of the same generated problem."""
+    full P-APG iterations of the FULL problem when its two N x N fp64 states fit in half the
+    available host memory (iterations in place until ~budget_s), else of the first N'
+    observations.  C1-C3 also get a 1-thread run."""
     import numpy as np
     import crdata
     import oracle
-    X, ybar = crdata.make_problem(cfg)
-    # N' so that one oracle iteration is ~budget/6 s (probe on a small prefix)
-    Np = min(cfg.N, 1024)
-    t0 = time.perf_counter()
-    oracle.papg(X[:Np], ybar[:Np], cfg.gamma, 1e6, 1)
-    dt = max(time.perf_counter() - t0, 1e-4)
-    Np = int(min(cfg.N, Np * max(1.0, (budget_s / 6 / dt)) ** 0.5))
-    Xs, ys = np.ascontiguousarray(X[:Np]), np.ascontiguousarray(ybar[:Np])
     from oracle import ref
+    X, ybar = crdata.make_problem(cfg)
+    full = 2 * cfg.N * cfg.N * 8 / 2**30 <= 0.5 * _mem_available_gib()
+    if full:
+        Np = cfg.N
+    else:
+        # N' so that one oracle iteration is ~budget/6 s (probe on a small prefix)
+        Np = min(cfg.N, 1024)
+        t0 = time.perf_counter()
+        oracle.papg(X[:Np], ybar[:Np], cfg.gamma, 1e6, 1)
+        dt = max(time.perf_counter() - t0, 1e-4)
+        Np = int(min(cfg.N, Np * max(1.0, (budget_s / 6 / dt)) ** 0.5))
+    Xs, ys = np.ascontiguousarray(X[:Np]), np.ascontiguousarray(ybar[:Np])
     L = ref.lipschitz(Xs, cfg.gamma, form="structured")
-    t0 = time.perf_counter()
-    st = oracle.papg(Xs, ys, cfg.gamma, L, 1)           # warm-up (also sizes the timed run)
-    dt = max(time.perf_counter() - t0, 1e-4)
-    iters = int(max(1, min(1000, budget_s * 0.8 / dt)))
-    t0 = time.perf_counter()                            # one call: no per-iteration state copies
-    oracle.papg(Xs, ys, cfg.gamma, L, iters, Tprev=st["Tprev"], Tt=st["Tt"], t=st["t"])
-    t_used = time.perf_counter() - t0
-    return {"value": Np * Np * iters / t_used, "unit": "pairs/s", "cores": oracle.max_threads(),
-            "kind": "oracle", "host": host_info(),
-            "sample": f"{iters} full fp64 P-APG iterations on the first N'={Np} of {cfg.N} observations "
-                      f"of {cfg.name} (n={cfg.n}), {t_used:.1f} s"}
+    P, Q = np.zeros((Np, Np)), np.zeros((Np, Np))
+    P[0, 0] = Q[0, 0] = 0.0                           # touch: page-faulting is not oracle time
+    P.fill(0.0)
+    Q.fill(0.0)
+    t, iters, t_used = 1.0, 0, 0.0
+    while True:                                       # whole iterations, in place, until the budget
+        t0 = time.perf_counter()
+        t = oracle.papg(Xs, ys, cfg.gamma, L, 1, Tprev=P, Tt=Q, t=t, inplace=True)["t"]
+        t_used += time.perf_counter() - t0
+        iters += 1
+        if t_used + t_used / iters > budget_s or iters >= 1000:
+            break
+    out = {"value": Np * Np * iters / t_used, "unit": "pairs/s", "cores": oracle.max_threads(),
+           "kind": "oracle", "host": host_info(),
+           "sample": (f"{iters} full fp64 P-APG iteration(s) of the full {cfg.name} problem (N={Np}, n={cfg.n}) "
+                      if full else
+                      f"{iters} full fp64 P-APG iterations on the first N'={Np} of {cfg.N} observations of "
+                      f"{cfg.name} (n={cfg.n}), ") + f"from Theta^0 = 0, {t_used:.1f} s"}
+    del P, Q
+    if cfg.name in ("C1", "C2", "C3"):
+        P1, Q1 = np.zeros((Np, Np)), np.zeros((Np, Np))
+        t, it1, t1 = 1.0, 0, 0.0
+        while True:
+            t0 = time.perf_counter()
+            t = oracle.papg(Xs, ys, cfg.gamma, L, 1, Tprev=P1, Tt=Q1, t=t, inplace=True, nthreads=1)["t"]
+            t1 += time.perf_counter() - t0
+            it1 += 1
+            if t1 + t1 / it1 > budget_s / 2 or it1 >= 1000:
+                break
+        oracle.papg(Xs[:2], ys[:2], cfg.gamma, L, 1, nthreads=oracle.max_threads())   # restore the pool
+        out["one_thread"] = {"value": Np * Np * it1 / t1, "unit": "pairs/s", "cores": 1,
+                             "sample": f"{it1} iterations, {t1:.1f} s"}
+    return out
 
 
 def host_info():
@@ -237,7 +330,6 @@ def main():
     clk = ClockSampler(torch.cuda.current_device())
     if rank == 0:
         clk.start()
-    mark = clk.mark()
     # The timed region runs the product path: cr_solve replays one CUDA graph per iteration
     # (constant rule; per accepted iteration with a device-side trial loop for the adaptive
     # rule).  Per-kernel CUDA events would turn the graphs back into eager launches (and cost
@@ -251,6 +343,7 @@ def main():
     torch.cuda.synchronize()
     if group is not None:
         dist.barrier()
+    mark = clk.mark()
     e0.record(stream)
     s.solve(K)
     e1.record(stream)
@@ -285,6 +378,9 @@ def main():
     if not args.no_e2e:
         Xp = torch.from_numpy(X).pin_memory().numpy()
         yp = torch.from_numpy(ybar).pin_memory().numpy()
+        row0, rows = crp.binding.shard_range(cfg.N, rank, world)
+        yo_pin = torch.empty(cfg.N, dtype=torch.float64).pin_memory().numpy()
+        xio_pin = torch.empty((rows, cfg.n), dtype=torch.float64).pin_memory().numpy()
         torch.cuda.synchronize()
         if group is not None:
             dist.barrier()
@@ -299,7 +395,7 @@ def main():
         s2.solve(K)
         torch.cuda.synchronize()
         t_solve = time.perf_counter() - t0 - t_init
-        y, xi, _ = s2.primal()
+        y, xi, _ = s2.primal(out=(yo_pin, xio_pin))
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
         if group is not None:
@@ -310,7 +406,8 @@ def main():
         e2e = {"value": cfg.N * cfg.N * K / te, "unit": "pairs/s",
                "h2d_bytes_per_step": (X.nbytes + ybar.nbytes) / K,
                "d2h_bytes_per_step": (y.nbytes + xi.nbytes + 64) / K,
-               "timed": "Solver(X, ybar) [H2D + Lanczos L + init] + solve(K) + primal() [D2H y, xi]",
+               "timed": "Solver(X, ybar) [H2D from pinned host + Lanczos L + init] + solve(K) + "
+                        "primal() [eta(Theta^K) + diagnostics, D2H of y, xi into pinned host buffers]",
                "split_ms": {"init": 1e3 * t_init, "solve": 1e3 * t_solve, "primal": 1e3 * (te - t_init - t_solve),
                             "init_detail": init_detail}}
 

@@ -33,11 +33,12 @@
  *   - Every call enqueues on cfg.stream; calls that return host data
  *     synchronize that stream.
  *   - Every call returns cr_status; nothing is thrown across the ABI.
- *     CR_ERR_INVALID_ARG / CR_ERR_STATE leave the context usable;
+ *     CR_ERR_INVALID_ARG / CR_ERR_STATE leave the context usable (except an exhausted
+ *     adaptive iteration, see cr_set_step_rule);
  *     CR_ERR_CUDA / CR_ERR_NCCL / CR_ERR_OOM poison it (only cr_destroy,
  *     cr_last_error are then allowed).  cr_last_error() holds the message.
  *   - Multi-GPU: one process per GPU; rank p owns the contiguous row block
- *     [p*S, min(N,(p+1)*S)), S = ceil(N/world), of both Theta buffers.
+ *     [p*S, min(N,(p+1)*S)), S = cr_shard_rows(N, world, nbar), of both Theta buffers.
  *     Per iteration ranks exchange an all-gather of y and a reduce-scatter of
  *     the column sums (NCCL); X and ybar are replicated.
  *   - Not thread-safe per context.
@@ -173,6 +174,20 @@ size_t cr_workspace_size_ex(int64_t N, int32_t n, cr_precision prec, cr_kernel k
 /* Largest n this library was built for. */
 int32_t cr_max_dim(void);
 
+/* Debug: the first ring-protocol violation the tensor-core pass recorded since cr_init, when the
+ * context was created with CR_TC_CHECK=1 in the environment (0 = none, or checks off; ~0 on a CUDA
+ * error).  Layout: (code << 56) | (CTA << 32) | tile index; codes: 1/2/3 Theta slot seen by the
+ * epilogue / GEMM1 / storer holds another tile, 4/5 X_J / X_J^T slot, 6 Theta^k A operand,
+ * 7 Xi' run.  With CR_TC_G1_RUNAHEAD=1, GEMM1 no longer waits for the tile's Theta.  Synchronizes. */
+uint64_t cr_tc_check_word(cr_ctx *ctx);
+
+/* Rows S of each rank's shard (rank p owns [p*S, min(N, (p+1)*S))): ceil(N/world), rounded up to
+ * a multiple of 128 when world > 1, nbar <= 1 and every rank still owns at least one row (so the
+ * peer-memory column-sum exchange, whose 128-column blocks must not straddle owners, covers
+ * shapes like N = 4000 at 2/4/8 ranks); a partition (nbar > 1) keeps ceil(N/world), which must
+ * be a multiple of nbar.  0 for N < 1 or world < 1.  Host-only; no device needed. */
+int64_t cr_shard_rows(int64_t N, int32_t world, int64_t nbar);
+
 /* In-process group for world > 1 contexts driven by `world` host threads of one process
  * (tests run the row-sharded path on one GPU this way).  Its collectives are host rendezvous
  * of the rank threads plus cross-stream event dependencies, copies and a fixed-order sum
@@ -242,7 +257,10 @@ cr_status cr_get_sums(cr_ctx *ctx, int32_t which, double *r, double *c, double *
  *         ||A1^T D||^2 + ||A2^T D||^2 / gamma <= s ||D||^2,   D = Theta^k - theta~^k,
  *     which is the same inequality because g_gamma is quadratic at K = N (R15);
  *     one host synchronisation per trial (a trial whose Theta^k overflows the storage
- *     precision counts as failing).  More than 64 trials: CR_ERR_STATE.
+ *     precision counts as failing).  An iteration whose 64 trials all fail returns
+ *     CR_ERR_STATE and POISONS the context (t_k was not advanced and the spare buffer holds a
+ *     rejected trial, so no valid iterate remains; cr_solve reports it at its next stop test or
+ *     at its end, the failed iteration's successors being no-ops on the device).
  * Errors: CR_ERR_INVALID_ARG for a bad rule / upsilon / s_prev (context unchanged). */
 cr_status cr_set_step_rule(cr_ctx *ctx, cr_step_rule rule, double upsilon, double s_prev);
 
@@ -254,8 +272,8 @@ cr_status cr_step_info(cr_ctx *ctx, double *s_k, int64_t *trials_last, int64_t *
  * nrb rows of fp32 column partials (HOST colpart[world][nrb][N], the fused pass's layout), run
  * the production column-sum blocks (push into the owners' slabs + release) and owner gathers
  * (acquire + rank-order sum) in ONE cooperative launch; c (HOST, N) receives every owner's
- * slice = the column sums over all ranks and rows.  1 <= world <= 8, ceil(N/world) % 128 == 0
- * (else CR_ERR_UNSUPPORTED); CR_ERR_CUDA on a CUDA error. */
+ * slice = the column sums over all ranks and rows.  1 <= world <= 8, cr_shard_rows(N, world, 1)
+ * % 128 == 0 (else CR_ERR_UNSUPPORTED); CR_ERR_CUDA on a CUDA error. */
 cr_status cr_selftest_p2p(int32_t world, int64_t N, int32_t nrb, const float *colpart, double *c);
 
 /* Self-test of the CR_FLAG_P2P y' all-gather on the current device: `world` virtual ranks each

@@ -30,7 +30,8 @@ EXPORTS = (
     "cr_lipschitz_host", "cr_launch_count", "cr_set_pass_timing", "cr_pass_timing", "cr_active_kernel",
     "cr_last_error", "cr_status_string", "cr_destroy", "cr_set_step_rule", "cr_step_info", "cr_set_gamma",
     "cr_continuation", "cr_local_group_create", "cr_local_group_destroy", "cr_predict", "cr_workspace_size_ex",
-    "cr_partition_info", "cr_selftest_p2p", "cr_selftest_p2p_allgather",
+    "cr_partition_info", "cr_selftest_p2p", "cr_selftest_p2p_allgather", "cr_shard_rows",
+    "cr_tc_check_word",
 )
 
 
@@ -101,6 +102,8 @@ def load(path: str = LIB_PATH):
         "cr_selftest_p2p": (C.c_int, [i32, i64, i32, vp, vp]),
         "cr_selftest_p2p_allgather": (C.c_int, [i32, i64, vp, vp]),
         "cr_max_dim": (i32, []),
+        "cr_shard_rows": (i64, [i64, i32, i64]),
+        "cr_tc_check_word": (C.c_uint64, [vp]),
         "cr_nccl_get_unique_id": (C.c_int, [vp]),
         "cr_init": (C.c_int, [C.POINTER(CrConfig), C.POINTER(vp)]),
         "cr_set_theta": (C.c_int, [vp, vp, vp, d, d]),
@@ -188,9 +191,14 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def shard_range(N: int, rank: int, world: int):
-    """Rows [row0, row0 + rows) of Theta owned by `rank` (include/cr.h: S = ceil(N/world))."""
-    S = -(-int(N) // int(world))
+def shard_rows(N: int, world: int, nbar: int = 1) -> int:
+    """Rows per shard, S = cr_shard_rows(N, world, nbar) (include/cr.h)."""
+    return int(load().cr_shard_rows(int(N), int(world), int(nbar)))
+
+
+def shard_range(N: int, rank: int, world: int, nbar: int = 1):
+    """Rows [row0, row0 + rows) of Theta owned by `rank` (include/cr.h: S = cr_shard_rows)."""
+    S = shard_rows(N, world, nbar)
     row0 = min(int(N), int(rank) * S)
     return row0, min(int(N), row0 + S) - row0
 
@@ -239,7 +247,7 @@ class Solver:
     """One rank's share of the smoothed-dual P-APG solve (Fig. 2).
 
     X [N, n], ybar [N] are host arrays (copied).  With ``group`` (a torch.distributed
-    process group of world > 1) rank r owns rows [r*S, min(N, (r+1)*S)), S = ceil(N/world),
+    process group of world > 1) rank r owns rows [r*S, min(N, (r+1)*S)), S = shard_rows(N, world),
     and NCCL is bootstrapped by broadcasting the unique id over ``group``.
     """
 
@@ -269,7 +277,7 @@ class Solver:
             if self.world > 1:
                 uid = (C.c_char * 128).from_buffer_copy(broadcast_unique_id(group, dev))
         self._uid = uid
-        self.row0, self.rows = shard_range(self.N, self.rank, self.world)
+        self.row0, self.rows = shard_range(self.N, self.rank, self.world, max(int(nbar), 1))
         flags = (CR_FLAG_ADAPTIVE if adaptive else 0) | (CR_FLAG_P2P if p2p else 0)
         self.nbar = int(nbar)
         nbytes = workspace_size(self.N, self.n, prec, kernel, self.rank, self.world, flags, self.nbar)
@@ -326,9 +334,18 @@ class Solver:
                     "cr_solve")
         return dict(iters=rep.iters, converged=bool(rep.converged), last=rep.last.as_dict() if stop else None)
 
-    def primal(self):
-        y = np.empty(self.N)
-        xi = np.empty((self.rows, self.n))
+    def primal(self, out=None):
+        """eta(Theta^k) (Theorem 1) and its diagnostics (cr_primal).  out = (y, xi): caller
+        buffers (float64 C-contiguous, N and rows x n; e.g. pinned host memory) to fill instead
+        of fresh arrays."""
+        if out is None:
+            y = np.empty(self.N)
+            xi = np.empty((self.rows, self.n))
+        else:
+            y, xi = out
+            if not (y.dtype == np.float64 and xi.dtype == np.float64 and y.flags.c_contiguous
+                    and xi.flags.c_contiguous and y.shape == (self.N,) and xi.shape == (self.rows, self.n)):
+                raise ValueError("primal(out=(y, xi)): float64 C-contiguous arrays of shape (N,), (rows, n)")
         s = CrStepStats()
         self._check(self.lib.cr_primal(self.h, y.ctypes.data, xi.ctypes.data, C.byref(s)), "cr_primal")
         return y, xi, s.as_dict()
@@ -418,6 +435,11 @@ class Solver:
         out = np.empty(Z.shape[0])
         self._check(self.lib.cr_predict(self.h, Z.ctypes.data, Z.shape[0], out.ctypes.data), "cr_predict")
         return out
+
+    @property
+    def tc_check_word(self) -> int:
+        """First ring-protocol violation of the tensor-core pass (CR_TC_CHECK=1 at construction)."""
+        return int(self.lib.cr_tc_check_word(self.h))
 
     def set_pass_timing(self, on: bool):
         self._check(self.lib.cr_set_pass_timing(self.h, 1 if on else 0), "cr_set_pass_timing")

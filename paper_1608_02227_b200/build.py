@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc, lib = _nccl_paths()
     os.makedirs(BUILD, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp", f"-I{ROOT}/include",
-              f"-I{inc}", "--expt-relaxed-constexpr"]
+              f"-I{inc}", "--expt-relaxed-constexpr"] + os.environ.get("CR_NVCC_EXTRA", "").split()
     objs, cmds = [], []
     for src in sources():
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

@@ -23,6 +23,7 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <limits>
 
 #include "../../include/cr.h"
 #include "comm.h"
@@ -62,7 +63,8 @@ struct Layout {
     size_t yg = 0, cpart = 0;      // resident solver: y of all rows, per-CTA column partials
     size_t th[3] = {0, 0, 0}, XT, Xh, X64, ybar, r[3] = {0, 0, 0}, c[3] = {0, 0, 0}, P[3] = {0, 0, 0}, dsq = 0, y64, yv, bv, XiT, Xi64, a64, colpart, rowpart,
         slot0, rb_ptr, rb_slots, cfull, ts, statpro, statres, g1h, g1l, g2h, g2l, XiR, slot0_tc, rb_ptr_tc, rb_slots_tc,
-        total;
+        XT64, XiT64, total;
+    int nP = 0;                    // n rounded up to 8: rows of the k-major fp64 operands of the residual pass
 };
 
 // Kernel the library uses for this shape: the tcgen05 pass for fp32 with n >= 16 (where the
@@ -100,7 +102,7 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     L->NB = simt_bucket(n);
     if (L->NB == 0 || (L->fp64 && L->NB > 24)) return false;
     L->NBP = L->NB + 4;
-    L->S = (N + world - 1) / world;
+    L->S = shard_rows(N, world, L->nbar);
     L->row0 = std::min<int64_t>(N, (int64_t)rank * L->S);
     L->Ns = std::min<int64_t>(N, L->row0 + L->S) - L->row0;
     L->Rp = (int64_t)align_up((size_t)std::max<int64_t>(L->S, 1), kRowAlign);
@@ -114,6 +116,9 @@ bool make_layout(int64_t N, int n, cr_precision prec, cr_kernel kernel, int rank
     L->XT = take((size_t)L->NB * L->ldT * es);
     L->Xh = take((size_t)L->ldT * L->NBP * es);
     L->X64 = take((size_t)N * n * 8);
+    L->nP = (n + 7) / 8 * 8;
+    L->XT64 = take((size_t)L->nP * L->ldT * 8);
+    L->XiT64 = take((size_t)L->nP * L->Rp * 8);
     L->ybar = take((size_t)N * 8);
     for (int s = 0; s < L->nbuf; ++s) {
         L->r[s] = take((size_t)L->Rp * 8);
@@ -223,6 +228,11 @@ struct cr_ctx {
     int64_t T = 0;
     int64_t launches = 0;
     bool poisoned = false;
+    int64_t multi_launches = 0;   // kernels in one kMultiIters-iteration graph
+    int g1passes = 3;             // tcgen05 pass: tf32 passes of GEMM1
+    int g1f16 = 1, xexp = 0;      // tcgen05 pass: GEMM1 in kind::f16 (X scaled by 2^xexp)
+    int g1_runahead = 0;          // tcgen05 pass: GEMM1 runs ahead of the Theta stream (CR_TC_G1_RUNAHEAD)
+    unsigned long long *tc_check = nullptr;   // CR_TC_CHECK=1: ring-protocol violation word
     std::string err;
     // pass timing
     bool timing = false;
@@ -407,6 +417,10 @@ TcParams tc_params(cr_ctx *ctx, int b1, int b2, int bo, bool adapt = false) {
     p.stages = ctx->stages;
     p.window = ctx->window;
     p.g1stages = ctx->g1stages;
+    p.g1passes = ctx->g1passes;
+    p.g1f16 = ctx->g1f16;
+    p.xexp = ctx->xexp;
+    p.n = Ly.n;
     p.g2stages = ctx->g2stages;
     p.adapt = adapt ? 1 : 0;
     p.poll_ns = std::getenv("CR_TC_POLL_NS") ? std::atoi(std::getenv("CR_TC_POLL_NS")) : 64;
@@ -431,6 +445,8 @@ TcParams tc_params(cr_ctx *ctx, int b1, int b2, int bo, bool adapt = false) {
     p.cta_slot0 = ctx->at<int>(Ly.slot0_tc);
     p.trace = ctx->trace;
     p.ts = ctx->at<double>(Ly.ts);
+    p.g1_runahead = ctx->g1_runahead;
+    p.check = ctx->tc_check;
     return p;
 }
 
@@ -535,20 +551,39 @@ cr_status project_blocks(cr_ctx *ctx, SmallParams sp, int *nb_pro, bool allow_ti
 // Theta^{k-2} (bB) with step 1/s (scale), then the fused pass writing Theta^k into buffer bo
 // (bB in place for the constant step; the spare buffer for an adaptive trial) and its sums
 // into slot bo.  advance_t: Step 3 on the device (constant step); adapt: also ||D||^2 per row.
+// fuse (constant step inside a multi-iteration graph, can_fuse): FUSE_NONE = prologue, pass,
+// reduce; FUSE_FIRST = prologue, pass (reduce deferred); FUSE_MID = reduce of the previous
+// iteration fused with this prologue (reduce_prologue_kernel), pass; FUSE_LAST = fused, pass, reduce.
+enum FuseMode { FUSE_NONE = 0, FUSE_FIRST = 1, FUSE_MID = 2, FUSE_LAST = 3 };
+
+bool can_fuse(const cr_ctx *ctx) {
+    const Layout &Ly = ctx->lay;
+    return !Ly.fp64 && !ctx->coll && !ctx->p2p && Ly.nbar == 1 && !std::getenv("CR_NO_FUSE");
+}
+
 cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, bool advance_t, bool adapt,
-                       const double *s_dev = nullptr) {
+                       const double *s_dev = nullptr, int fuse = FUSE_NONE) {
     const Layout &Ly = ctx->lay;
     const int bA = ctx->bA, bB = ctx->bB;
     SmallParams sp = small_params(ctx, bA, bB, 1, scale, false);
     sp.s_dev = s_dev;
     sp.p2p_push = (ctx->p2p && Ly.nbar == 1) ? 1 : 0;
-    CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
+    if (fuse == FUSE_MID || fuse == FUSE_LAST) {
+        // the previous iteration's Theta^k is buffer bA now: its reduce + this Step 1
+        ReduceParams q = reduce_params(ctx, bA, 1, Ly.tc, false);
+        CK(launch_reduce_prologue(q, sp, ctx->stream));
+    } else {
+        CK(launch_prologue(sp, Ly.fp64, ctx->stream, nullptr));
+    }
     if (Ly.nbar > 1) {
         sp.p2p_push = 0;
         cr_status st = project_blocks(ctx, sp, nullptr, allow_timing, ctx->p2p);
         if (st != CR_OK) return st;
     }
-    if (ctx->p2p) {
+    // CR_FLAG_P2P with the tensor-core pass (all pairs): the y' acquire is fused into the pass
+    // (TcParams::yflag, own columns first); otherwise a one-CTA acquire + copy kernel
+    const bool p2p_fused = ctx->p2p && Ly.tc && Ly.nbar == 1 && !std::getenv("CR_P2P_YGATHER");
+    if (ctx->p2p && !p2p_fused) {
         // y' all-gather over peer memory: every rank's prologue pushed its rows; acquire + copy
         P2PYGather g{};
         g.yrecv = reinterpret_cast<char *>(ctx->p2p_buf) + ctx->p2p_yr;
@@ -572,6 +607,15 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
     }
     if (Ly.tc) {
         TcParams tp = tc_params(ctx, bA, bB, bo, adapt);
+        if (p2p_fused) {
+            char *pb = reinterpret_cast<char *>(ctx->p2p_buf);
+            tp.yv = reinterpret_cast<const float *>(pb + ctx->p2p_yr);
+            tp.yflag = reinterpret_cast<const unsigned long long *>(pb + ctx->p2p_yf);
+            tp.yepoch = tp.yflag + ctx->world;
+            tp.W = ctx->world;
+            tp.S = Ly.S;
+            tp.rot = (int)((Ly.row0 / kTcBN) % Ly.nCBtc);
+        }
         CK(launch_pass_tc(tp, ctx->stream));
     } else {
         PassParams p = pass_params(ctx, bA, bB, bo, adapt);
@@ -581,7 +625,14 @@ cr_status enqueue_step(cr_ctx *ctx, bool allow_timing, int bo, double scale, boo
         CK(cudaEventRecord(e1, ctx->stream));
         ctx->ev_iters += 1;
     }
+    if (fuse == FUSE_FIRST || fuse == FUSE_MID) {      // reduce deferred into the next prologue
+        ctx->launches += 2;
+        return CR_OK;
+    }
     ReduceParams q = reduce_params(ctx, bo, advance_t ? 1 : 0, Ly.tc, adapt);
+    if (p2p_fused)                                     // the pass consumed this epoch's peer y'
+        q.yepoch = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ctx->p2p_buf) + ctx->p2p_yf) +
+                   ctx->world;
     CK(launch_reduce(q, Ly.fp64, ctx->stream));
     if (ctx->coll) {
         cr_status st = reduce_scatter_c(ctx, bo);
@@ -628,6 +679,25 @@ cr_status enqueue_adaptive_trial(cr_ctx *ctx, unsigned long long cond, int has_c
     return CR_OK;
 }
 
+// An adaptive iteration whose trials l = 0 .. max_trials-1 all failed Eq. (adaptive-check): the
+// device did not advance t_k and holds a rejected trial in the spare buffer, so there is no valid
+// iterate to continue from -- the context is poisoned (include/cr.h, cr_set_step_rule).
+cr_status adaptive_exhausted(cr_ctx *ctx) {
+    ctx->poisoned = true;
+    return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check); context poisoned",
+                ctx->max_trials);
+}
+
+// true if the device recorded an exhausted adaptive iteration (synchronizes)
+cr_status adaptive_error_flag(cr_ctx *ctx, bool *failed) {
+    double err = 0.0;
+    CK(cudaMemcpyAsync(&err, &ctx->at<DevScalars>(ctx->lay.ts)->ad[AD_ERR], sizeof err, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *failed = err != 0.0;
+    return CR_OK;
+}
+
 // One adaptive iteration driven from the host (local groups, per-pass timing): one trial per
 // round trip; the accept/retry state lives on the device exactly as in the graph path.
 cr_status adaptive_step(cr_ctx *ctx) {
@@ -640,8 +710,7 @@ cr_status adaptive_step(cr_ctx *ctx) {
         double ad[8];
         CK(cudaMemcpyAsync(ad, ts->ad, sizeof ad, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
-        if (ad[AD_ERR] != 0.0)
-            return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check)", ctx->max_trials);
+        if (ad[AD_ERR] != 0.0) return adaptive_exhausted(ctx);
         if (ad[AD_L] == 0.0) break;                       // accepted
     }
     advance_host(ctx, bo);
@@ -692,8 +761,9 @@ bool use_adaptive_graph(const cr_ctx *ctx) {
     return !ctx->coll && !ctx->timing && ctx->world == 1 && !std::getenv("CR_NO_ADAPTIVE_GRAPH");
 }
 
-// eta(Theta^k) and diagnostics (Theorem 1 semantics); synchronizes.
-cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
+// eta(Theta^k) and diagnostics (Theorem 1 semantics); synchronizes once.  With y_host / xi_host
+// (cr_primal) the D2H copies of eta join the same synchronization.
+cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out, double *y_host = nullptr, double *xi_host = nullptr) {
     const Layout &Ly = ctx->lay;
     const int s = ctx->bA, b = ctx->bA;
     int nb_pro = 0, nb_res = 0;
@@ -720,11 +790,15 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     rp.Xi64 = ctx->at<double>(Ly.Xi64);
     rp.a64 = ctx->at<double>(Ly.a64);
     rp.statpart = ctx->at<double>(Ly.statres);
+    rp.nP = Ly.nP;
+    rp.XT = ctx->at<double>(Ly.XT64);
+    rp.ldX = Ly.ldT;
+    rp.XiT = ctx->at<double>(Ly.XiT64);
     CK(launch_residual(rp, Ly.fp64, ctx->stream, &nb_res));
     DevScalars *ts = ctx->at<DevScalars>(Ly.ts);
     CK(launch_stats_finalize(ctx->at<double>(Ly.statpro), nb_pro, ctx->at<double>(Ly.statres), nb_res, ts,
                              ctx->stream));
-    ctx->launches += 3;
+    ctx->launches += 4;
     if (ctx->coll) {
         // stats[0..5] and [7] are sums; [6] is a max
         CM(comm_allreduce_f64(ctx->comm, ts->stats, 6, COLL_SUM, ctx->stream));
@@ -733,6 +807,10 @@ cr_status eval_stats(cr_ctx *ctx, cr_step_stats *out) {
     }
     DevScalars h{};
     CK(cudaMemcpyAsync(&h, ts, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    if (y_host) CK(cudaMemcpyAsync(y_host, y64, (size_t)Ly.N * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (xi_host && Ly.Ns > 0)
+        CK(cudaMemcpyAsync(xi_host, ctx->ws + Ly.Xi64, (size_t)Ly.Ns * Ly.n * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (out) {
         const double u2 = h.stats[0], uy = h.stats[1], xi2 = h.stats[2];
@@ -801,13 +879,16 @@ cr_status build_graph_multi(cr_ctx *ctx, int key) {
         return fail(ctx, CR_ERR_CUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(e));
     }
     cr_status st = CR_OK;
+    const bool fuse = can_fuse(ctx);
     for (int i = 0; i < kMultiIters && st == CR_OK; ++i) {
         const int bo = ctx->bB;
-        st = enqueue_step(ctx, false, bo, 1.0 / ctx->L, true, false);
+        const int mode = !fuse ? FUSE_NONE : i == 0 ? FUSE_FIRST : i == kMultiIters - 1 ? FUSE_LAST : FUSE_MID;
+        st = enqueue_step(ctx, false, bo, 1.0 / ctx->L, true, false, nullptr, mode);
         advance_host(ctx, bo);
     }
     e = cudaStreamEndCapture(ctx->stream, &g);
     ctx->stream = user;
+    ctx->multi_launches = ctx->launches - launches;
     ctx->bA = bA; ctx->bB = bB; ctx->k = k; ctx->launches = launches;
     if (st != CR_OK) { if (g) cudaGraphDestroy(g); return st; }
     if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
@@ -841,6 +922,25 @@ cr_status build_graph(cr_ctx *ctx, int key) {
     e = cudaGraphInstantiate(&ctx->graph[key], g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(ctx, CR_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    return CR_OK;
+}
+
+// Instantiate every constant-step graph cr_solve may replay -- the 8-iteration and the
+// 1-iteration graph of both buffer-role assignments -- on first use, so no later cr_solve call
+// (e.g. a timed one after a short warm-up) pays a capture.
+cr_status prebuild_graphs(cr_ctx *ctx) {
+    const int bA = ctx->bA, bB = ctx->bB;
+    for (int swap = 0; swap < 2; ++swap) {
+        ctx->bA = swap ? bB : bA;
+        ctx->bB = swap ? bA : bB;
+        const int key = 3 * ctx->bA + ctx->bB;
+        cr_status st = CR_OK;
+        if (!ctx->graph_multi[key]) st = build_graph_multi(ctx, key);
+        if (st == CR_OK && !ctx->graph[key]) st = build_graph(ctx, key);
+        ctx->bA = bA;
+        ctx->bB = bB;
+        if (st != CR_OK) return st;
+    }
     return CR_OK;
 }
 
@@ -938,6 +1038,20 @@ cr_status cr_nccl_get_unique_id(void *out) {
     if (ncclGetUniqueId(&id) != ncclSuccess) return CR_ERR_NCCL;
     std::memcpy(out, &id, sizeof id);
     return CR_OK;
+}
+
+uint64_t cr_tc_check_word(cr_ctx *ctx) {
+    if (!ctx || !ctx->tc_check) return 0;
+    unsigned long long w = 0;
+    if (cudaMemcpyAsync(&w, ctx->tc_check, sizeof w, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return ~0ULL;
+    return w;
+}
+
+int64_t cr_shard_rows(int64_t N, int32_t world, int64_t nbar) {
+    if (N < 1 || world < 1) return 0;
+    return shard_rows(N, world, std::max<int64_t>(nbar, 1));
 }
 
 size_t cr_workspace_size(int64_t N, int32_t n, cr_precision prec, cr_kernel kernel, int32_t rank,
@@ -1064,7 +1178,8 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
     mark("lanczos");
     IK(launch_fill_inputs(ctx->at<double>(Ly.X64), N, n, Ly.NB, Ly.NBP, Ly.ldT, Ly.fp64, ctx->ws + Ly.XT,
                           ctx->ws + Ly.Xh, ctx->stream));
-    ctx->launches += 1;
+    IK(launch_transpose_pad(ctx->at<double>(Ly.X64), N, n, Ly.nP, Ly.ldT, ctx->at<double>(Ly.XT64), ctx->stream));
+    ctx->launches += 2;
     DevScalars h{};
     h.t_prev = 1.0;   // beta_0 = 0: theta~^1 = theta^0
     h.t_cur = 1.0;    // t_1 = 1
@@ -1091,14 +1206,40 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         // X_J^T image rings (hi + lo per slot).  Defaults: 5 Theta slots and 3 + 3 image slots,
         // reduced (images first, not below 2, then Theta slots) until they fit: C4 5/3/2, C5 4/2/2.
         // CR_TC_STAGES / CR_TC_G1STAGES / CR_TC_G2STAGES override.
-        const size_t tb = 2 * (size_t)kTcBM * kTcBN * 4, b1 = 2 * (size_t)Ly.NK * 128, b2 = 2 * (size_t)Ly.NP2 * 128;
+        // GEMM1 passes (TcParams::g1passes): 3 by default; CR_TC_G1PASSES=2 drops Xi_hi X_lo
+        ctx->g1passes = 3;
+        if (const char *e = std::getenv("CR_TC_G1PASSES")) ctx->g1passes = std::atoi(e) == 2 ? 2 : 3;
+        // GEMM1 in kind::f16 (TcParams::g1f16) for n > 56: there the X_J images' shared memory
+        // limits the Theta ring (fp16 halves them: 5 slots instead of 4 at n = 80) and the tensor
+        // work drives the power cap; measured C5 0.70 -> 0.78 of the copy peak, C4 (n = 40) 0.90 ->
+        // 0.88, C3 0.64 -> 0.60 -- so kind::tf32 below.  CR_TC_G1_F16 / CR_TC_G1_TF32 override.  X
+        // is scaled by 2^xexp so its largest |x| sits just below 2^14 (fp16 range, exact scaling)
+        ctx->g1f16 = Ly.NK > 56 ? 1 : 0;
+        if (std::getenv("CR_TC_G1_F16")) ctx->g1f16 = 1;
+        if (std::getenv("CR_TC_G1_TF32")) ctx->g1f16 = 0;
+        {
+            double mx = 0.0;
+            for (int64_t e = 0; e < N * (int64_t)n; ++e) mx = std::max(mx, std::fabs(cfg->X[e]));
+            int E = 0;
+            if (mx > 0.0) std::frexp(mx, &E);
+            ctx->xexp = mx > 0.0 ? 14 - E : 0;
+        }
+        const int NK16 = Ly.NP2;
+        if (const char *e = std::getenv("CR_TC_G1_RUNAHEAD")) ctx->g1_runahead = std::atoi(e) != 0;
+        if (std::getenv("CR_TC_CHECK")) {
+            IK(cudaMalloc(&ctx->tc_check, sizeof(unsigned long long)));
+            IK(cudaMemsetAsync(ctx->tc_check, 0, sizeof(unsigned long long), ctx->stream));
+        }
+        const size_t tb = 2 * (size_t)kTcBM * kTcBN * 4, b2 = 2 * (size_t)Ly.NP2 * 128;
+        const size_t b1 = (ctx->g1passes == 3 ? 2 : 1) * (ctx->g1f16 ? (size_t)NK16 * 64 : (size_t)Ly.NK * 128);
         const size_t fixed = tc_barrier_bytes() + 1024 + 64;
         const size_t budget = 227 * 1024 - fixed;
-        auto env_int = [](const char *k, int d) {
+        auto env_int = [](const char *k, int d, int lo) {
             const char *e = std::getenv(k);
-            return e ? std::max(2, std::min(kTcMaxStages, std::atoi(e))) : d;
+            return e ? std::max(lo, std::min(kTcMaxStages, std::atoi(e))) : d;
         };
-        int st = env_int("CR_TC_STAGES", 5), s1 = env_int("CR_TC_G1STAGES", 3), s2 = env_int("CR_TC_G2STAGES", 3);
+        int st = env_int("CR_TC_STAGES", 5, 2), s1 = env_int("CR_TC_G1STAGES", 3, 1),
+            s2 = env_int("CR_TC_G2STAGES", 3, 1);
         auto bytes = [&]() { return st * tb + s1 * b1 + s2 * b2; };
         while (bytes() > budget && (s1 > 2 || s2 > 2)) {
             if (s1 * b1 >= s2 * b2 && s1 > 2) --s1;
@@ -1122,7 +1263,8 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         IK(cudaMemcpyAsync(ctx->ws + Ly.rb_slots_tc, slotst.data(), slotst.size() * 4, cudaMemcpyHostToDevice,
                            ctx->stream));
         IK(launch_tc_images(ctx->at<double>(Ly.X64), N, n, Ly.NK, Ly.NP2, Ly.nCBtc, ctx->at<float>(Ly.g1h),
-                            ctx->at<float>(Ly.g1l), ctx->at<float>(Ly.g2h), ctx->at<float>(Ly.g2l), ctx->stream));
+                            ctx->at<float>(Ly.g1l), ctx->at<float>(Ly.g2h), ctx->at<float>(Ly.g2l), ctx->g1f16,
+                            ctx->xexp, ctx->stream));
         ctx->launches += 1;
     }
     if (std::getenv("CR_TC_TRACE")) {     // debug timelines (tcgen05 pass / resident solver)
@@ -1200,7 +1342,8 @@ static cr_status p2p_setup(cr_ctx *ctx) {
     ctx->p2p_yr = (cbytes + ((size_t)W + 1) * 8 + 255) / 256 * 256;  // y' receive [W S]
     const size_t bytes = ctx->p2p_yr + (size_t)W * Ly.S * Ly.es;
     CK(cudaMalloc(&ctx->p2p_buf, bytes));
-    CK(cudaMemset(ctx->p2p_buf, 0, bytes));
+    CK(cudaMemsetAsync(ctx->p2p_buf, 0, bytes, ctx->stream));      // ordered before the exchange below
+    CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaMalloc(&ctx->p2p_tab, 4 * kP2PTab * sizeof(void *)));
     std::vector<void *> base(W, nullptr);
     base[ctx->rank] = ctx->p2p_buf;
@@ -1250,14 +1393,19 @@ cr_status cr_set_theta(cr_ctx *ctx, const double *tk1, const double *tk2, double
     const double *src[2] = {tk1, tk2};
     for (int b = 0; b < 2; ++b) {
         if (!src[b]) continue;
-        for (int64_t i = 0; i < Ly.Ns; ++i)
+        int bad_sign = 0, bad_diag = 0;      // host validation, rows in parallel (full-size C5: 2 x 4.3e9)
+#pragma omp parallel for schedule(static) reduction(| : bad_sign, bad_diag)
+        for (int64_t i = 0; i < Ly.Ns; ++i) {
+            const double *row = src[b] + i * Ly.N;
+            const int64_t blk = (Ly.row0 + i) / Ly.nbar;
             for (int64_t j = 0; j < Ly.N; ++j) {
-                const double v = src[b][i * Ly.N + j];
-                if (!(v >= 0.0) || !std::isfinite(v))
-                    return fail(ctx, CR_ERR_INVALID_ARG, "Theta entries must be finite and >= 0");
-                if ((Ly.row0 + i) / Ly.nbar == j / Ly.nbar && v != 0.0)
-                    return fail(ctx, CR_ERR_INVALID_ARG, "Theta must be 0 on the diagonal / intra-block pairs");
+                const double v = row[j];
+                if (!(v >= 0.0) || !std::isfinite(v)) bad_sign = 1;
+                if (j / Ly.nbar == blk && v != 0.0) bad_diag = 1;
             }
+        }
+        if (bad_sign) return fail(ctx, CR_ERR_INVALID_ARG, "Theta entries must be finite and >= 0");
+        if (bad_diag) return fail(ctx, CR_ERR_INVALID_ARG, "Theta must be 0 on the diagonal / intra-block pairs");
     }
     drop_graphs(ctx);
     for (int b = 0; b < 2; ++b) {
@@ -1266,6 +1414,7 @@ cr_status cr_set_theta(cr_ctx *ctx, const double *tk1, const double *tk2, double
             // tile-major fp32 image of this rank's rows (theta_off), zero padding, one copy
             const size_t tiles = (size_t)Ly.nRBtc * Ly.nCBtc;
             std::vector<float> tmp(tiles * (size_t)kTcBM * kTcBN, 0.f);
+#pragma omp parallel for schedule(static)
             for (int64_t i = 0; i < Ly.Ns; ++i)
                 for (int64_t j = 0; j < Ly.N; ++j)
                     tmp[(size_t)theta_off(i, j, Ly.ldT, 1, Ly.nCBtc)] = (float)src[b][i * Ly.N + j];
@@ -1277,7 +1426,8 @@ cr_status cr_set_theta(cr_ctx *ctx, const double *tk1, const double *tk2, double
                                      cudaMemcpyHostToDevice, ctx->stream));
             } else {
                 std::vector<float> tmp((size_t)Ly.Ns * Ly.N);
-                for (size_t e = 0; e < tmp.size(); ++e) tmp[e] = (float)src[b][e];
+#pragma omp parallel for schedule(static)
+                for (int64_t e = 0; e < (int64_t)tmp.size(); ++e) tmp[e] = (float)src[b][e];
                 CK(cudaMemcpy2DAsync(ctx->th[b], Ly.ldT * 4, tmp.data(), Ly.N * 4, Ly.N * 4, Ly.Ns,
                                      cudaMemcpyHostToDevice, ctx->stream));
                 CK(cudaStreamSynchronize(ctx->stream));
@@ -1309,6 +1459,7 @@ static cr_status read_buffer(cr_ctx *ctx, int b, int64_t row0, int64_t nrows, do
         CK(cudaMemcpyAsync(tmp.data(), static_cast<const float *>(ctx->th[b]) + rb0 * per_rb, tmp.size() * 4,
                            cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < nrows; ++i)
             for (int64_t j = 0; j < Ly.N; ++j)
                 out[i * Ly.N + j] = tmp[(size_t)theta_off(row0 + i - rb0 * kTcBM, j, Ly.ldT, 1, Ly.nCBtc)];
@@ -1393,6 +1544,9 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
         ttot0 = (int64_t)v;
     }
     const double Nd = (double)ctx->lay.N;
+    if (use_graph && max_iters > 0 && ctx->rule == CR_STEP_CONSTANT && !use_resident(ctx) &&
+        (st = prebuild_graphs(ctx)) != CR_OK)
+        return st;
     int64_t it = 0;
     while (it < max_iters) {
         if (use_resident(ctx)) {
@@ -1417,7 +1571,7 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
                 const int key = 3 * ctx->bA + ctx->bB;
                 if (!ctx->graph_multi[key] && (st = build_graph_multi(ctx, key)) != CR_OK) return st;
                 CK(cudaGraphLaunch(ctx->graph_multi[key], ctx->stream));
-                ctx->launches += (int64_t)per_iter * kMultiIters;
+                ctx->launches += ctx->multi_launches;
                 for (int i = 0; i < kMultiIters; ++i) advance_host(ctx, ctx->bB);
                 it += kMultiIters - 1;
             } else if (use_graph) {
@@ -1433,6 +1587,11 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
         }
         ++it;
         if (stop && (it % stop->report_every == 0 || it == max_iters)) {
+            if (ctx->rule == CR_STEP_ADAPTIVE) {          // never report stats of a rejected trial
+                bool failed = false;
+                if ((st = adaptive_error_flag(ctx, &failed)) != CR_OK) return st;
+                if (failed) return adaptive_exhausted(ctx);
+            }
             cr_step_stats s{};
             if ((st = eval_stats(ctx, &s)) != CR_OK) return st;
             if (out) out->last = s;
@@ -1448,9 +1607,7 @@ cr_status cr_solve(cr_ctx *ctx, int64_t max_iters, const cr_stop *stop, cr_repor
         CK(cudaMemcpyAsync(ad, ctx->at<DevScalars>(ctx->lay.ts)->ad, sizeof ad, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         ctx->launches += 6 * ((int64_t)ad[AD_TTOT] - ttot0);     // prologue, pass, reduce, check x2, decide
-        const double err = ad[AD_ERR];
-        if (err != 0.0)
-            return fail(ctx, CR_ERR_STATE, "adaptive step: no l < %d passed Eq. (adaptive-check)", ctx->max_trials);
+        if (ad[AD_ERR] != 0.0) return adaptive_exhausted(ctx);
     }
     return CR_OK;
 }
@@ -1459,9 +1616,11 @@ cr_status cr_primal(cr_ctx *ctx, double *y, double *xi, cr_step_stats *out) {
     cr_status st = check_ctx(ctx);
     if (st != CR_OK) return st;
     cr_step_stats s{};
-    if ((st = eval_stats(ctx, &s)) != CR_OK) return st;   // eta(Theta^k) into y64 / Xi64
+    // eta(Theta^k) into y64 / Xi64 (all ranks' y gathered), the diagnostics, and the D2H of y, xi:
+    // one synchronization
+    if ((st = eval_stats(ctx, &s, y, xi)) != CR_OK) return st;
     if (out) *out = s;
-    return cr_get_eta(ctx, y, xi);
+    return CR_OK;
 }
 
 cr_status cr_get_eta(cr_ctx *ctx, double *y, double *xi) {
@@ -1581,7 +1740,7 @@ cr_status cr_partition_info(cr_ctx *ctx, cr_partition_stats *out) {
 
 cr_status cr_selftest_p2p(int32_t world, int64_t N, int32_t nrb, const float *colpart, double *c) {
     if (world < 1 || world > kP2PTab || N < 1 || nrb < 1 || !colpart || !c) return CR_ERR_INVALID_ARG;
-    const int64_t S = (N + world - 1) / world;
+    const int64_t S = shard_rows(N, world, 1);
     if (S % 128) return CR_ERR_UNSUPPORTED;
     const int64_t ldT = (N + 3) / 4 * 4;
     float *dcp = nullptr;
@@ -1590,12 +1749,14 @@ cr_status cr_selftest_p2p(int32_t world, int64_t N, int32_t nrb, const float *co
     cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&dcp, sizeof(float) * (size_t)world * nrb * ldT);
     if (e == cudaSuccess) e = cudaMalloc(&dc, sizeof(double) * (size_t)N);
-    if (e == cudaSuccess) e = cudaMemset(dcp, 0, sizeof(float) * (size_t)world * nrb * ldT);
+    // inputs staged on the test's own (non-blocking) stream, so they are ordered before the kernel
+    if (e == cudaSuccess) e = cudaMemsetAsync(dcp, 0, sizeof(float) * (size_t)world * nrb * ldT, st);
     if (e == cudaSuccess)
-        e = cudaMemcpy2D(dcp, ldT * sizeof(float), colpart, N * sizeof(float), N * sizeof(float),
-                         (size_t)world * nrb, cudaMemcpyHostToDevice);
+        e = cudaMemcpy2DAsync(dcp, ldT * sizeof(float), colpart, N * sizeof(float), N * sizeof(float),
+                              (size_t)world * nrb, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = p2p_selftest(world, N, nrb, dcp, ldT, dc, st);
-    if (e == cudaSuccess) e = cudaMemcpy(c, dc, sizeof(double) * N, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c, dc, sizeof(double) * N, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (dcp) cudaFree(dcp);
     if (dc) cudaFree(dc);
     if (st) cudaStreamDestroy(st);
@@ -1609,9 +1770,11 @@ cr_status cr_selftest_p2p_allgather(int32_t world, int64_t N, const float *y, fl
     cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&dy, sizeof(float) * (size_t)N);
     if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(float) * (size_t)world * N);
-    if (e == cudaSuccess) e = cudaMemcpy(dy, y, sizeof(float) * (size_t)N, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dy, y, sizeof(float) * (size_t)N, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = p2p_selftest_y(world, N, dy, dout, st);
-    if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(float) * (size_t)world * N, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out, dout, sizeof(float) * (size_t)world * N, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (dy) cudaFree(dy);
     if (dout) cudaFree(dout);
     if (st) cudaStreamDestroy(st);
@@ -1716,7 +1879,11 @@ cr_status cr_predict(cr_ctx *ctx, const double *Z, int64_t M, double *out) {
         CK(launch_predict(p, ctx->stream));
         ctx->launches += 2;
     } else {
-        CK(cudaMemsetAsync(dout, 0xff, ob, ctx->stream));      // NaN pattern; replaced by the max below
+        // no rows on this rank: -inf, the identity of the max all-reduce below (a NaN pattern
+        // is not guaranteed to be ignored by ncclMax)
+        std::vector<double> ninf((size_t)M, -std::numeric_limits<double>::infinity());
+        CK(cudaMemcpyAsync(dout, ninf.data(), ob, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     if (ctx->coll) CM(comm_allreduce_f64(ctx->comm, dout, (size_t)M, COLL_MAX, ctx->stream));
     CK(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1766,9 +1933,12 @@ cr_status cr_pass_timing(cr_ctx *ctx, double *total_ms, int64_t *launches) {
 void cr_destroy(cr_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    // cr_solve is asynchronous: let queued work finish before the caller may reuse the workspace
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     drop_graphs(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->trace) cudaFree(ctx->trace);
+    if (ctx->tc_check) cudaFree(ctx->tc_check);
     for (auto e : ctx->ev) cudaEventDestroy(e);
     for (auto e : ctx->bp_ev) cudaEventDestroy(e);
     if (ctx->comm.nccl) ncclCommDestroy(ctx->comm.nccl);

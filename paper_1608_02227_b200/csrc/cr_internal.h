@@ -52,6 +52,16 @@ constexpr int64_t kLanczosHostMax = 1 << 14;   // N (n + 1) at or below: L by th
 constexpr int64_t kResidentMaxN = 4096;   // SMEM-resident small-N solver: eligible sizes
 constexpr int kResidentMaxCTAs = 256;
 
+// Rows per shard (include/cr.h, cr_shard_rows): ceil(N / world), rounded up to the 128-column
+// block of the column-sum / peer-memory exchange when world > 1 and every rank keeps >= 1 row
+// (all-pairs only: a partition needs S % nbar == 0 instead).
+inline int64_t shard_rows(int64_t N, int world, int64_t nbar) {
+    const int64_t S = (N + world - 1) / world;
+    if (world <= 1 || nbar > 1) return S;
+    const int64_t Sp = (S + 127) / 128 * 128;
+    return (int64_t)(world - 1) * Sp < N ? Sp : S;
+}
+
 // Element (i, j) of a Theta buffer (local row i, column j), in elements from the buffer base.
 //   row-major (SIMT configs): i * ldT + j
 //   tile-major (tensor-core configs): 128 x 32 tiles of 16 KB, each contiguous, tiles in
@@ -78,6 +88,8 @@ struct DevScalars {
     // [4] trials in total  [5] l of the next trial  [6] max trials  [7] error (no l passed)
     // [8] variant: 0 the paper's s_{k-1} ups^(l-1), 1 monotone backtracking s_{k-1} ups^l
     double ad[10];
+    unsigned long long fuse_cnt;   // reduce_prologue_kernel: arrivals of this launch (the last block
+                                   // advances t and resets it to 0)
 };
 enum AdaptSlots { AD_S = 0, AD_STRY = 1, AD_UPS = 2, AD_TLAST = 3, AD_TTOT = 4, AD_L = 5, AD_MAX = 6, AD_ERR = 7,
                   AD_MONO = 8 };
@@ -157,6 +169,7 @@ struct ReduceParams {
     double *c_out;         // column sums for all N columns (shard partial)
     DevScalars *ts;
     int advance_t;         // 1: t_prev <- t_cur, t_cur <- (1 + sqrt(1 + 4 t^2)) / 2
+    unsigned long long *yepoch;   // non-null: ++*yepoch (the pass consumed this epoch's peer y')
     // Peer-memory reduce-scatter (CR_FLAG_P2P): non-null -> column j's partial goes straight to
     // its owner q = j / S, at p2p_recv[q][p2p_rank * S + j - q S] (NVLink peer store), and each
     // column block then bumps p2p_flag[q][p2p_rank] with a system-scope release (S % block = 0)
@@ -167,6 +180,13 @@ struct ReduceParams {
 };
 
 cudaError_t launch_reduce(const ReduceParams &p, int prec_fp64, cudaStream_t s);
+
+// reduce of iteration k fused with the prologue of iteration k+1 (one rank, fp32 storage,
+// constant step): a block owns 32 rows i, and column i's sum is c_i, so the block needs only its
+// own columns' partials -- no grid-wide dependency between the two halves.  Same arithmetic and
+// summation order as reduce_kernel followed by prologue_kernel (bitwise identical results);
+// Step 3 (t update) by the last block to finish.  rd.advance_t must be 1.
+cudaError_t launch_reduce_prologue(const ReduceParams &rd, const SmallParams &pr, cudaStream_t s);
 int reduce_col_block(int prec_fp64);   // columns per column-sum CTA (128 fp32 partials, 32 fp64)
 
 // Owner side of the peer-memory reduce-scatter: one CTA waits (acquire, system scope) until
@@ -223,12 +243,20 @@ struct ResidualParams {
     const void *Theta;     // storage precision, layout theta_off(tiled, nCBt)
     int64_t ldT, N, Ns, row0, Rp;
     int tiled, nCBt;
-    int n;
+    int n, nP;             // features; nP = n rounded up to 8 (k-major operand rows)
     const double *X64, *y64, *Xi64, *a64;
+    const double *XT;      // [nP][ldX] x_j[k], k-major, zero padded (cr_init)
+    int64_t ldX;
+    double *XiT;           // [nP][Rp] xi_i[k], k-major (written by launch_residual from Xi64)
     double *statpart;      // [kStatBlocks][8]
 };
 
+// kernels/residual.cu: the fp64 residual pass of cr_primal (transposes Xi64 into XiT first)
 cudaError_t launch_residual(const ResidualParams &p, int prec_fp64, cudaStream_t s, int *nblocks_out);
+size_t residual_smem_bytes();
+// dst[k][i] = src[i][k] (k < n; zero for n <= k < nP and rows <= i < ld)
+cudaError_t launch_transpose_pad(const double *src, int64_t rows, int n, int nP, int64_t ld, double *dst,
+                                 cudaStream_t s);
 
 // Sum the per-CTA partials: prologue partials (nb_pro blocks: |u|^2, u.ybar, |xi|^2,
 // nonfinite) and residual partials (nb_res blocks: gap, sum R_-^2, max -R, nonfinite)
@@ -242,6 +270,22 @@ struct TcParams {
     int64_t N, Ns, row0, ldT, T;
     int G, nCB, NK, NP2, stages, window;
     int g1stages, g2stages;          // X_J / X_J^T image ring slots
+    int g1passes;                    // GEMM1 passes: 3 = Xi_hi X_hi + Xi_hi X_lo + Xi_lo X_hi;
+                                     // 2 = without Xi_hi X_lo (the X_J ring then holds X_hi only)
+    int g1f16;                       // 1: GEMM1 in kind::f16 (hi / lo halves of 11 bits each, like tf32,
+                                     //    at twice the rate and half the X_J image); Xi' rows scaled by
+                                     //    2^e_i, X by 2^xexp into the fp16 range, D1 scaled back exactly
+    int xexp;                        // the X scale exponent of the f16 images
+    // CR_FLAG_P2P y' all-gather fused into the pass (SURVEY §8(e) fix 1): yv is this rank's receive
+    // array (global row order); before the first tile of owner q's columns the producer acquires
+    // (system scope) yflag[q] >= (*yepoch + 1) * rows_q; the CTAs sweep their columns starting at
+    // column tile rot (this rank's own columns, whose y' is local), so the peers' pushes overlap
+    // the first tiles.  yflag == nullptr: yv already holds every row (NCCL / one rank).
+    const unsigned long long *yflag;
+    const unsigned long long *yepoch;
+    int W, rot;
+    int64_t S;
+    int n;                           // features (Xi' entries k >= n are treated as 0)
     int adapt;                       // 1: also accumulate ||Theta^k - theta~||^2 per row (adaptive step)
     int poll_ns;                     // producer back-off when no ring slot is free (ns)
     int theta_l2;                    // 1: Theta loads/stores with the evict-normal L2 policy (state ~ L2 size)
@@ -256,6 +300,9 @@ struct TcParams {
     double *rowpart;                 // [slots][128][NP2 + 4]: Theta X | r (wg 0, 1) | ||D||^2 (wg 0, 1)
     const int *cta_slot0;
     unsigned long long *trace;       // debug: clock64 timeline of CTA 0 (nullptr = off)
+    int g1_runahead;                 // 1: GEMM1 does not wait for the tile's Theta (needs X_J, Xi' only)
+    unsigned long long *check;       // CR_TC_CHECK: first ring-protocol violation (nullptr = checks off),
+                                     // (code << 56) | (CTA << 32) | tile; see tc_check_code
     const double *ts;
 };
 
@@ -264,7 +311,7 @@ cudaError_t launch_pass_tc(const TcParams &p, cudaStream_t s);
 cudaError_t pass_tc_prepare(int NK, int smem_bytes);
 size_t tc_barrier_bytes();
 cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,
-                             float *g2h, float *g2l, cudaStream_t s);
+                             float *g2h, float *g2l, int g1f16, int xexp, cudaStream_t s);
 
 // SMEM-resident multi-iteration solver for small N (kernels/resident.cu): K constant-step
 // iterations in one cooperative launch, row-major Theta buffers (SIMT layout), world == 1.

@@ -21,6 +21,7 @@
 // Persistent: CTA g owns tiles [g T / G, (g+1) T / G) of the row-major (row block, column
 // tile) order, like the SIMT pass.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "../cr_internal.h"
@@ -46,7 +47,14 @@ struct __align__(8) TcBarriers {
     uint64_t d1_full[2], d1_empty[2], at_full[2], at_empty[2];
     uint64_t d2_full, d2_empty, xi_full;
     uint32_t tmem_base;
+    // CR_TC_CHECK tags: the tile index u (or run index) a slot / buffer holds, written by its
+    // producer before the release (arrive) its consumer acquires (wait), checked after the wait
+    int tagT[kTcMaxStages], tagX1[kTcMaxStages], tagX2[kTcMaxStages], tagAT[2], tagXi;
 };
+
+// ring-protocol violation codes (TcParams::check)
+enum TcCheckCode { TCC_THETA_EPI = 1, TCC_THETA_G1 = 2, TCC_THETA_ST = 3, TCC_X1 = 4, TCC_X2 = 5, TCC_AT = 6,
+                   TCC_XI = 7 };
 
 // tf32 "hi" part of x: round to the nearest 10-bit-mantissa value (ties away), low 13 bits
 // cleared, so the remainder x - hi (exact in fp32) is at most 2^-12 |x| and the product error
@@ -67,6 +75,26 @@ __device__ __forceinline__ void bfly(const float *v, float *o, int lane) {
     }
 }
 
+__device__ __forceinline__ void tc_check_fail(const TcParams &p, int code, int u) {
+    atomicCAS(p.check, 0ULL, ((unsigned long long)code << 56) | ((unsigned long long)blockIdx.x << 32) | (unsigned)u);
+}
+// ring-protocol checks exist only in the TC_CHECK instantiations (kernel template below): even
+// guarded by a runtime flag they cost the C4 pass 3.5% and C5 6% (code size in the role loops)
+#define tc_check(p, cond, code, u)                                                               \
+    do {                                                                                         \
+        if constexpr (CHECK) {                                                                   \
+            if (!(cond)) tc_check_fail((p), (code), (u));                                        \
+        }                                                                                        \
+    } while (0)
+#define tc_tag(p, stmt)                                                                          \
+    do {                                                                                         \
+        if constexpr (CHECK) { stmt; }                                                           \
+    } while (0)
+
+// kernel variants (template MODE): plain, ring-protocol checks (TcParams::check), or the P2P y'
+// acquire fused into the producer with the own-columns-first rotation (TcParams::yflag)
+enum TcMode { TC_PLAIN = 0, TC_CHECK = 1, TC_P2PY = 2 };
+
 // Position of the u-th tile a CTA processes: segment k of its schedule (a row block rb and a
 // column-tile range [cbb, cbe)), column tile cb, and the slot / phase parity of the Theta ring
 // (s, ph), the X_J ring (x, xph) and the X_J^T ring (z, zph) (all incremental: no divisions).
@@ -81,10 +109,15 @@ struct Cursor {
             p.trace[((role) * 256 + (u)) * 8 + (ev)] = clock64();                               \
     } while (0)
 
-template <int NK>
+// F16: GEMM1 in kind::f16 (TcParams::g1f16) -- a compile-time switch, so each instantiation keeps
+// one GEMM1 / Xi'-load code path (the kernel is instruction-cache sensitive: a runtime switch with
+// both paths unrolled cost the C4 pass 15%)
+template <int NK, bool F16, int MODE>
 __global__ void __launch_bounds__(NTHR, 1)
 pass_tc_kernel(const TcParams p) {
+    constexpr bool CHECK = MODE == TC_CHECK, P2PY = MODE == TC_P2PY;
     constexpr int NP2 = (NK + 15) / 16 * 16;           // GEMM2 N (multiple of 16 for M = 128)
+    constexpr int NK16 = NP2;                          // GEMM1 K in kind::f16 (16 per instruction)
     extern __shared__ __align__(16) uint8_t smem_raw[];
     // 1024-byte alignment by offsetting the shared pointer itself (an integer round trip would
     // lose the shared address space and turn every access into a generic LD/ST)
@@ -97,13 +130,19 @@ pass_tc_kernel(const TcParams p) {
     // so the L2-resident operand images never wait on the epilogue of an older tile.
     const int S = p.stages, S1 = p.g1stages, S2 = p.g2stages;
     constexpr uint32_t stage_bytes = 2 * TILE_BYTES;
-    // X slot images (hi, lo)
-    constexpr uint32_t g1_bytes = (uint32_t)NK * 128, g2_bytes = (uint32_t)NP2 * 128;
+    // X slot images (hi, lo); the X_J slot holds X_hi only when GEMM1 runs 2 passes.  X_J image:
+    // tf32 NK x 32 x 4 B, or fp16 NK16 x 32 x 2 B (kind::f16 GEMM1)
+    constexpr bool f16 = F16;
+    constexpr uint32_t g1_bytes = f16 ? (uint32_t)NK16 * 64 : (uint32_t)NK * 128;
+    constexpr uint32_t g2_bytes = (uint32_t)NP2 * 128;
+    const bool g1lo = p.g1passes >= 3;
+    const uint32_t g1_slot = g1lo ? 2 * g1_bytes : g1_bytes;
     uint8_t *g1ring = smem + (size_t)S * stage_bytes;
-    uint8_t *g2ring = g1ring + (size_t)S1 * 2 * g1_bytes;
+    uint8_t *g2ring = g1ring + (size_t)S1 * g1_slot;
     uint8_t *yring = g2ring + (size_t)S2 * 2 * g2_bytes;
     TcBarriers *bar = reinterpret_cast<TcBarriers *>(yring + (size_t)kTcMaxStages * 128);
     float *colS = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + sizeof(TcBarriers) + 8);  // [2 wg][2][4][32]
+    float *rowscale = colS + 2 * 2 * 4 * 32;          // [2 runs][128] f16 GEMM1: 2^-(e_i + xexp) per row
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t0 = (int)((int64_t)blockIdx.x * p.T / p.G), t1 = (int)((int64_t)(blockIdx.x + 1) * p.T / p.G);
@@ -134,6 +173,16 @@ pass_tc_kernel(const TcParams p) {
     };
 
     auto stage_ptr = [&](int s) { return smem + (size_t)s * stage_bytes; };
+    // actual column tile of virtual column tile cb (rotation by p.rot: own columns first, P2P)
+    const int rot = P2PY ? p.rot : 0;
+    auto acb = [&](int cb) {
+        if constexpr (P2PY) {
+            const int a = cb + rot;
+            return a >= nCB ? a - nCB : a;
+        } else {
+            return cb;
+        }
+    };
     auto adv = [&](Cursor &c, int k) {
         for (int i = 0; i < k; ++i) {
             ++c.u;
@@ -185,7 +234,9 @@ pass_tc_kernel(const TcParams p) {
     pdl_wait();
     pdl_trigger();
     // TMEM columns: D1[2] 0..63 | Theta^k A operand [2] x (hi 32, lo 32) 64..191 | D2 (NP2) | Xi' hi, lo
+    // (tf32: NK columns each; fp16: NK16 / 2 columns each, two K elements per column)
     const uint32_t c_d1 = 0, c_at = 64, c_d2 = 192, c_xi = 192 + (uint32_t)NP2;
+    constexpr uint32_t xi_lo_off = f16 ? (uint32_t)NK16 / 2 : (uint32_t)NK;
 
     if (warp == 0) {
         // ============================================================ TMA producer
@@ -196,30 +247,51 @@ pass_tc_kernel(const TcParams p) {
             const uint64_t pol_stream = (p.theta_l2 & 1) ? policy_evict_normal() : policy_evict_first();
             const uint64_t pol_keep = policy_evict_last();
             Cursor c = start(), c1 = start(), c2 = start();
+            // P2P: peer y' acquired per source rank before its first column tile (see TcParams)
+            uint32_t acquired = 0;
+            const unsigned long long yep = P2PY ? *p.yepoch + 1 : 0;
             while (c.u < U || c1.u < U || c2.u < U) {
                 bool issued = false;
+                if (P2PY && c.u < U) {
+                    const int q = (int)((int64_t)acb(c.cb) * TBN / p.S);
+                    if (!((acquired >> q) & 1u)) {
+                        const int64_t rows = max((int64_t)0, min(p.S, p.N - (int64_t)q * p.S));
+                        const unsigned long long target = yep * (unsigned long long)rows;
+                        unsigned long long v;
+                        while (true) {
+                            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.yflag + q) : "memory");
+                            if (v >= target) break;
+                            __nanosleep(64);
+                        }
+                        asm volatile("fence.proxy.async.global;" ::: "memory");   // generic -> bulk-copy reads
+                        acquired |= 1u << q;
+                    }
+                }
                 if (c.u < U && mbar_test(&bar->empty[c.s], (uint32_t)(c.ph ^ 1))) {
                     issued = true;
                     TC_TRACE(0, c.u, 1);
                     uint8_t *st = stage_ptr(c.s);
                     uint64_t *fb = &bar->full[c.s];
+                    tc_tag(p, bar->tagT[c.s] = c.u);
                     mbar_arrive_expect_tx(fb, 2 * TILE_BYTES + TBN * 4);
                     // tile-major Theta: each 128 x 32 tile is 16 KB contiguous, already in the
                     // 128-B-swizzled smem image (theta_off): one bulk copy per tile
-                    const size_t toff = ((size_t)c.rb * nCB + c.cb) * (TILE_BYTES / 4);
+                    const size_t toff = ((size_t)c.rb * nCB + acb(c.cb)) * (TILE_BYTES / 4);
                     bulk_load(st, p.B1 + toff, TILE_BYTES, fb, pol_stream);
                     bulk_load(st + TILE_BYTES, p.B2 + toff, TILE_BYTES, fb, pol_stream);
-                    bulk_load(yring + c.s * 128, p.yv + c.cb * TBN, TBN * 4, fb, pol_keep);
+                    bulk_load(yring + c.s * 128, p.yv + acb(c.cb) * TBN, TBN * 4, fb, pol_keep);
                     adv(c, 1);
                 }
                 if (c1.u < U && mbar_test(&bar->g1empty[c1.x], (uint32_t)(c1.xph ^ 1))) {
                     issued = true;
                     TC_TRACE(0, c1.u, 2);
-                    uint8_t *xs = g1ring + (size_t)c1.x * 2 * g1_bytes;
+                    uint8_t *xs = g1ring + (size_t)c1.x * g1_slot;
                     uint64_t *fb = &bar->g1full[c1.x];
-                    mbar_arrive_expect_tx(fb, 2 * g1_bytes);
-                    bulk_load(xs, p.g1_hi + (size_t)c1.cb * NK * 32, g1_bytes, fb, pol_keep);
-                    bulk_load(xs + g1_bytes, p.g1_lo + (size_t)c1.cb * NK * 32, g1_bytes, fb, pol_keep);
+                    tc_tag(p, bar->tagX1[c1.x] = c1.u);
+                    mbar_arrive_expect_tx(fb, g1_slot);
+                    bulk_load(xs, p.g1_hi + (size_t)acb(c1.cb) * (g1_bytes / 4), g1_bytes, fb, pol_keep);
+                    if (g1lo)
+                        bulk_load(xs + g1_bytes, p.g1_lo + (size_t)acb(c1.cb) * (g1_bytes / 4), g1_bytes, fb, pol_keep);
                     adv(c1, 1);
                 }
                 if (c2.u < U && mbar_test(&bar->g2empty[c2.z], (uint32_t)(c2.zph ^ 1))) {
@@ -227,9 +299,10 @@ pass_tc_kernel(const TcParams p) {
                     TC_TRACE(0, c2.u, 3);
                     uint8_t *xs = g2ring + (size_t)c2.z * 2 * g2_bytes;
                     uint64_t *fb = &bar->g2full[c2.z];
+                    tc_tag(p, bar->tagX2[c2.z] = c2.u);
                     mbar_arrive_expect_tx(fb, 2 * g2_bytes);
-                    bulk_load(xs, p.g2_hi + (size_t)c2.cb * NP2 * 32, g2_bytes, fb, pol_keep);
-                    bulk_load(xs + g2_bytes, p.g2_lo + (size_t)c2.cb * NP2 * 32, g2_bytes, fb, pol_keep);
+                    bulk_load(xs, p.g2_hi + (size_t)acb(c2.cb) * NP2 * 32, g2_bytes, fb, pol_keep);
+                    bulk_load(xs + g2_bytes, p.g2_lo + (size_t)acb(c2.cb) * NP2 * 32, g2_bytes, fb, pol_keep);
                     adv(c2, 1);
                 }
                 // nothing to issue: back off instead of spinning on the issue slots the
@@ -246,36 +319,48 @@ pass_tc_kernel(const TcParams p) {
         const uint32_t g1base = __shfl_sync(0xffffffffu, smem_u32(g1ring), 0);
         const uint32_t g2base = __shfl_sync(0xffffffffu, smem_u32(g2ring), 0);
         if (warp == 1) {
-            const uint32_t id1 = idesc_tf32(TBM, TBN, 0, 0);   // A K-major (TMEM), B K-major
+            constexpr uint32_t id1 = f16 ? idesc_f16(TBM, TBN, 0, 0) : idesc_tf32(TBM, TBN, 0, 0);   // A, B K-major
             int run = 0;
             for (Cursor c = start(); c.u < U; adv(c, 1)) {
                 const int b = c.u & 1;
                 if (lane == 0) TC_TRACE(1, c.u, 0);
                 if (run_start(c)) {                          // Xi' of this run loaded into TMEM
                     mbar_wait(&bar->xi_full, (uint32_t)(run & 1));
+                    tc_check(p, bar->tagXi == run, TCC_XI, c.u);
                     ++run;
                 }
                 mbar_wait(&bar->g1full[c.x], (uint32_t)c.xph);
-                // GEMM1 also waits for the tile's Theta: letting it run ahead of the Theta stream
-                // (it needs only X_J and Xi') faulted the kernel with a 3-slot Theta ring at C4/C5
-                // (cudaErrorLaunchFailure within ~100-500 launches; 4 and 5 slots ran clean) and
-                // buys nothing, since Theta is prefetched S tiles ahead anyway.
-                mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
+                tc_check(p, bar->tagX1[c.x] == c.u, TCC_X1, c.u);
+                // GEMM1 needs only X_J and Xi'.  By default it also waits for the tile's Theta
+                // (g1_runahead = 0); run-ahead lets S' of later tiles be computed while their Theta
+                // is still in flight (ring invariants).
+                if (!p.g1_runahead) {
+                    mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
+                    tc_check(p, bar->tagT[c.s] == c.u, TCC_THETA_G1, c.u);
+                }
                 mbar_wait(&bar->d1_empty[b], (uint32_t)(((c.u >> 1) & 1) ^ 1));
                 if (lane == 0) TC_TRACE(1, c.u, 1);
                 tc_fence_after();
-                const uint32_t xh = g1base + (uint32_t)c.x * 2 * g1_bytes;
+                const uint32_t xh = g1base + (uint32_t)c.x * g1_slot;
                 const uint32_t d = tmu + c_d1 + (uint32_t)b * TBN;
                 // K-major interleave: 4-k chunks LBO = 512 B apart, 8-row j groups SBO = 128 B;
                 // K-step kk advances the start address by 1024 B (= 64 in the >>4 address field)
                 const uint64_t bh = smem_desc_u32(xh, 512, 128, 0), bl = smem_desc_u32(xh + g1_bytes, 512, 128, 0);
 #pragma unroll
                 for (int pass = 0; pass < 3; ++pass) {
+                    if (pass == 1 && !g1lo) continue;          // 2 passes: Xi_hi X_hi + Xi_lo X_hi
                     const uint64_t bd0 = pass == 1 ? bl : bh;
-                    const uint32_t a0 = tmu + c_xi + (pass == 2 ? (uint32_t)NK : 0u);
+                    const uint32_t a0 = tmu + c_xi + (pass == 2 ? xi_lo_off : 0u);
+                    if constexpr (f16) {
+                        // K = 16 per instruction: 8 TMEM columns of A, two 8-element core matrices of B
 #pragma unroll
-                    for (int kk = 0; kk < NK / 8; ++kk)
-                        mma_tf32_ts_warp(d, a0 + (uint32_t)kk * 8, bd0 + (uint64_t)(kk * 64), id1, (pass | kk) != 0);
+                        for (int kk = 0; kk < NK16 / 16; ++kk)
+                            mma_f16_ts_warp(d, a0 + (uint32_t)kk * 8, bd0 + (uint64_t)(kk * 64), id1, (pass | kk) != 0);
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < NK / 8; ++kk)
+                            mma_tf32_ts_warp(d, a0 + (uint32_t)kk * 8, bd0 + (uint64_t)(kk * 64), id1, (pass | kk) != 0);
+                    }
                 }
                 mma_commit_warp(&bar->d1_full[b]);
                 mma_commit_warp(&bar->g1empty[c.x]);
@@ -289,7 +374,9 @@ pass_tc_kernel(const TcParams p) {
                 const int a = c.u & 1;
                 if (lane == 0) TC_TRACE(1, c.u, 3);
                 mbar_wait(&bar->at_full[a], (uint32_t)((c.u >> 1) & 1));
+                tc_check(p, bar->tagAT[a] == c.u, TCC_AT, c.u);
                 mbar_wait(&bar->g2full[c.z], (uint32_t)c.zph);
+                tc_check(p, bar->tagX2[c.z] == c.u, TCC_X2, c.u);
                 if (window_start && flushes > 0) mbar_wait(&bar->d2_empty, (uint32_t)((flushes - 1) & 1));
                 if (lane == 0) TC_TRACE(1, c.u, 4);
                 tc_fence_after();
@@ -325,8 +412,9 @@ pass_tc_kernel(const TcParams p) {
             for (Cursor c = start(); c.u < U; adv(c, 1)) {
                 TC_TRACE(2, c.u, 0);
                 mbar_wait(&bar->st_full[c.s], (uint32_t)c.ph);
+                tc_check(p, bar->tagT[c.s] == c.u, TCC_THETA_ST, c.u);
                 TC_TRACE(2, c.u, 1);
-                bulk_store(p.Bout + ((size_t)c.rb * nCB + c.cb) * (TILE_BYTES / 4), stage_ptr(c.s) + TILE_BYTES,
+                bulk_store(p.Bout + ((size_t)c.rb * nCB + acb(c.cb)) * (TILE_BYTES / 4), stage_ptr(c.s) + TILE_BYTES,
                            TILE_BYTES, pol_stream);
                 bulk_commit();
                 bulk_wait_read<0>();                      // slot read by the store engine
@@ -351,24 +439,58 @@ pass_tc_kernel(const TcParams p) {
         int cur_rb = -1;
         float *my_colS = colS + wg * 2 * 4 * 32;
 
-        auto load_xi = [&](int rb) {
+        auto load_xi = [&](int rb, int run) {        // run: the segment index (GEMM1's run count)
             // Xi' row r of row block rb into TMEM (hi and lo columns)
             const float *src = p.XiR + ((int64_t)rb * TBM + r) * NK;
+            if constexpr (f16) {
+                // fp16 hi / lo of Xi' 2^e_r, e_r putting the row's largest |Xi'| just below 2^14
+                float mx = 0.f;
+                for (int k = 0; k < p.n; ++k) mx = fmaxf(mx, fabsf(src[k]));
+                // mx < 2^E, E = biased exponent - 126 (mx normal); e = 14 - E, clamped so 2^e is a float
+                const int E = (int)((__float_as_uint(mx) >> 23) & 0xffu) - 126;
+                const int e = mx > 0.f ? min(14 - E, 120) : 0;
+                const float sc = __int_as_float((uint32_t)(127 + e) << 23);   // 2^e (exact scaling)
+#pragma unroll 1
+                for (int k0 = 0; k0 < NK16; k0 += 16) {
+                    uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int k0 = 0; k0 < NK; k0 += 8) {
-                uint32_t hi[8], lo[8];
+                    for (int e2 = 0; e2 < 8; ++e2) {
+                        uint32_t hb[2], lb[2];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float x = src[k0 + e];
-                    const float h = tf32_hi(x);
-                    hi[e] = __float_as_uint(h);
-                    lo[e] = __float_as_uint(x - h);
+                        for (int h = 0; h < 2; ++h) {
+                            const int k = k0 + 2 * e2 + h;
+                            const float x = k < p.n ? src[k] * sc : 0.f;
+                            const __half xh = __float2half_rn(x);
+                            const __half xl = __float2half_rn(x - __half2float(xh));
+                            hb[h] = __half_as_ushort(xh);
+                            lb[h] = __half_as_ushort(xl);
+                        }
+                        hi[e2] = hb[0] | (hb[1] << 16);
+                        lo[e2] = lb[0] | (lb[1] << 16);
+                    }
+                    tmem_st8(tmem + lane_off + c_xi + (uint32_t)(k0 / 2), hi);
+                    tmem_st8(tmem + lane_off + c_xi + xi_lo_off + (uint32_t)(k0 / 2), lo);
                 }
-                tmem_st8(tmem + lane_off + c_xi + (uint32_t)k0, hi);
-                tmem_st8(tmem + lane_off + c_xi + (uint32_t)(NK + k0), lo);
+                rowscale[(run & 1) * TBM + r] = ldexpf(1.f, -(e + p.xexp));
+            } else {
+#pragma unroll
+                for (int k0 = 0; k0 < NK; k0 += 8) {
+                    uint32_t hi[8], lo[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float x = src[k0 + e];
+                        const float h = tf32_hi(x);
+                        hi[e] = __float_as_uint(h);
+                        lo[e] = __float_as_uint(x - h);
+                    }
+                    tmem_st8(tmem + lane_off + c_xi + (uint32_t)k0, hi);
+                    tmem_st8(tmem + lane_off + c_xi + (uint32_t)(NK + k0), lo);
+                }
             }
             tmem_wait_st();
             tc_fence_before();
+            // (the phase completes only with warp 0's arrive, which follows its tag store)
+            tc_tag(p, if (q == 0 && lane == 0) bar->tagXi = run);
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->xi_full);
         };
@@ -401,21 +523,22 @@ pass_tc_kernel(const TcParams p) {
 
         Cursor c = start();
         if (wg == 1) adv(c, 1);
-        if (wg == 0) load_xi(c.rb);
+        if (wg == 0) load_xi(c.rb, 0);
         const bool tr = (q == 0 && lane == 0);
         for (; c.u < U; adv(c, 2)) {
             const int b = c.u & 1;
-            const int rb = c.rb, cb = c.cb;
+            const int rb = c.rb, cb = acb(c.cb);
             if (tr) TC_TRACE(3 + wg, c.u, 0);
             if (c.u > 0 && run_start(c)) {
                 // new run: all GEMM1 of the previous run are complete once D1 of tile u-1 is
                 mbar_wait(&bar->d1_full[b ^ 1], (uint32_t)(((c.u - 1) >> 1) & 1));
-                load_xi(rb);
+                load_xi(rb, c.k);
             }
             const int lr = rb * TBM + r;                  // local row (< 2^31: Rp * 128)
             if (rb != cur_rb) { bi = p.bv[lr]; cur_rb = rb; }
             // ---- Theta tiles landed? (B1, B2, y' of this tile); S' = Xi' X^T ready in TMEM?
             mbar_wait(&bar->full[c.s], (uint32_t)c.ph);
+            tc_check(p, bar->tagT[c.s] == c.u, TCC_THETA_EPI, c.u);
             if (tr) TC_TRACE(3 + wg, c.u, 1);
             mbar_wait(&bar->d1_full[b], (uint32_t)((c.u >> 1) & 1));
             if (tr) TC_TRACE(3 + wg, c.u, 2);
@@ -452,6 +575,11 @@ pass_tc_kernel(const TcParams p) {
                 uint32_t sv[16];
                 tmem_ld16(tmem + lane_off + c_d1 + (uint32_t)b * TBN + 16 * half, sv);
                 tmem_wait_ld();
+                if constexpr (f16) {                       // undo the fp16 scalings (exact: powers of 2)
+                    const float rs = rowscale[(c.k & 1) * TBM + r];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) sv[e] = __float_as_uint(__uint_as_float(sv[e]) * rs);
+                }
                 float th[16];
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4) {
@@ -525,6 +653,7 @@ pass_tc_kernel(const TcParams p) {
             tc_fence_before();
             __syncwarp();
             if (tr) TC_TRACE(3 + wg, c.u, 4);
+            tc_tag(p, if (q == 0 && lane == 0) bar->tagAT[b] = c.u);
             if (lane == 0) {
                 mbar_arrive(&bar->d1_empty[b]);
                 mbar_arrive(&bar->at_full[b]);
@@ -571,11 +700,13 @@ pass_tc_kernel(const TcParams p) {
 }
 
 // Per-32-column-tile B-operand images (K-major, no swizzle: 8-row x 16-B core matrices):
-//   g1 = X_J   [j][k]: byte ((k/4) * 4 + j/8) * 128 + (j%8) * 16 + (k%4) * 4,      NK * 128 B / tile
+//   g1 = X_J   [j][k]: tf32: byte ((k/4) * 4 + j/8) * 128 + (j%8) * 16 + (k%4) * 4,   NK * 128 B / tile
+//                      fp16: byte ((k/8) * 4 + j/8) * 128 + (j%8) * 16 + (k%8) * 2,   NK16 * 64 B / tile
+//                      (values x 2^xexp, hi = fp16 rounding, lo = fp16 of the remainder)
 //   g2 = X_J^T [d][j]: byte ((j/4) * NP2/8 + d/8) * 128 + (d%8) * 16 + (j%4) * 4, NP2 * 128 B / tile
 // hi = tf32 truncation, lo = remainder; k >= n, d >= n and j >= N hold 0.
 __global__ void tc_images_kernel(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h,
-                                 float *g1l, float *g2h, float *g2l) {
+                                 float *g1l, float *g2h, float *g2l, int g1f16, int xexp) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)nCB * TBN * NP2;
     if (e >= total) return;
@@ -585,7 +716,15 @@ __global__ void tc_images_kernel(const double *X64, int64_t N, int n, int NK, in
     const int jj = (int)(j % TBN);
     const float x = (j < N && d < n) ? (float)X64[j * n + d] : 0.f;
     const float h = tf32_hi(x), l = x - h;
-    if (d < NK) {
+    if (g1f16) {
+        // d < NP2 = NK16
+        const float xs = ldexpf(x, xexp);
+        const __half xh = __float2half_rn(xs);
+        const __half xl = __float2half_rn(xs - __half2float(xh));
+        const int64_t o = cb * (int64_t)NP2 * 32 + ((d / 8) * 4 + jj / 8) * 64 + (jj % 8) * 8 + (d % 8);
+        reinterpret_cast<__half *>(g1h)[o] = xh;
+        reinterpret_cast<__half *>(g1l)[o] = xl;
+    } else if (d < NK) {
         const int64_t o = cb * (int64_t)NK * 32 + ((d / 4) * 4 + jj / 8) * 32 + (jj % 8) * 4 + (d % 4);
         g1h[o] = h;
         g1l[o] = l;
@@ -601,7 +740,18 @@ __global__ void tc_images_kernel(const double *X64, int64_t N, int n, int NK, in
 
 cudaError_t launch_pass_tc(const TcParams &p, cudaStream_t s) {
     switch (p.NK) {
-#define CR_CASE(V) case V: { cudaError_t e = pdl_launch(pass_tc_kernel<V>, dim3(p.G), dim3(NTHR), (size_t)p.smem_bytes, s, p); if (e != cudaSuccess) return e; } break;
+#define CR_CASE(V)                                                                                           \
+    case V: {                                                                                                \
+        const dim3 g(p.G), b(NTHR);                                                                          \
+        const size_t sm = (size_t)p.smem_bytes;                                                              \
+        cudaError_t e = p.g1f16 ? (p.check   ? pdl_launch(pass_tc_kernel<V, true, TC_CHECK>, g, b, sm, s, p)  \
+                                   : p.yflag ? pdl_launch(pass_tc_kernel<V, true, TC_P2PY>, g, b, sm, s, p)   \
+                                             : pdl_launch(pass_tc_kernel<V, true, TC_PLAIN>, g, b, sm, s, p)) \
+                                : (p.check   ? pdl_launch(pass_tc_kernel<V, false, TC_CHECK>, g, b, sm, s, p) \
+                                   : p.yflag ? pdl_launch(pass_tc_kernel<V, false, TC_P2PY>, g, b, sm, s, p)  \
+                                             : pdl_launch(pass_tc_kernel<V, false, TC_PLAIN>, g, b, sm, s, p)); \
+        if (e != cudaSuccess) return e;                                                                      \
+    } break;
         CR_TC_NK_LIST(CR_CASE)
 #undef CR_CASE
         default: return cudaErrorInvalidValue;
@@ -611,20 +761,32 @@ cudaError_t launch_pass_tc(const TcParams &p, cudaStream_t s) {
 
 cudaError_t pass_tc_prepare(int NK, int smem_bytes) {
     switch (NK) {
-#define CR_CASE(V) \
-    case V: return cudaFuncSetAttribute(pass_tc_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+#define CR_CASE(V)                                                                                           \
+    case V: {                                                                                                \
+        const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;                                          \
+        cudaError_t e = cudaFuncSetAttribute(pass_tc_kernel<V, false, TC_PLAIN>, A, smem_bytes);            \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, true, TC_PLAIN>, A, smem_bytes);   \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, true, TC_CHECK>, A, smem_bytes);   \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, true, TC_P2PY>, A, smem_bytes);    \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, false, TC_CHECK>, A, smem_bytes);  \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, false, TC_P2PY>, A, smem_bytes);   \
+        return e;                                                                                            \
+    }
         CR_TC_NK_LIST(CR_CASE)
 #undef CR_CASE
         default: return cudaErrorInvalidValue;
     }
 }
 
-size_t tc_barrier_bytes() { return (size_t)kTcMaxStages * 128 + sizeof(TcBarriers) + 8 + 2 * 2 * 4 * 32 * 4; }
+size_t tc_barrier_bytes() {
+    return (size_t)kTcMaxStages * 128 + sizeof(TcBarriers) + 8 + 2 * 2 * 4 * 32 * 4 + 2 * TBM * 4;
+}
 
 cudaError_t launch_tc_images(const double *X64, int64_t N, int n, int NK, int NP2, int nCB, float *g1h, float *g1l,
-                             float *g2h, float *g2l, cudaStream_t s) {
+                             float *g2h, float *g2l, int g1f16, int xexp, cudaStream_t s) {
     const int64_t total = (int64_t)nCB * TBN * NP2;
-    tc_images_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(X64, N, n, NK, NP2, nCB, g1h, g1l, g2h, g2l);
+    tc_images_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(X64, N, n, NK, NP2, nCB, g1h, g1l, g2h, g2l,
+                                                                      g1f16, xexp);
     return cudaGetLastError();
 }
 

@@ -190,6 +190,20 @@ __device__ __forceinline__ void mma_tf32_ts_warp(uint32_t d_tmem, uint32_t a_tme
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// kind::f16 (fp16 inputs, fp32 accumulate), A in TMEM: each 32-bit TMEM column holds two
+// consecutive K elements of a row (lower K index in the low half); K = 16 per instruction
+__device__ __forceinline__ void mma_f16_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+        "}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 __device__ __forceinline__ void mma_commit_warp(uint64_t *bar) {
     asm volatile(
         "{\n\t"
@@ -214,6 +228,17 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn_major, 
            | ((uint32_t)b_mn_major << 16)          // b_major
            | ((uint32_t)(N >> 3) << 17)            // n_dim
            | ((uint32_t)(M >> 4) << 24);           // m_dim
+}
+
+// Instruction descriptor, kind::f16 with fp16 A and B, fp32 accumulate.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn_major, int b_mn_major) {
+    return (1u << 4)                               // c_format = F32
+           | (0u << 7)                             // a_format = F16
+           | (0u << 10)                            // b_format = F16
+           | ((uint32_t)a_mn_major << 15)
+           | ((uint32_t)b_mn_major << 16)
+           | ((uint32_t)(N >> 3) << 17)
+           | ((uint32_t)(M >> 4) << 24);
 }
 
 // Shared-memory matrix descriptor (cute::UMMA::SmemDescriptor layout), version 1 (sm100).

@@ -1,4 +1,4 @@
-// O(N n) kernels around the fused pass, and the read-only residual pass.
+// O(N n) kernels around the fused pass (the residual pass of cr_primal is kernels/residual.cu).
 //
 //   prologue   : Step 1 of Fig. 2 in closed form at K = N, from the linear sums
 //                S = (r, c, Theta X) of Theta^{k-1} and Theta^{k-2}:
@@ -9,11 +9,12 @@
 //                all in fp64; writes the storage-precision operands of the pass
 //                (y' = y s, b' = (a - y) s, xi' = xi s with s = 1/L) and fp64 masters.
 //   reduce     : fixed-order fp64 sums of the pass's row / column partials -> S^k; t update.
-//   residual   : (C eta)_ij = y_j - y_i + a_i - xi_i . x_j in fp64 over Theta^k:
-//                sum Theta R (gap), sum (R_-)^2 and max (-R)_+ (P:1106).
+//   stats      : finalize of the prologue and residual partials.
+
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <algorithm>
+#include <cstdlib>
 #include "../cr_internal.h"
 
 namespace cr {
@@ -244,6 +245,8 @@ __device__ void colsum_block(const ReduceParams &p, int64_t cb) {
     }
 }
 
+__device__ __forceinline__ void reduce_row(const ReduceParams &p, int i, int lane);
+
 template <typename Tc>
 __global__ void __launch_bounds__(256, 4) reduce_kernel(const ReduceParams p, int ncolb) {
     pdl_wait();
@@ -254,51 +257,178 @@ __global__ void __launch_bounds__(256, 4) reduce_kernel(const ReduceParams p, in
         // one warp per row, lanes over d <= n (32-bit index math: Ns < 2^31)
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const int i = (int)(blockIdx.x - ncolb) * 8 + warp;
-        if (i < p.Ns) {
-            const int rb = i / p.rbm, ii = i - rb * p.rbm;
-            const int e0 = p.rb_ptr[rb], ns = p.rb_ptr[rb + 1] - e0;
-            const double *rp = p.rowpart;
-            // the row's partial loads are issued 4 at a time before the fixed-order sum
-            // (slot ids are broadcast loads: every lane reads the same address)
-            for (int base = 0; base < ns; base += 32) {
-                const int m = min(32, ns - base);
-                const int *ids = p.rb_slots + e0 + base;
-                // virtual columns: d < n -> Theta X, d = n -> r, d = n + 1 -> ||D||^2 (adaptive)
-                const int dmax = p.n + (p.dcol0 >= 0 ? 1 : 0);
-                for (int d = lane; d <= dmax; d += 32) {
-                    const int col = d < p.n ? d : (d == p.n ? p.rcol0 : p.dcol0);
-                    const int col2 = d < p.n ? -1 : (d == p.n ? p.rcol1 : p.dcol1);
-                    const bool two = col2 >= 0;
-                    double *out = d < p.n ? p.P + (int64_t)i * p.n + d : (d == p.n ? p.r + i : p.dsq + i);
-                    double s = base == 0 ? 0.0 : *out;
-                    for (int q0 = 0; q0 < m; q0 += 4) {
-                        double v[4], w[4];
-                        const double *rows[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {           // 4 independent loads in flight
-                            const bool ok = q0 + k < m;
-                            const int sl = ok ? ids[q0 + k] : 0;
-                            rows[k] = rp + ((int64_t)sl * p.rbm + ii) * p.NBP;
-                            v[k] = ok ? rows[k][col] : 0.0;
-                            w[k] = (ok && two) ? rows[k][col2] : 0.0;
-                        }
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            if (q0 + k < m) {
-                                s += v[k];
-                                if (two) s += w[k];
-                            }
-                        }
-                    }
-                    *out = s;
-                }
-            }
-        }
+        if (i < p.Ns) reduce_row(p, i, lane);
     }
     if (p.advance_t && blockIdx.x == 0 && threadIdx.x == 0) {
         const double t = p.ts->t_cur;
         p.ts->t_prev = t;
         p.ts->t_cur = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;   // Step 3
+    }
+    if (p.yepoch && blockIdx.x == 0 && threadIdx.x == 0) *p.yepoch += 1;
+}
+
+// Row partial sums of one row (warp, lanes over d): the reduce's row half, shared by
+// reduce_kernel and reduce_prologue_kernel (identical fixed order).
+__device__ __forceinline__ void reduce_row(const ReduceParams &p, int i, int lane) {
+    const int rb = i / p.rbm, ii = i - rb * p.rbm;
+    const int e0 = p.rb_ptr[rb], ns = p.rb_ptr[rb + 1] - e0;
+    const double *rp = p.rowpart;
+    for (int base = 0; base < ns; base += 32) {
+        const int m = min(32, ns - base);
+        const int *ids = p.rb_slots + e0 + base;
+        // virtual columns: d < n -> Theta X, d = n -> r, d = n + 1 -> ||D||^2 (adaptive)
+        const int dmax = p.n + (p.dcol0 >= 0 ? 1 : 0);
+        for (int d = lane; d <= dmax; d += 32) {
+            const int col = d < p.n ? d : (d == p.n ? p.rcol0 : p.dcol0);
+            const int col2 = d < p.n ? -1 : (d == p.n ? p.rcol1 : p.dcol1);
+            const bool two = col2 >= 0;
+            double *out = d < p.n ? p.P + (int64_t)i * p.n + d : (d == p.n ? p.r + i : p.dsq + i);
+            double s = base == 0 ? 0.0 : *out;
+            for (int q0 = 0; q0 < m; q0 += 4) {
+                double v[4], w[4];
+                const double *rows[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {           // 4 independent loads in flight
+                    const bool ok = q0 + k < m;
+                    const int sl = ok ? ids[q0 + k] : 0;
+                    rows[k] = rp + ((int64_t)sl * p.rbm + ii) * p.NBP;
+                    v[k] = ok ? rows[k][col] : 0.0;
+                    w[k] = (ok && two) ? rows[k][col2] : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (q0 + k < m) {
+                        s += v[k];
+                        if (two) s += w[k];
+                    }
+                }
+            }
+            *out = s;
+        }
+    }
+}
+
+// reduce (iteration k) + prologue (iteration k+1) for 32 rows per block, fp32 storage, one rank.
+//   phase A: c_i for the block's 32 columns (= its rows): warp w sums row blocks
+//            [nRB w / 8, nRB (w+1) / 8) of the fp32 column partials in order, lane = column, the
+//            8 warp sums combined in warp order -- reduce_kernel's colsum_block order per column;
+//            r_i, (Theta X)_i from the row-partial slots (reduce_row).
+//   phase B: prologue_kernel's per-row Step 1 at theta~^{k+1} from S^k (phase A, read back after
+//            the block barrier) and S^{k-1}.
+// beta_k = (t_k - 1) / t_{k+1} is formed from t_k read at the start; the last block to arrive
+// (after every block has read t_k) stores t_prev = t_k, t_cur = t_{k+1} (Step 3).
+// RPB rows per block (32 or 8): the block's critical path is RPB / 8 row reductions + RPB / 8
+// row prologues per warp, so small problems (few blocks) take RPB = 8 for more, shorter blocks
+template <int kPQ, int RPB>
+__global__ void __launch_bounds__(256) reduce_prologue_kernel(const ReduceParams rd, const SmallParams p) {
+    constexpr int RPW = RPB / 8;                 // rows per warp
+    __shared__ double cs[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = p.n;
+    const int64_t i0 = (int64_t)blockIdx.x * RPB;
+    // static inputs of the warp's 4 rows (final before this launch: X, ybar, S^{k-1})
+    ProRow<kPQ> row[RPW];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+        const int64_t r = i0 + warp * RPW + q;
+        if (r < p.Ns) {
+            row[q].yb = p.ybar[p.row0 + r];
+            row[q].r2 = p.r2[r];
+            row[q].c2 = p.c2[r];
+#pragma unroll
+            for (int qq = 0; qq < kPQ; ++qq) {
+                const int dd = lane + 32 * qq;
+                row[q].x[qq] = dd < n ? p.X64[(p.row0 + r) * n + dd] : 0.0;
+                row[q].P2[qq] = dd < n ? p.P2[r * n + dd] : 0.0;
+            }
+        }
+    }
+    pdl_wait();
+    pdl_trigger();
+    const double tk = p.ts->t_cur;
+    const double tn = (1.0 + sqrt(1.0 + 4.0 * tk * tk)) / 2.0;   // Step 3
+    const double beta = (tk - 1.0) / tn;                         // beta_k = (t_k - 1) / t_{k+1}
+    // ---- phase A: column sums of the block's 32 columns, row sums of its 32 rows
+    {
+        const int rb0 = (int)((int64_t)rd.nRB * warp / 8), rb1 = (int)((int64_t)rd.nRB * (warp + 1) / 8);
+        const int64_t j = i0 + lane;
+        const float *cp = static_cast<const float *>(rd.colpart);
+        double s = 0.0;
+        if (lane < RPB && j < rd.N) {
+            int rb = rb0;
+            for (; rb + 4 <= rb1; rb += 4) {
+                float v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] = cp[(int64_t)(rb + k) * rd.ldT + j];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s += (double)v[k];
+            }
+            for (; rb < rb1; ++rb) s += (double)cp[(int64_t)rb * rd.ldT + j];
+        }
+        cs[warp][lane] = s;
+    }
+#pragma unroll 1
+    for (int q = 0; q < RPW; ++q) {
+        const int64_t r = i0 + warp * RPW + q;
+        if (r < p.Ns) reduce_row(rd, (int)r, lane);
+    }
+    __syncthreads();
+    if (warp == 0 && lane < RPB && i0 + lane < rd.N) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += cs[w][lane];
+        rd.c_out[i0 + lane] = t;
+    }
+    __syncthreads();
+    // ---- phase B: Step 1 for the warp's rows
+    const double scale = p.scale;
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+        const int64_t i = i0 + warp * RPW + q;
+        if (i >= p.Ns) continue;
+        ProRow<kPQ> &cur = row[q];
+        cur.r1 = p.r1[i];
+        cur.c1 = p.c1[i];
+#pragma unroll
+        for (int qq = 0; qq < kPQ; ++qq) {
+            const int dd = lane + 32 * qq;
+            cur.P1[qq] = dd < n ? p.P1[i * n + dd] : 0.0;
+        }
+        const int64_t gi = p.row0 + i;
+        const double rt = cur.r1 + beta * (cur.r1 - cur.r2);
+        const double ct = cur.c1 + beta * (cur.c1 - cur.c2);
+        const double u = ct - rt;                                // (A1^T theta~)_i
+        const double y = cur.yb + u;
+        double a = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < kPQ; ++qq) {
+            const int d = lane + 32 * qq;
+            if (d >= n) continue;
+            const double Pt = cur.P1[qq] + beta * (cur.P1[qq] - cur.P2[qq]);
+            const double xi = (rt * cur.x[qq] - Pt) / p.gamma;  // (A2^T theta~)_i / gamma
+            p.Xi64[i * n + d] = xi;
+            if (p.XiT) static_cast<float *>(p.XiT)[(int64_t)d * p.Rp + i] = (float)(xi * scale);
+            if (p.XiR) p.XiR[i * p.NK + d] = (float)(xi * scale);
+            a += xi * cur.x[qq];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) {
+            p.y64[gi] = y;
+            p.a64[i] = a;
+            static_cast<float *>(p.yv)[gi] = (float)(y * scale);
+            static_cast<float *>(p.bv)[i] = (float)((a - y) * scale);
+        }
+    }
+    // ---- Step 3 by the last block (every block has read t_k by now)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long prev = atomicAdd(&p.ts->fuse_cnt, 1ULL);
+        if (prev == gridDim.x - 1) {
+            p.ts->t_prev = tk;
+            p.ts->t_cur = tn;
+            p.ts->fuse_cnt = 0ULL;
+        }
     }
 }
 
@@ -345,6 +475,10 @@ __global__ void __launch_bounds__(256) adapt_check_kernel(const AdaptParams p) {
 __global__ void adapt_decide_kernel(DevScalars *ts, cudaGraphConditionalHandle cond, int has_cond) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double *ad = ts->ad;
+    if (ad[AD_ERR] != 0.0) {                // an earlier iteration exhausted its trials: the
+        if (has_cond) cudaGraphSetConditional(cond, 0u);   // context is poisoned, change nothing
+        return;
+    }
     const double Q = ts->stats[8], D = ts->stats[9], s = ad[AD_STRY];
     const bool ok = isfinite(Q) && isfinite(D) && Q <= s * D;
     bool more;
@@ -403,107 +537,6 @@ __global__ void __launch_bounds__(256) adapt_finalize_kernel(const double *part,
     if (threadIdx.x == 0) {
         ts->stats[8] = q;
         ts->stats[9] = d;
-    }
-}
-
-// Residual pass: 64 rows x 128 columns per tile, thread = 8 rows x 4 columns (register-blocked
-// fp64 outer products over d: 12 shared loads -- 8 of them warp broadcasts -- per 32 FMAs).
-// Feature chunks of kRDC: shared memory stays ~50 KB whatever n is, so several CTAs share an
-// SM (latency hiding for the fp64 FMA chains); the d loop is unrolled for load / FMA overlap.
-constexpr int kRDC = 32;
-
-template <typename T>
-__global__ void __launch_bounds__(256, 2) residual_kernel(const ResidualParams p) {
-    constexpr int RBM = 64, RBN = 128;
-    extern __shared__ double rsm[];
-    double *xs = rsm;                        // [kRDC][RBN]   x_j[d] of the current feature chunk
-    double *xis = xs + kRDC * RBN;           // [kRDC][RBM]   xi_i[d]
-    double *ab = xis + RBM * kRDC;           // [RBM]         a_i - y_i
-    double *yj = ab + RBM;                   // [RBN]         y_j
-    __shared__ double red[3][256];
-    const int nrb = (int)((p.Ns + RBM - 1) / RBM), ncb = (int)((p.N + RBN - 1) / RBN);
-    const int64_t ntiles = (int64_t)nrb * ncb;
-    const T *Th = static_cast<const T *>(p.Theta);
-    double gap = 0.0, v2 = 0.0, vmax = 0.0;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t rb = t / ncb, cb = t % ncb;
-        __syncthreads();
-        for (int e = threadIdx.x; e < RBM; e += blockDim.x) {
-            const int64_t i = rb * RBM + e;
-            ab[e] = i < p.Ns ? p.a64[i] - p.y64[p.row0 + i] : 0.0;
-        }
-        for (int e = threadIdx.x; e < RBN; e += blockDim.x) {
-            const int64_t j = cb * RBN + e;
-            yj[e] = j < p.N ? p.y64[j] : 0.0;
-        }
-        double acc[8][4];
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-        for (int d0 = 0; d0 < p.n; d0 += kRDC) {
-            const int dc = min(kRDC, p.n - d0);
-            if (d0 > 0) __syncthreads();
-            for (int f = threadIdx.x; f < dc * RBN; f += blockDim.x) {      // rows of X, chunk columns
-                const int cc = f / dc, d = f % dc;
-                const int64_t j = cb * RBN + cc;
-                xs[d * RBN + cc] = j < p.N ? p.X64[j * p.n + d0 + d] : 0.0;
-            }
-            for (int e = threadIdx.x; e < RBM * dc; e += blockDim.x) {
-                const int ii = e / dc, d = e % dc;
-                const int64_t i = rb * RBM + ii;
-                xis[d * RBM + ii] = i < p.Ns ? p.Xi64[i * p.n + d0 + d] : 0.0;
-            }
-            __syncthreads();
-#pragma unroll 4
-            for (int d = 0; d < dc; ++d) {
-                const double2 x01 = *reinterpret_cast<const double2 *>(xs + d * RBN + tx * 4);
-                const double2 x23 = *reinterpret_cast<const double2 *>(xs + d * RBN + tx * 4 + 2);
-                const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
-                double xi[8];
-#pragma unroll
-                for (int r = 0; r < 8; r += 2) {
-                    const double2 q = *reinterpret_cast<const double2 *>(xis + d * RBM + ty * 8 + r);
-                    xi[r] = q.x;
-                    xi[r + 1] = q.y;
-                }
-#pragma unroll
-                for (int r = 0; r < 8; ++r)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[r][c] = fma(xi[r], xv[c], acc[r][c]);
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int ii = ty * 8 + r;
-            const int64_t i = rb * RBM + ii;
-            if (i >= p.Ns) continue;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int64_t j = cb * RBN + tx * 4 + c;
-                if (j >= p.N || p.row0 + i == j) continue;
-                const double R = yj[tx * 4 + c] + ab[ii] - acc[r][c];   // y_j - y_i + a_i - xi_i . x_j
-                gap += (double)Th[theta_off(i, j, p.ldT, p.tiled, p.nCBt)] * R;
-                if (R < 0.0) { v2 += R * R; vmax = fmax(vmax, -R); }
-            }
-        }
-    }
-    red[0][threadIdx.x] = gap; red[1][threadIdx.x] = v2; red[2][threadIdx.x] = vmax;
-    __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if ((int)threadIdx.x < s) {
-            red[0][threadIdx.x] += red[0][threadIdx.x + s];
-            red[1][threadIdx.x] += red[1][threadIdx.x + s];
-            red[2][threadIdx.x] = fmax(red[2][threadIdx.x], red[2][threadIdx.x + s]);
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        p.statpart[blockIdx.x * 8 + 4] = red[0][0];
-        p.statpart[blockIdx.x * 8 + 5] = red[1][0];
-        p.statpart[blockIdx.x * 8 + 6] = red[2][0];
-        p.statpart[blockIdx.x * 8 + 7] = (isfinite(red[0][0]) && isfinite(red[1][0])) ? 0.0 : 1.0;
     }
 }
 
@@ -736,7 +769,7 @@ cudaError_t launch_p2p_ygather(const P2PYGather &g, int fp64, cudaStream_t s) {
 
 cudaError_t p2p_selftest_y(int W, int64_t N, const float *y, float *out, cudaStream_t s) {
     if (W < 1 || W > kP2PTab || N < 1) return cudaErrorInvalidValue;
-    const int64_t S = (N + W - 1) / W, nbp = (S + 255) / 256;
+    const int64_t S = shard_rows(N, W, 1), nbp = (S + 255) / 256;
     char *buf = nullptr;
     const size_t yb = (sizeof(float) * (size_t)N + 255) / 256 * 256, fb = sizeof(unsigned long long) * (size_t)W;
     const size_t per = (yb + fb + 255) / 256 * 256;     // y' receive, then the (8-B aligned) flags
@@ -777,7 +810,7 @@ cudaError_t launch_p2p_gather(const P2PGather &g, cudaStream_t s) {
 
 cudaError_t p2p_selftest(int W, int64_t N, int nRB, const float *colpart, int64_t ldT, double *c, cudaStream_t s) {
     if (W < 1 || W > kP2PMaxWorld || N < 1) return cudaErrorInvalidValue;
-    const int64_t S = (N + W - 1) / W;
+    const int64_t S = shard_rows(N, W, 1);
     if (S % 128) return cudaErrorInvalidValue;                 // column blocks may not straddle owners
     const int64_t ncolb = (N + 127) / 128;
     // per virtual rank: a receive slab [W][S] + flags [W] + epoch, one allocation
@@ -828,6 +861,23 @@ cudaError_t launch_reduce(const ReduceParams &p, int fp64, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+cudaError_t launch_reduce_prologue(const ReduceParams &rd, const SmallParams &pr, cudaStream_t s) {
+    if (!rd.advance_t || rd.p2p_recv || pr.p2p_push || pr.statpart || pr.s_dev || pr.from_eta || !pr.use_beta)
+        return cudaErrorInvalidValue;
+    // 32 rows per block once that still gives >= 4 blocks per SM-sized wave (148 SMs), else 8
+    int rpb = pr.Ns >= 32 * 4 * 148 ? 32 : 8;
+    if (const char *e = std::getenv("CR_FUSE_RPB")) rpb = std::atoi(e) == 32 ? 32 : 8;
+    const unsigned nb = (unsigned)std::max<int64_t>(1, (pr.Ns + rpb - 1) / rpb);
+    const int q = (pr.n + 31) / 32;
+#define CR_RP(Q) (rpb == 32 ? pdl_launch(reduce_prologue_kernel<Q, 32>, dim3(nb), dim3(256), 0, s, rd, pr) \
+                            : pdl_launch(reduce_prologue_kernel<Q, 8>, dim3(nb), dim3(256), 0, s, rd, pr))
+    if (q <= 1) return CR_RP(1);
+    if (q == 2) return CR_RP(2);
+    if (q == 3) return CR_RP(3);
+#undef CR_RP
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_adapt_check(const AdaptParams &p, cudaStream_t s) {
     int64_t nb = (p.Ns + 7) / 8;
     if (nb < 1) nb = 1;
@@ -842,24 +892,6 @@ cudaError_t launch_adapt_decide(DevScalars *ts, unsigned long long cond, int has
     return cudaGetLastError();
 }
 
-cudaError_t launch_residual(const ResidualParams &p, int fp64, cudaStream_t s, int *nb_out) {
-    const int64_t nrb = (p.Ns + 63) / 64, ncb = (p.N + 127) / 128;
-    int64_t tiles = nrb * ncb;
-    int nb = (int)(tiles < kStatBlocks ? (tiles > 0 ? tiles : 1) : kStatBlocks);
-    const size_t smem = sizeof(double) * ((size_t)kRDC * 128 + 64 * (size_t)kRDC + 64 + 128);
-    cudaError_t e;
-    if (fp64) {
-        e = cudaFuncSetAttribute(residual_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        residual_kernel<double><<<nb, 256, smem, s>>>(p);
-    } else {
-        e = cudaFuncSetAttribute(residual_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        residual_kernel<float><<<nb, 256, smem, s>>>(p);
-    }
-    if (nb_out) *nb_out = nb;
-    return cudaGetLastError();
-}
 
 cudaError_t launch_stats_finalize(const double *pro, int nb_pro, const double *res, int nb_res,
                                   DevScalars *ts, cudaStream_t s) {

@@ -73,3 +73,29 @@ def test_init_rejects_bad_problems(crp):
     with pytest.raises(crp.CrError):
         crp.Solver(X, ybar, 1e-3, prec="fp64", kernel="tc")   # tcgen05 pass is fp32 only
     assert lib.cr_init(None, C.byref(C.c_void_p())) == crp.binding.CR_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("path", ["graph", "host_step", "graph_with_stop"])
+def test_exhausted_adaptive_trials_poison_the_context(crp, path):
+    """an adaptive iteration whose trials l = 0..63 all fail Eq. (adaptive-check)
+     leaves no valid iterate (t_k not advanced, the spare buffer holds a rejected trial):
+    the call returns CR_ERR_STATE and the context is poisoned -- every later call is refused, on
+    the CUDA-graph path (cr_solve, checked at its end or at its stop tests) and the host path
+    (cr_dual_step) alike.  Forced with s_prev far below the curvature and upsilon close to 1, so
+    s_{k-1} upsilon^(l-1) never reaches the passing range in 64 trials."""
+    X, ybar = crdata.random_problem(300, 4, seed=52, fp32=True)
+    L = ref.lipschitz(X, 1e-3)
+    s = crp.Solver(X, ybar, 1e-3, L=L, adaptive=True)
+    s.set_step_rule("adaptive", 1.01, L * 1e-12)
+    with pytest.raises(crp.CrError, match="adaptive"):
+        if path == "graph":
+            s.solve(4)
+        elif path == "graph_with_stop":
+            s.solve(6, report_every=2)
+        else:
+            s.step()
+    with pytest.raises(crp.CrError):
+        s.step()
+    with pytest.raises(crp.CrError):
+        s.get_theta()
+    s.close()

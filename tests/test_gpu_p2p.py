@@ -45,7 +45,8 @@ def test_selftest_allgather_protocol(crp, W, N):
 
 def test_selftest_rejects_straddling_blocks(crp):
     with pytest.raises(crp.CrError):
-        crp.selftest_p2p(np.zeros((3, 2, 1000), dtype=np.float32))      # ceil(1000/3) % 128 != 0
+        crp.selftest_p2p(np.zeros((4, 2, 300), dtype=np.float32))       # S = ceil(300/4) = 75: padding to
+                                                                        # 128 would leave rank 3 no rows
 
 
 @pytest.mark.parametrize("N,n,prec,kernel", [(1024, 20, "fp32", "tc"), (512, 5, "fp32", "simt"),

@@ -102,7 +102,29 @@ def test_shard_ranges_cover_rows_once():
         for world in (1, 2, 3, 4, 8):
             rows = [shard_range(N, r, world) for r in range(world)]
             assert sum(k for _, k in rows) == N
-            assert all(rows[r][0] == min(N, r * (-(-N // world))) for r in range(world))
+            S = crp.binding.shard_rows(N, world)
+            assert all(rows[r][0] == min(N, r * S) for r in range(world))
+            assert all(rows[r][0] + rows[r][1] == rows[r + 1][0] for r in range(world - 1))
             # every rank gets a workspace (possibly for zero rows) and ranks never overlap
             for r in range(world):
                 assert crp.workspace_size(N, 5, rank=r, world=world) > 0
+
+
+def test_shard_rows_padded_to_column_blocks():
+    """cr_shard_rows (include/cr.h): with world > 1 the shard is ceil(N/world) rounded up to the
+    128-column block of the column-sum exchange whenever every rank keeps >= 1 row -- so the
+    peer-memory path (CR_FLAG_P2P) covers C3 (N = 4000) at 2/4/8 ranks; a partition keeps
+    ceil(N/world) (S % nbar == 0 is required instead); world 1 is the whole problem."""
+    import paper_1608_02227_b200 as crp
+    sr = crp.binding.shard_rows
+    for N in (4000, 16384, 65536):
+        for W in (2, 4, 8):
+            S = sr(N, W)
+            assert S % 128 == 0 and (W - 1) * S < N and S >= -(-N // W)
+    assert sr(4000, 8) == 512 and sr(4000, 4) == 1024 and sr(4000, 2) == 2048
+    assert sr(300, 4) == 75                      # padding would leave rank 3 without rows
+    assert sr(1000, 1) == 1000 and sr(4000, 4, 100) == 1000
+    for N in range(2, 700, 7):
+        for W in (2, 3, 5, 8):
+            S = sr(N, W)
+            assert S >= -(-N // W) and (W - 1) * S < N or S == -(-N // W)

@@ -113,10 +113,10 @@ def gpu_leg(cfg, K):
         "fp32_storage_floor": floor,
         "oracle_seconds": float(d["seconds"]), "oracle_threads": int(d["threads"]),
     }
-    os.makedirs(OUT, exist_ok=True)
-    path = os.path.join(OUT, f"parity_{cfg.name}_K{K}.json")
-    with open(path, "w") as f:
-        json.dump(out, f, indent=1)
+    for od in (OUT, os.path.join(ROOT, "gpurun_out")):    # (gpurun_out: merged back from a GPU box)
+        os.makedirs(od, exist_ok=True)
+        with open(os.path.join(od, f"parity_{cfg.name}_K{K}.json"), "w") as f:
+            json.dump(out, f, indent=1)
     print(json.dumps(out), flush=True)
     return out
 
