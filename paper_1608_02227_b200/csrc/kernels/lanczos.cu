@@ -226,15 +226,32 @@ __global__ void lz_shift_kernel(double *v, double *vprev, const double *w, int64
     }
 }
 
+// Start vector on the device: the host Lanczos's splitmix64 sequence (value i = mix(seed + (i+1)
+// golden), counter-based, so every entry is computed independently), then unit-normalized with
+// the fixed-order device reductions (the norm's summation order differs from the host loop's, so
+// L agrees with the host Lanczos to rounding, not bit for bit).  Generating and copying the 5.3M
+// entries of C5's start vector on the host cost ~25 ms of cr_init.
+__global__ void lz_start_kernel(double *v, int64_t m, uint64_t seed) {
+    for (int64_t i = (int64_t)blockIdx.x * LB + threadIdx.x; i < m; i += (int64_t)gridDim.x * LB) {
+        uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        v[i] = (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    }
+}
+__global__ void lz_scale_kernel(double *v, int64_t m, const double *nrm) {
+    const double inv = 1.0 / *nrm;
+    for (int64_t i = (int64_t)blockIdx.x * LB + threadIdx.x; i < m; i += (int64_t)gridDim.x * LB) v[i] *= inv;
+}
+
 }  // namespace
 
 // sigma_max(C)^2 by device Lanczos.  X: device [N][n] fp64.  Scratch is stream-ordered
-// (cudaMallocAsync).  start: host start vector of length N (n + 1), unit norm.  Returns < 0 on
+// (cudaMallocAsync).  The start vector is generated on the device (lz_start_kernel).  Returns < 0 on
 // a CUDA error (then *err holds it).
 double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol, int max_iter, cudaStream_t st,
                                    cudaError_t *err, void *scratch, size_t scratch_bytes) {
-    std::vector<double> start((size_t)N * (n + 1));
-    lanczos_start(N, n, start.data());
     const int64_t m = N * (int64_t)(n + 1);
     const int nbk = (int)((N + LROWS - 1) / LROWS);           // lz_sums blocks
     const int nba = (int)((N + (int64_t)LW * LR - 1) / ((int64_t)LW * LR));   // lz_apply blocks (warp per LR rows)
@@ -273,7 +290,10 @@ double sigma_max_sq_lanczos_device(int64_t N, int n, const double *X, double tol
         vp = v + m;
         w = vp + m;
         double *al_d = ab, *be_d = ab + itmax, *zero_d = ab + 2 * itmax;
-        ok(cudaMemcpyAsync(v, start.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
+        lz_start_kernel<<<nbv, LB, 0, st>>>(v, m, 0x1608022270000001ull);
+        lz_dot_kernel<<<nbv, LB, 0, st>>>(v, v, m, part);
+        lz_final_kernel<<<1, LB, 0, st>>>(part, nbv, tot, 1);
+        lz_scale_kernel<<<nbv, LB, 0, st>>>(v, m, tot);
         ok(cudaMemsetAsync(vp, 0, sizeof(double) * m, st));
         ok(cudaMemsetAsync(zero_d, 0, sizeof(double), st));
         lz_gram_kernel<<<n * (n + 1), LB, 0, st>>>(X, N, n, S2, s);

@@ -11,10 +11,9 @@
 //     32 x 32 block of 4 x 4 fp64 tensor-core tiles (mma.sync m8n8k4 .f64: 256 FMA per
 //     instruction).  A CUDA-core DFMA version (8 x 8 or 4 x 8 register tiles) left the fp64 pipe
 //     41% busy with "wait" (fixed-latency issue) the top stall: the issue rate, not the pipe,
-//     was the limit.  Operand rows are padded to 132 doubles so the 4 k-rows a fragment load
-//     touches fall in different banks.
+//     was the limit.  Operand rows are padded (LDK) so a fragment load is conflict-free.
 //   * Both operands k-major in global memory (X^T prepared once in cr_init, Xi^T by a transpose
-//     before the pass), moved in chunks of 8 features by cp.async into a 3-stage shared ring; the
+//     before the pass), moved in chunks of KC features by cp.async into a shared ring; the
 //     chunk sequence runs across tiles, so the next tile's first chunks load under this tile's
 //     last ones.  Features beyond n are zero-filled (cp.async src-size 0).
 //   * Theta (fp32) for the tile is staged into a double-buffered shared image together with the
@@ -30,9 +29,17 @@
 namespace cr {
 namespace {
 
-constexpr int RBM = 128, RBN = 128, RTH = 512, KC = 8, STAGES = 3, LDK = 132;
-constexpr int A_BYTES = KC * LDK * 8, B_BYTES = KC * LDK * 8;      // 8.25 KB each (padded rows)
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+// KC = 16 features per chunk with a 2-stage ring (one barrier per 16 features: ncu showed the
+// per-chunk barrier as the third stall at KC = 8); rows padded to 136 doubles so a fragment
+// load's four k-rows fall in bank halves {0, 1} / {2, 3} (two wavefronts, the minimum for 256 B)
+// (KC = 8 with 3 stages when n is not a multiple of 16: C4's n = 40 would otherwise run 20% zero
+// features)
+constexpr int RBM = 128, RBN = 128, RTH = 512, LDK = 136;
+template <int KC> struct ResCfg {
+    static constexpr int STAGES = KC == 16 ? 2 : 3;
+    static constexpr int A_BYTES = KC * LDK * 8, B_BYTES = KC * LDK * 8;   // padded rows
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+};
 constexpr int TH_BYTES = RBM * RBN * 4;                              // fp32 Theta tile, 64 KB
 constexpr int VEC_BYTES = 3 * 128 * 8;                               // y_j, a_i, y_i
 constexpr int TBUF_BYTES = TH_BYTES + VEC_BYTES;
@@ -51,8 +58,9 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <typename T>
+template <typename T, int KC>
 __global__ void __launch_bounds__(RTH, 1) residual2_kernel(const ResidualParams p) {
+    constexpr int STAGES = ResCfg<KC>::STAGES, A_BYTES = ResCfg<KC>::A_BYTES, STAGE_BYTES = ResCfg<KC>::STAGE_BYTES;
     extern __shared__ __align__(16) uint8_t rsm[];
     uint8_t *stages = rsm;                                   // [STAGES][A | B]
     uint8_t *tbuf = rsm + STAGES * STAGE_BYTES;              // [2][Theta tile | y_j | a_i | y_i]
@@ -88,8 +96,8 @@ __global__ void __launch_bounds__(RTH, 1) residual2_kernel(const ResidualParams 
             double *As = reinterpret_cast<double *>(st), *Bs = reinterpret_cast<double *>(st + A_BYTES);
             // A: Xi^T rows k0..k0+7, columns i0..i0+127 (8 x 1 KB); B: X^T, columns j0..
 #pragma unroll
-            for (int e = 0; e < 512 / RTH; ++e) {
-                const int f = tid + e * RTH;                // 512 pieces of 16 B per operand
+            for (int e = 0; e < KC * 64 / RTH; ++e) {
+                const int f = tid + e * RTH;                // KC x 64 pieces of 16 B per operand
                 const int kk = f >> 6, q = f & 63;
                 const int k = c.kc * KC + kk;
                 const bool ok = k < p.nP;
@@ -241,7 +249,10 @@ __global__ void transpose_pad_kernel(const double *src, int64_t rows, int n, int
 
 }  // namespace
 
-size_t residual_smem_bytes() { return (size_t)STAGES * STAGE_BYTES + 2 * (size_t)TBUF_BYTES; }
+size_t residual_smem_bytes() {
+    const size_t a = (size_t)ResCfg<16>::STAGES * ResCfg<16>::STAGE_BYTES, b = (size_t)ResCfg<8>::STAGES * ResCfg<8>::STAGE_BYTES;
+    return (a > b ? a : b) + 2 * (size_t)TBUF_BYTES;
+}
 
 cudaError_t launch_transpose_pad(const double *src, int64_t rows, int n, int nP, int64_t ld, double *dst,
                                  cudaStream_t s) {
@@ -262,15 +273,19 @@ cudaError_t launch_residual(const ResidualParams &p, int fp64, cudaStream_t s, i
     const int cap = sms < kStatBlocks ? sms : kStatBlocks;
     const int nb = (int)(ntiles < cap ? (ntiles > 0 ? ntiles : 1) : cap);
     const int smem = (int)residual_smem_bytes();
+    const bool k16 = p.nP % 16 == 0;
+#define CR_RES(T, K)                                                                                 \
+    do {                                                                                             \
+        e = cudaFuncSetAttribute(residual2_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        if (e != cudaSuccess) return e;                                                              \
+        residual2_kernel<T, K><<<nb, RTH, smem, s>>>(p);                                             \
+    } while (0)
     if (fp64) {
-        e = cudaFuncSetAttribute(residual2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        residual2_kernel<double><<<nb, RTH, smem, s>>>(p);
+        if (k16) CR_RES(double, 16); else CR_RES(double, 8);
     } else {
-        e = cudaFuncSetAttribute(residual2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        residual2_kernel<float><<<nb, RTH, smem, s>>>(p);
+        if (k16) CR_RES(float, 16); else CR_RES(float, 8);
     }
+#undef CR_RES
     if (nb_out) *nb_out = nb;
     return cudaGetLastError();
 }
