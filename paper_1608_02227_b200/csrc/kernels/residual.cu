@@ -7,19 +7,19 @@
 // violation is a small difference of O(|xi||x|) terms).  The pass is an fp64 rank-n contraction
 // S = Xi X^T with a reduction epilogue: N^2 n DFMA against one 4-byte read of Theta per pair, so it
 // is bound by the fp64 FMA pipe (64 DFMA / clk / SM), not by HBM.  Layout for that bound:
-//   * CTA tile 128 rows (i) x 128 columns (j), 512 threads = 16 warps in a 4 x 4 grid, each warp a
-//     32 x 32 block of 4 x 4 fp64 tensor-core tiles (mma.sync m8n8k4 .f64: 256 FMA per
+//   * CTA tile 128 rows (i) x 64 columns (j), 256 threads = 8 warps in a 4 x 2 grid, 2 CTAs per SM,
+//     each warp a 32 x 32 block of 4 x 4 fp64 tensor-core tiles (mma.sync m8n8k4 .f64: 256 FMA per
 //     instruction).  A CUDA-core DFMA version (8 x 8 or 4 x 8 register tiles) left the fp64 pipe
 //     41% busy with "wait" (fixed-latency issue) the top stall: the issue rate, not the pipe,
-//     was the limit.  Operand rows are padded (LDK) so a fragment load is conflict-free.
+//     was the limit.  Operand rows are padded (LDA, LDB) so a fragment load is conflict-free.
 //   * Both operands k-major in global memory (X^T prepared once in cr_init, Xi^T by a transpose
 //     before the pass), moved in chunks of KC features by cp.async into a shared ring; the
 //     chunk sequence runs across tiles, so the next tile's first chunks load under this tile's
 //     last ones.  Features beyond n are zero-filled (cp.async src-size 0).
-//   * Theta (fp32) for the tile is staged into a double-buffered shared image together with the
-//     tile's first chunk (16 KB bulk per 128 x 32 tile-major tile, or 128 row segments of 512 B),
-//     so its HBM latency overlaps the previous tile's contraction; fp64 Theta (small problems) is
-//     read from global memory in the epilogue.
+//   * Theta (fp32) for the tile is staged into a shared image together with the tile's second
+//     chunk (16 KB per 128 x 32 tile-major tile, or 128 row segments of 256 B), so its HBM
+//     latency overlaps the tile's remaining chunks; fp64 Theta (small problems) is read from
+//     global memory in the epilogue.
 //   * Persistent CTAs (one per SM) walk tiles blockIdx.x, +gridDim.x, ... in a fixed order; the
 //     per-thread sums and the final block tree are fixed-order, so results are bitwise repeatable.
 #include <cuda_runtime.h>
@@ -34,14 +34,17 @@ namespace {
 // load's four k-rows fall in bank halves {0, 1} / {2, 3} (two wavefronts, the minimum for 256 B)
 // (KC = 8 with 3 stages when n is not a multiple of 16: C4's n = 40 would otherwise run 20% zero
 // features)
-constexpr int RBM = 128, RBN = 128, RTH = 512, LDK = 136;
+// Two CTAs of 8 warps per SM, CTA tile 128 x 64: one CTA's epilogue and barriers overlap the
+// other's tensor work (with one 16-warp CTA per SM every warp reached the epilogue and every
+// chunk barrier together).  Operand rows padded: LDA = 136, LDB = 72 doubles.
+constexpr int RBM = 128, RBN = 64, RTH = 256, LDA = 136, LDB = 72;
 template <int KC> struct ResCfg {
     static constexpr int STAGES = KC == 16 ? 2 : 3;
-    static constexpr int A_BYTES = KC * LDK * 8, B_BYTES = KC * LDK * 8;   // padded rows
+    static constexpr int A_BYTES = KC * LDA * 8, B_BYTES = KC * LDB * 8;   // padded rows
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 };
-constexpr int TH_BYTES = RBM * RBN * 4;                              // fp32 Theta tile, 64 KB
-constexpr int VEC_BYTES = 3 * 128 * 8;                               // y_j, a_i, y_i
+constexpr int TH_BYTES = RBM * RBN * 4;                              // fp32 Theta tile, 32 KB
+constexpr int VEC_BYTES = (RBN + 2 * RBM) * 8;                       // y_j, a_i, y_i
 constexpr int TBUF_BYTES = TH_BYTES + VEC_BYTES;
 
 __device__ __forceinline__ void cp16(void *smem, const void *gmem, bool valid) {
@@ -59,21 +62,24 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <typename T, int KC>
-__global__ void __launch_bounds__(RTH, 1) residual2_kernel(const ResidualParams p) {
+__global__ void __launch_bounds__(RTH, 2) residual2_kernel(const ResidualParams p) {
     constexpr int STAGES = ResCfg<KC>::STAGES, A_BYTES = ResCfg<KC>::A_BYTES, STAGE_BYTES = ResCfg<KC>::STAGE_BYTES;
     extern __shared__ __align__(16) uint8_t rsm[];
     uint8_t *stages = rsm;                                   // [STAGES][A | B]
-    uint8_t *tbuf = rsm + STAGES * STAGE_BYTES;              // [2][Theta tile | y_j | a_i | y_i]
+    uint8_t *tbuf = rsm + STAGES * STAGE_BYTES;              // Theta tile | y_j | a_i | y_i (one buffer)
     __shared__ double red[3][RTH];
 
     const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31, wr = warp >> 2, wc = warp & 3;   // warp block (wr, wc)
+    const int warp = tid >> 5, lane = tid & 31, wr = warp >> 1, wc = warp & 1;   // warp block (wr, wc): 4 x 2
     const int fg = lane >> 2, ft = lane & 3;                    // mma fragment group / thread in group
     const int nrb = (int)((p.Ns + RBM - 1) / RBM), ncb = (int)((p.N + RBN - 1) / RBN);
     const int ntiles = nrb * ncb;                             // < 2^31 (N <= 2^22 rows / columns)
     const int G = gridDim.x;
     const int my = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / G + 1 : 0;   // tiles of this CTA
-    const int nCk = max((p.nP + KC - 1) / KC, STAGES - 1);   // chunks per tile (zero chunks pad small n)
+    // chunks per tile (zero chunks pad small n); the tile's Theta is staged with chunk STAGES - 1,
+    // the first one issued after the previous tile's epilogue has passed its barrier
+    constexpr int KTH = STAGES - 1;
+    const int nCk = max((p.nP + KC - 1) / KC, KTH + 1);
     const bool stage_theta = sizeof(T) == 4;
 
     // Loads of one chunk (tile it of this CTA at (rb, cb), feature chunk kc) into ring stage st;
@@ -94,50 +100,60 @@ __global__ void __launch_bounds__(RTH, 1) residual2_kernel(const ResidualParams 
             const int64_t i0 = (int64_t)c.rb * RBM, j0 = (int64_t)c.cb * RBN;
             uint8_t *st = stages + c.st * STAGE_BYTES;
             double *As = reinterpret_cast<double *>(st), *Bs = reinterpret_cast<double *>(st + A_BYTES);
-            // A: Xi^T rows k0..k0+7, columns i0..i0+127 (8 x 1 KB); B: X^T, columns j0..
+            // A: Xi^T rows k0.., columns i0..i0+127 (KC x 1 KB); B: X^T, columns j0..j0+63 (KC x 512 B)
 #pragma unroll
             for (int e = 0; e < KC * 64 / RTH; ++e) {
-                const int f = tid + e * RTH;                // KC x 64 pieces of 16 B per operand
+                const int f = tid + e * RTH;                // KC x 64 pieces of 16 B
                 const int kk = f >> 6, q = f & 63;
                 const int k = c.kc * KC + kk;
                 const bool ok = k < p.nP;
-                cp16(As + kk * LDK + q * 2, p.XiT + (ok ? (int64_t)k * p.Rp + i0 + q * 2 : 0), ok);
-                cp16(Bs + kk * LDK + q * 2, p.XT + (ok ? (int64_t)k * p.ldX + j0 + q * 2 : 0), ok);
+                cp16(As + kk * LDA + q * 2, p.XiT + (ok ? (int64_t)k * p.Rp + i0 + q * 2 : 0), ok);
             }
-            if (c.kc == 0) {
-                uint8_t *tb = tbuf + (c.it & 1) * TBUF_BYTES;
+#pragma unroll
+            for (int e = 0; e < KC * 32 / RTH; ++e) {
+                const int f = tid + e * RTH;                // KC x 32 pieces of 16 B
+                const int kk = f >> 5, q = f & 31;
+                const int k = c.kc * KC + kk;
+                const bool ok = k < p.nP;
+                cp16(Bs + kk * LDB + q * 2, p.XT + (ok ? (int64_t)k * p.ldX + j0 + q * 2 : 0), ok);
+            }
+            if (c.kc == KTH) {
+                // the tile's Theta and vectors into the single tile buffer: chunk KTH is issued
+                // in iteration (tile start), after the barrier that follows the previous tile's
+                // epilogue; consumed after chunk nCk - 1 >= KTH
+                uint8_t *tb = tbuf;
                 if (stage_theta) {
                     const float *Th = static_cast<const float *>(p.Theta);
                     if (p.tiled) {
-                        // four 128 x 32 tiles of 16 KB (tile-major, swizzled image kept as is)
+                        // two 128 x 32 tiles of 16 KB (tile-major, swizzled image kept as is)
                         const int64_t tbase = ((i0 >> 7) * p.nCBt) << 12;
 #pragma unroll
-                        for (int e = 0; e < 4096 / RTH; ++e) {
-                            const int f = tid + e * RTH;    // 4096 pieces
+                        for (int e = 0; e < 2048 / RTH; ++e) {
+                            const int f = tid + e * RTH;    // 2048 pieces
                             const int q = f >> 10, w = f & 1023;
-                            const int tcb = c.cb * 4 + q;
+                            const int tcb = c.cb * 2 + q;
                             const bool ok = tcb < p.nCBt;
                             const float *src = Th + (ok ? tbase + ((int64_t)tcb << 12) + w * 4 : 0);
                             cp16(tb + q * 16384 + w * 16, src, ok);
                         }
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 4096 / RTH; ++e) {
-                            const int f = tid + e * RTH;    // 128 rows x 32 pieces
-                            const int r = f >> 5, w = f & 31;
-                            cp16(tb + r * 512 + w * 16, Th + (i0 + r) * p.ldT + j0 + w * 4, true);
+                        for (int e = 0; e < 2048 / RTH; ++e) {
+                            const int f = tid + e * RTH;    // 128 rows x 16 pieces
+                            const int r = f >> 4, w = f & 15;
+                            cp16(tb + r * 256 + w * 16, Th + (i0 + r) * p.ldT + j0 + w * 4, true);
                         }
                     }
                 }
                 double *v = reinterpret_cast<double *>(tb + TH_BYTES);
-                if (tid < 128) {
+                if (tid < RBN) {
                     const int64_t j = j0 + tid;
                     cp8(v + tid, p.y64 + (j < p.N ? j : 0), j < p.N);
-                } else if (tid < 256) {
-                    const int e = tid - 128;
-                    const int64_t i = i0 + e;
-                    cp8(v + 128 + e, p.a64 + (i < p.Ns ? i : 0), i < p.Ns);
-                    cp8(v + 256 + e, p.y64 + (i < p.Ns ? p.row0 + i : 0), i < p.Ns);
+                }
+                if (tid < RBM) {
+                    const int64_t i = i0 + tid;
+                    cp8(v + RBN + tid, p.a64 + (i < p.Ns ? i : 0), i < p.Ns);
+                    cp8(v + RBN + RBM + tid, p.y64 + (i < p.Ns ? p.row0 + i : 0), i < p.Ns);
                 }
             }
         }
@@ -162,15 +178,15 @@ __global__ void __launch_bounds__(RTH, 1) residual2_kernel(const ResidualParams 
         advance(ci);
         const uint8_t *st = stages + cc.st * STAGE_BYTES;
         // fragments (m8n8k4, .row A / .col B): A[fg][ft] = Xi_{i0+fg}[k0+ft], B[ft][fg] = x_{j0+fg}[k0+ft]
-        const double *As = reinterpret_cast<const double *>(st) + ft * LDK + wr * 32 + fg;
-        const double *Bs = reinterpret_cast<const double *>(st + A_BYTES) + ft * LDK + wc * 32 + fg;
+        const double *As = reinterpret_cast<const double *>(st) + ft * LDA + wr * 32 + fg;
+        const double *Bs = reinterpret_cast<const double *>(st + A_BYTES) + ft * LDB + wc * 32 + fg;
 #pragma unroll
         for (int k4 = 0; k4 < KC / 4; ++k4) {
             double a[4], b[4];
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) a[mt] = As[k4 * 4 * LDK + mt * 8];
+            for (int mt = 0; mt < 4; ++mt) a[mt] = As[k4 * 4 * LDA + mt * 8];
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) b[nt] = Bs[k4 * 4 * LDK + nt * 8];
+            for (int nt = 0; nt < 4; ++nt) b[nt] = Bs[k4 * 4 * LDB + nt * 8];
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -183,7 +199,7 @@ __global__ void __launch_bounds__(RTH, 1) residual2_kernel(const ResidualParams 
             // ---- epilogue of the tile: R = (y_j + (a_i - y_i)) - xi_i . x_j over the thread's 32 pairs
             // (accumulator [mt][nt][c] = pair (wr*32 + mt*8 + fg, wc*32 + nt*8 + 2 ft + c))
             const int64_t i0 = (int64_t)cc.rb * RBM, j0 = (int64_t)cc.cb * RBN;
-            const uint8_t *tb = tbuf + (cc.it & 1) * TBUF_BYTES;
+            const uint8_t *tb = tbuf;
             const double *v = reinterpret_cast<const double *>(tb + TH_BYTES);
             const float *Ts = reinterpret_cast<const float *>(tb);
 #pragma unroll
@@ -191,7 +207,7 @@ __global__ void __launch_bounds__(RTH, 1) residual2_kernel(const ResidualParams 
                 const int il = wr * 32 + mt * 8 + fg;
                 const int64_t i = i0 + il;
                 if (i >= p.Ns) continue;
-                const double ab = v[128 + il] - v[256 + il];
+                const double ab = v[RBN + il] - v[RBN + RBM + il];
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) {
 #pragma unroll
@@ -204,7 +220,7 @@ __global__ void __launch_bounds__(RTH, 1) residual2_kernel(const ResidualParams 
                         double th;
                         if (stage_theta) {
                             th = p.tiled ? (double)Ts[wc * 4096 + il * 32 + (((jj >> 2) ^ (il & 7)) << 2) + (jj & 3)]
-                                         : (double)Ts[il * 128 + jl];
+                                         : (double)Ts[il * RBN + jl];
                         } else {
                             th = (double)static_cast<const T *>(p.Theta)[theta_off(i, j, p.ldT, p.tiled, p.nCBt)];
                         }
@@ -251,7 +267,7 @@ __global__ void transpose_pad_kernel(const double *src, int64_t rows, int n, int
 
 size_t residual_smem_bytes() {
     const size_t a = (size_t)ResCfg<16>::STAGES * ResCfg<16>::STAGE_BYTES, b = (size_t)ResCfg<8>::STAGES * ResCfg<8>::STAGE_BYTES;
-    return (a > b ? a : b) + 2 * (size_t)TBUF_BYTES;
+    return (a > b ? a : b) + (size_t)TBUF_BYTES;
 }
 
 cudaError_t launch_transpose_pad(const double *src, int64_t rows, int n, int nP, int64_t ld, double *dst,
@@ -270,7 +286,7 @@ cudaError_t launch_residual(const ResidualParams &p, int fp64, cudaStream_t s, i
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int cap = sms < kStatBlocks ? sms : kStatBlocks;
+    const int cap = 2 * sms < kStatBlocks ? 2 * sms : kStatBlocks;   // two CTAs per SM
     const int nb = (int)(ntiles < cap ? (ntiles > 0 ? ntiles : 1) : cap);
     const int smem = (int)residual_smem_bytes();
     const bool k16 = p.nP % 16 == 0;
