@@ -334,7 +334,8 @@ def full_size_beta_step(crp, cfg_name, row_blocks=None):
     whose extrapolation weight beta_2 = (t_2 - 1)/t_3 = 0.28 makes GEMM1 (Xi' X^T) and GEMM2
     (Theta^k X, the A2^T theta sums of Def. A1A2 P:103-128 feeding Step 1 P:386) both non-trivial.
     Compared: Theta^3 (all rows, or `row_blocks` = [(row0, nrows)] at C5) and eta^3 = (y, xi)
-    of Step 1 at theta~^3 on all rows.  No oracle input comes from the GPU."""
+    of Step 1 at theta~^3 on all rows; then Theta^4 and eta^4, whose Step 1 uses the sums the
+    fused pass accumulated for Theta^3 (GEMM2).  No oracle input comes from the GPU."""
     cfg = crdata.CONFIGS[cfg_name]
     X, ybar = crdata.make_problem(cfg)
     N = cfg.N
@@ -358,37 +359,52 @@ def full_size_beta_step(crp, cfg_name, row_blocks=None):
         Pa = P[a:a + 1024]
         Q[a:a + 1024] = Pa + beta * (Pa - Q[a:a + 1024])
     o3 = oracle.papg(X, ybar, cfg.gamma, L, 1, Tprev=P, Tt=Q, t=t3, inplace=True)       # P = Theta^3
-    del Q
     s.step()
     y, xi = s.get_eta()
     out = dict(y=rel(y, o3["y"]), xi=rel(xi, o3["xi"]))
     assert out["y"] <= 1e-5 and out["xi"] <= 1e-5, out
-    if row_blocks is None:
-        Tg = s.get_theta()[0]
-        Tw = P
-    else:
-        Tg = np.concatenate([s.get_theta_rows(0, int(r0), int(nr)) for r0, nr in row_blocks])
-        Tw = np.concatenate([P[r0:r0 + nr] for r0, nr in row_blocks])
+
+    def rows_of(T_gpu_fn, T_host):
+        if row_blocks is None:
+            return T_gpu_fn(), T_host
+        return (np.concatenate([s.get_theta_rows(0, int(r0), int(nr)) for r0, nr in row_blocks]),
+                np.concatenate([T_host[r0:r0 + nr] for r0, nr in row_blocks]))
+
+    Tg, Tw = rows_of(lambda: s.get_theta()[0], P)
     out["theta"] = rel(Tg, Tw)
     out["rows"] = Tg.shape[0]
     assert np.all(Tg >= 0)
     assert out["theta"] <= 1e-5, out
     out["elementwise"] = elementwise(Tg, Tw, 1e-5)
+    del Tg, Tw
+    # iteration 4: its Step 1 uses the sums of Theta^3 that the fused pass itself accumulated (r, c
+    # on the CUDA cores, Theta X = A2^T theta on the tensor cores, GEMM2) -- the step above took its
+    # Step 1 from the sums cr_set_theta computed -- so eta^4 checks GEMM2 at full size.  The oracle
+    # continues from its own Theta^3 (one fp32 rounding apart, ~5e-8).
+    o4 = oracle.papg(X, ybar, cfg.gamma, L, 1, Tprev=P, Tt=Q, t=o3["t"], inplace=True)  # P = Theta^4
+    del Q
+    s.step()
+    y4, xi4 = s.get_eta()
+    out["y4"], out["xi4"] = rel(y4, o4["y"]), rel(xi4, o4["xi"])
+    assert out["y4"] <= 1e-5 and out["xi4"] <= 1e-5, out
+    Tg, Tw = rows_of(lambda: s.get_theta()[0], P)
+    out["theta4"] = rel(Tg, Tw)
+    assert out["theta4"] <= 1e-5, out
     s.close()
     return out
 
 
 def test_full_size_C4_beta_step(crp):
-    """C4 at full size (N=16384, n=40): iteration 3 from the oracle's (Theta^2, Theta^1), every
-    row of Theta^3 plus y and Xi."""
+    """C4 at full size (N=16384, n=40): iterations 3 and 4 from the oracle's (Theta^2, Theta^1),
+    every row of Theta^3 / Theta^4 plus y and Xi of both steps."""
     print(full_size_beta_step(crp, "C4"))
 
 
 def test_full_size_C5_beta_step(crp):
     """C5 at full size (N=65536, n=80, 2 x 16 GiB of state on one GPU): iteration 3 from the
     oracle's (Theta^2, Theta^1); 4096 rows of Theta^3 (32 blocks of 128, tile-aligned and not,
-    spread over the matrix, both ends included) plus all of y and Xi -- GEMM2's Theta X at
-    n = 80 enters through Xi.  Needs ~100 GiB of host memory for the in-place fp64 oracle."""
+    spread over the matrix, both ends included) plus all of y and Xi; then iteration 4, whose Xi
+    comes from GEMM2's Theta X of Theta^3 at n = 80.  Needs ~100 GiB of host memory for the in-place fp64 oracle."""
     if _host_gib_available() < 110:
         pytest.skip(f"C5 oracle needs ~100 GiB of host RAM; {_host_gib_available():.0f} GiB available")
     N = 65536
