@@ -177,20 +177,6 @@ def test_K_iterations_C2_500(crp):
     k_iteration_case(crp, "C2", "fp32", K=500)
 
 
-def test_K_iterations_C2_full(crp):
-    """C2 after its full 2000 iterations.  Objective within 1e-4.  The max violation is bounded by
-    the fp32-storage floor (tests/numerics/fp32_storage_floor.py): rounding Theta to
-    fp32 once per iteration -- with every other operation exact -- already moves it by 1.6e-3 at
-    K = 2000, so the test uses 5e-3 for that quantity."""
-    k_iteration_case(crp, "C2", "fp32", tol_viol=5e-3)
-
-
-def test_K_iterations_C2_fp64_storage(crp):
-    """C2's problem with fp64 storage (prec='fp64'): 2000 iterations, both quantities within 1e-4
-    (the storage floor is gone, so the north star's tolerance applies unchanged)."""
-    k_iteration_case(crp, "C2", "fp64")
-
-
 def _storage_floor(cfg_name, K):
     """The fp32-storage floor of the max violation (tests/numerics/fp32_storage_floor.py, written
     by that script from oracle/ only; tests/golden/fp32_storage_floor.json)."""
@@ -201,6 +187,20 @@ def _storage_floor(cfg_name, K):
         if r["config"] == cfg_name and r["K"] == K and r["N"] == crdata.CONFIGS[cfg_name].N:
             return r["max_violation"]
     raise KeyError((cfg_name, K))
+
+
+def test_K_iterations_C2_full(crp):
+    """C2 after its full 2000 iterations.  Objective within 1e-4.  The max violation is bounded by
+    the fp32-storage floor (R24, tests/numerics/fp32_storage_floor.py): rounding Theta to
+    fp32 once per iteration -- with every other operation exact -- already moves it by 1.75e-3 at
+    K = 2000 (tests/golden/fp32_storage_floor.json), so the test uses max(1e-4, 3 x floor)."""
+    k_iteration_case(crp, "C2", "fp32", tol_viol=max(1e-4, 3.0 * _storage_floor("C2", 2000)))
+
+
+def test_K_iterations_C2_fp64_storage(crp):
+    """C2's problem with fp64 storage (prec='fp64'): 2000 iterations, both quantities within 1e-4
+    (the storage floor is gone, so the north star's tolerance applies unchanged)."""
+    k_iteration_case(crp, "C2", "fp64")
 
 
 def test_K_iterations_C3_full(crp):
