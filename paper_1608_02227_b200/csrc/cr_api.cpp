@@ -1247,6 +1247,12 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
             else --s1;
         }
         while (bytes() > budget && st > 2) --st;
+        // GEMM1 run-ahead drops the in-order guard GEMM1's own Theta wait gives the epilogue: an
+        // epilogue warpgroup at tile u then relies on its parity wait on slot u % S alone, and with
+        // an odd S the slot's previous tile u - S belongs to the OTHER warpgroup, which may still be
+        // pending -- the wait would match the phase of tile u - 2S and read a slot being refilled
+        // (the round-1 fault with 3 slots).  With S even the previous tile is the warpgroup's own.
+        if (ctx->g1_runahead && (st & 1)) --st;
         if (bytes() > budget) {
             fail(ctx, CR_ERR_UNSUPPORTED, "tc pass: smem");
             return bail(CR_ERR_UNSUPPORTED);
