@@ -187,13 +187,18 @@ __global__ void __launch_bounds__(RTH, 2) residual2_kernel(const ResidualParams 
             for (int mt = 0; mt < 4; ++mt) a[mt] = As[k4 * 4 * LDA + mt * 8];
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) b[nt] = Bs[k4 * 4 * LDB + nt * 8];
+            // m16n8k4 (sm_90+): rows fg and fg + 8 of a 16-row tile = the m8 sub-tiles 2 mp, 2 mp + 1
+            // (a0 = A[fg][ft], a1 = A[fg + 8][ft]; c0, c1 / c2, c3 = rows fg / fg + 8): half the
+            // instructions of m8n8k4 for the same fragments
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt)
+            for (int mp = 0; mp < 2; ++mp)
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt)
-                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                 : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
-                                 : "d"(a[mt]), "d"(b[nt]));
+                    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+                                 "{%0,%1,%2,%3};"
+                                 : "+d"(acc[2 * mp][nt][0]), "+d"(acc[2 * mp][nt][1]), "+d"(acc[2 * mp + 1][nt][0]),
+                                   "+d"(acc[2 * mp + 1][nt][1])
+                                 : "d"(a[2 * mp]), "d"(a[2 * mp + 1]), "d"(b[nt]));
         }
         if (cc.kc == nCk - 1) {
             // ---- epilogue of the tile: R = (y_j + (a_i - y_i)) - xi_i . x_j over the thread's 32 pairs
