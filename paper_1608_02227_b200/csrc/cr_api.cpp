@@ -1274,8 +1274,8 @@ cr_status cr_init(const cr_config *cfg, cr_ctx **out) {
         ctx->launches += 1;
     }
     if (std::getenv("CR_TC_TRACE")) {     // debug timelines (tcgen05 pass / resident solver)
-        IK(cudaMalloc(&ctx->trace, 5 * 256 * 8 * 8));
-        IK(cudaMemsetAsync(ctx->trace, 0, 5 * 256 * 8 * 8, ctx->stream));
+        IK(cudaMalloc(&ctx->trace, kTraceWords * 8));
+        IK(cudaMemsetAsync(ctx->trace, 0, kTraceWords * 8, ctx->stream));
     }
     if (Ly.resident) {
         // SMEM-resident solver geometry: enough CTAs that one iteration's N^2 n work is spread
@@ -1520,7 +1520,7 @@ cr_status cr_dual_step(cr_ctx *ctx, cr_step_stats *out) {
     const int bo = ctx->bB;
     if ((st = enqueue_step(ctx, true, bo, 1.0 / ctx->L, true, false)) != CR_OK) return st;
     if (ctx->trace) {   // debug: dump the tensor-core pass timeline of CTA 0
-        std::vector<unsigned long long> h(5 * 256 * 8);
+        std::vector<unsigned long long> h(kTraceWords);
         CK(cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         if (FILE *f = std::fopen(std::getenv("CR_TC_TRACE"), "wb")) {

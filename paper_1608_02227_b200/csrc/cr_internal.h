@@ -14,6 +14,9 @@ namespace cr {
 // the predecessor's outputs (griddepcontrol.wait: all prerequisite grids complete, memory
 // visible) and pdl_trigger() once its own dependents may launch.  CR_NO_PDL=1 disables it.
 bool pdl_enabled();
+// CR_TC_TRACE buffer: [5 roles][256 tiles][8 events] clock64 of CTA 0, then per CTA
+// [entry, predecessor complete, exit, tiles] (globaltimer ns)
+constexpr int kTraceTile = 5 * 256 * 8, kTraceWords = kTraceTile + 4 * 1024;
 #ifdef __CUDACC__
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -299,7 +302,7 @@ struct TcParams {
     float *colpart;                  // [nRB128][ldT]
     double *rowpart;                 // [slots][128][NP2 + 4]: Theta X | r (wg 0, 1) | ||D||^2 (wg 0, 1)
     const int *cta_slot0;
-    unsigned long long *trace;       // debug: clock64 timeline of CTA 0 (nullptr = off)
+    unsigned long long *trace;       // debug: clock64 timeline of CTA 0 + per-CTA globaltimer records (nullptr = off)
     int g1_runahead;                 // 1: GEMM1 does not wait for the tile's Theta (needs X_J, Xi' only)
     unsigned long long *check;       // CR_TC_CHECK: first ring-protocol violation (nullptr = checks off),
                                      // (code << 56) | (CTA << 32) | tile; see tc_check_code

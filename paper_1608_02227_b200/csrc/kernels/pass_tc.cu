@@ -13,10 +13,12 @@
 // no-swizzle ("interleave") tiles prepared once at init: X_J as [j][k] and X_J^T as [d][j]
 // core matrices (8 rows x 16 B), so each per-tile image is exactly 32 n fp32.  (MN-major
 // tf32 operands would need the SW128_32B layout; two K-major images avoid it.)
-// Theta^{k-1}, Theta^{k-2} tiles arrive by TMA (128B-swizzled 128x32 boxes); Theta^k leaves by
-// TMA store from the same smem slot.  The Theta X accumulator lives in TMEM and is flushed to
-// fp64 (global, per CTA run slot) every `window` tiles.
-// Warp roles: 0 = TMA producer, 1 = GEMM1 issuer (+ TMEM owner), 2 = TMA storer, 3 = GEMM2 issuer,
+// Theta is stored tile-major (each 128 x 32 tile 16 KB contiguous, already in the 128-B-swizzled
+// smem image): Theta^{k-1}, Theta^{k-2} tiles arrive by one 1-D bulk copy each
+// (cp.async.bulk), Theta^k leaves by a 1-D bulk store from the same smem slot.  The Theta X
+// accumulator lives in TMEM and is flushed to fp64 (global, per CTA run slot) every `window` tiles.
+// GEMM1 runs in kind::f16 (fp16 hi/lo with exact power-of-2 row scalings) for n > 56.
+// Warp roles: 0 = bulk-copy producer, 1 = GEMM1 issuer (+ TMEM owner), 2 = bulk storer, 3 = GEMM2 issuer,
 // 4..7 / 8..11 = two epilogue warpgroups that take alternate tiles (ping-pong).
 // Persistent: CTA g owns tiles [g T / G, (g+1) T / G) of the row-major (row block, column
 // tile) order, like the SIMT pass.
@@ -73,6 +75,30 @@ __device__ __forceinline__ void bfly(const float *v, float *o, int lane) {
         const float keep = up ? v[c + H] : v[c];
         o[c] = keep + __shfl_xor_sync(0xffffffffu, send, H);
     }
+}
+
+// 16 x 16 transpose inside each half-warp: lane l's v[c] <- lane (l & 16) + c's v[l & 15].  Four
+// butterfly stages, stage H swapping bit H between the lane and the register index where they
+// differ (the stages commute); register indices stay compile-time.
+__device__ __forceinline__ void transpose16(uint32_t (&v)[16], int lane) {
+#pragma unroll
+    for (int H = 8; H >= 1; H >>= 1) {
+        const bool up = (lane & H) != 0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            if (c & H) continue;
+            const uint32_t send = up ? v[c] : v[c + H];
+            const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, H);
+            if (up) v[c] = recv;
+            else v[c + H] = recv;
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
 __device__ __forceinline__ void tc_check_fail(const TcParams &p, int code, int u) {
@@ -145,6 +171,8 @@ pass_tc_kernel(const TcParams p) {
     float *rowscale = colS + 2 * 2 * 4 * 32;          // [2 runs][128] f16 GEMM1: 2^-(e_i + xexp) per row
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) TC_TRACE(0, 0, 0);          // kernel entry
+    if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) p.trace[kTraceTile + 4 * blockIdx.x] = gtimer();
     const int t0 = (int)((int64_t)blockIdx.x * p.T / p.G), t1 = (int)((int64_t)(blockIdx.x + 1) * p.T / p.G);
     if (t0 >= t1) return;
     const int U = t1 - t0;
@@ -233,6 +261,11 @@ pass_tc_kernel(const TcParams p) {
     // xi', Theta) are read only after this wait
     pdl_wait();
     pdl_trigger();
+    if (threadIdx.x == 0) TC_TRACE(0, 0, 4);          // predecessor complete
+    if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+        p.trace[kTraceTile + 4 * blockIdx.x + 1] = gtimer();
+        p.trace[kTraceTile + 4 * blockIdx.x + 3] = (unsigned long long)U;
+    }
     // TMEM columns: D1[2] 0..63 | Theta^k A operand [2] x (hi 32, lo 32) 64..191 | D2 (NP2) | Xi' hi, lo
     // (tf32: NK columns each; fp16: NK16 / 2 columns each, two K elements per column)
     const uint32_t c_d1 = 0, c_at = 64, c_d2 = 192, c_xi = 192 + (uint32_t)NP2;
@@ -444,8 +477,11 @@ pass_tc_kernel(const TcParams p) {
             const float *src = p.XiR + ((int64_t)rb * TBM + r) * NK;
             if constexpr (f16) {
                 // fp16 hi / lo of Xi' 2^e_r, e_r putting the row's largest |Xi'| just below 2^14
+                // (compile-time trip count: the NK loads go out together, not one dependent
+                // round trip per feature -- 12 us at n = 80 on the kernel's critical path)
                 float mx = 0.f;
-                for (int k = 0; k < p.n; ++k) mx = fmaxf(mx, fabsf(src[k]));
+#pragma unroll
+                for (int k = 0; k < NK; ++k) mx = fmaxf(mx, k < p.n ? fabsf(src[k]) : 0.f);
                 // mx < 2^E, E = biased exponent - 126 (mx normal); e = 14 - E, clamped so 2^e is a float
                 const int E = (int)((__float_as_uint(mx) >> 23) & 0xffu) - 126;
                 const int e = mx > 0.f ? min(14 - E, 120) : 0;
@@ -502,17 +538,23 @@ pass_tc_kernel(const TcParams p) {
             const int sl = slot0 + (c.rb - rbA);
             const bool first = sl != last_flush_slot;
             last_flush_slot = sl;
-            double *dst = p.rowpart + ((int64_t)sl * TBM + r) * W;
+            // each thread holds its row's 16 columns d0..d0+15; transposed inside each half-warp,
+            // one store instruction then writes 2 rows x 16 consecutive columns (whole 128-B lines,
+            // not 32 rows' scattered words: the scattered form stalled the CTA ~5-8 us per flush)
+            const int hl = lane & 15;
+            double *dst = p.rowpart + ((int64_t)sl * TBM + q * 32 + (lane & 16)) * W + hl;
 #pragma unroll 1
             for (int d0 = 0; d0 < NP2; d0 += 16) {
                 uint32_t a[16];
                 tmem_ld16(tmem + lane_off + c_d2 + (uint32_t)d0, a);
                 tmem_wait_ld();
+                transpose16(a, lane);                  // a[k] = (row q*32 + (lane & 16) + k, column d0 + hl)
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const double v = (double)__uint_as_float(a[e]);
-                    if (first) dst[d0 + e] = v;
-                    else dst[d0 + e] += v;
+                for (int k = 0; k < 16; ++k) {
+                    const double v = (double)__uint_as_float(a[k]);
+                    double *o = dst + (int64_t)k * W + d0;
+                    if (first) *o = v;
+                    else *o += v;
                 }
             }
             tc_fence_before();
@@ -696,6 +738,8 @@ pass_tc_kernel(const TcParams p) {
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) TC_TRACE(0, 0, 5);          // all roles done
+    if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) p.trace[kTraceTile + 4 * blockIdx.x + 2] = gtimer();
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
