@@ -553,8 +553,11 @@ pass_tc_kernel(const TcParams p) {
                 for (int k = 0; k < 16; ++k) {
                     const double v = (double)__uint_as_float(a[k]);
                     double *o = dst + (int64_t)k * W + d0;
+                    // later windows: a fire-and-forget fp64 atomic add (RED) -- same single IEEE add per
+                    // window in window order (one thread per element, same-address ordering), without
+                    // the read-modify-write's load round trip (~8k cycles per flush at n = 80)
                     if (first) *o = v;
-                    else *o += v;
+                    else atomicAdd(o, v);
                 }
             }
             tc_fence_before();
