@@ -93,8 +93,13 @@ struct Smem {
     static constexpr size_t bytes = o_pd + sizeof(double) * 16 * (PB > 1 ? PB * NT : NT);
 };
 
+// fp64: one CTA per SM so the register-blocked 4x4 fp64 tiles and row accumulators fit in
+// registers (capped at 128 for 2 CTAs, ptxas spilled ~1 KB per thread)
+template <typename T, int NB>
+constexpr int simt_min_blocks() { return sizeof(T) == 8 ? 1 : 2; }
+
 template <typename T, int NB, int NBP, int MODE>
-__global__ void __launch_bounds__(NT, 2) pass_simt_kernel(const PassParams p) {
+__global__ void __launch_bounds__(NT, simt_min_blocks<T, NB>()) pass_simt_kernel(const PassParams p) {
     using S = Smem<T, NB, NBP>;
     constexpr int NOB = S::NOB, PB = S::PB, KS = S::KS;
     extern __shared__ __align__(16) unsigned char smem[];

@@ -29,7 +29,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / it
-        print(f"simt {prec} N={N} n={n}: {ms * 1e3:.1f} us/iteration, {N * N / ms / 1e9:.3e} pairs/s")
+        print(f"simt {prec} N={N} n={n}: {ms * 1e3:.1f} us/iteration, {N * N / (ms * 1e-3):.3e} pairs/s")
         s.close()
 
 
