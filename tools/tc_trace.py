@@ -1,6 +1,10 @@
 """Per-tile timeline of CTA 0 of the tensor-core pass (debug; CR_TC_TRACE).
 
+    CR_NVCC_EXTRA=-DCR_TC_TRACE_BUILD python -c "import paper_1608_02227_b200.build as b; b.build(force=True)"
     python tools/tc_trace.py C3 [steps]
+
+The timeline events exist only in a trace build (-DCR_TC_TRACE_BUILD; production builds compile
+them out -- they cost the pass several percent), so build one in a copy of the tree.
 
 Runs `steps` eager dual steps of the config's problem (the last one's timeline is kept) and
 prints, per tile u of CTA 0, the clock64 offsets (in cycles from kernel entry) of each role's
