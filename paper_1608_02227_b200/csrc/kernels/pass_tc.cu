@@ -119,7 +119,7 @@ __device__ __forceinline__ void tc_check_fail(const TcParams &p, int code, int u
 
 // kernel variants (template MODE): plain, ring-protocol checks (TcParams::check), or the P2P y'
 // acquire fused into the producer with the own-columns-first rotation (TcParams::yflag)
-enum TcMode { TC_PLAIN = 0, TC_CHECK = 1, TC_P2PY = 2 };
+enum TcMode { TC_PLAIN = 0, TC_CHECK = 1, TC_P2PY = 2, TC_ADAPT = 3 };
 
 // Position of the u-th tile a CTA processes: segment k of its schedule (a row block rb and a
 // column-tile range [cbb, cbe)), column tile cb, and the slot / phase parity of the Theta ring
@@ -128,12 +128,22 @@ struct Cursor {
     int u, k, rb, cb, cbb, cbe, s, ph, x, xph, z, zph;
 };
 
-// debug timeline (p.trace != nullptr): clock64 of role events for the first 256 tiles of CTA 0
+// debug timeline (p.trace != nullptr): clock64 of role events for the first 256 tiles of CTA 0.
+// Compiled in only with -DCR_TC_TRACE_BUILD (CR_NVCC_EXTRA): the per-tile checks of p.trace and
+// the clock reads cost the production pass (ncu source view: their LDC / CS2R stalls).
+#ifdef CR_TC_TRACE_BUILD
 #define TC_TRACE(role, u, ev)                                                                   \
     do {                                                                                        \
         if (p.trace && blockIdx.x == 0 && (u) < 256)                                            \
             p.trace[((role) * 256 + (u)) * 8 + (ev)] = clock64();                               \
     } while (0)
+#define TC_TRACE_ON 1
+#else
+#define TC_TRACE(role, u, ev) \
+    do {                      \
+    } while (0)
+#define TC_TRACE_ON 0
+#endif
 
 // F16: GEMM1 in kind::f16 (TcParams::g1f16) -- a compile-time switch, so each instantiation keeps
 // one GEMM1 / Xi'-load code path (the kernel is instruction-cache sensitive: a runtime switch with
@@ -172,7 +182,7 @@ pass_tc_kernel(const TcParams p) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) TC_TRACE(0, 0, 0);          // kernel entry
-    if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) p.trace[kTraceTile + 4 * blockIdx.x] = gtimer();
+    if (TC_TRACE_ON && p.trace && threadIdx.x == 0 && blockIdx.x < 1024) p.trace[kTraceTile + 4 * blockIdx.x] = gtimer();
     const int t0 = (int)((int64_t)blockIdx.x * p.T / p.G), t1 = (int)((int64_t)(blockIdx.x + 1) * p.T / p.G);
     if (t0 >= t1) return;
     const int U = t1 - t0;
@@ -262,7 +272,7 @@ pass_tc_kernel(const TcParams p) {
     pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 0) TC_TRACE(0, 0, 4);          // predecessor complete
-    if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+    if (TC_TRACE_ON && p.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
         p.trace[kTraceTile + 4 * blockIdx.x + 1] = gtimer();
         p.trace[kTraceTile + 4 * blockIdx.x + 3] = (unsigned long long)U;
     }
@@ -467,7 +477,9 @@ pass_tc_kernel(const TcParams p) {
         int last_flush_slot = -1;
         double rrun = 0.0;                            // this warpgroup's row sum over the current run
         double drun = 0.0;                            // ... and sum of (Theta^k - theta~)^2 (adaptive step)
-        const bool adapt = p.adapt != 0;
+        // the adaptive-step sums are compiled out of the plain variant (a smaller epilogue loop;
+        // adaptive runs use TC_ADAPT, the check / P2P variants keep the runtime switch)
+        const bool adapt = MODE != TC_PLAIN && p.adapt != 0;
         float bi = 0.f;
         int cur_rb = -1;
         float *my_colS = colS + wg * 2 * 4 * 32;
@@ -569,7 +581,7 @@ pass_tc_kernel(const TcParams p) {
         Cursor c = start();
         if (wg == 1) adv(c, 1);
         if (wg == 0) load_xi(c.rb, 0);
-        const bool tr = (q == 0 && lane == 0);
+        [[maybe_unused]] const bool tr = (q == 0 && lane == 0);
         for (; c.u < U; adv(c, 2)) {
             const int b = c.u & 1;
             const int rb = c.rb, cb = acb(c.cb);
@@ -746,7 +758,7 @@ pass_tc_kernel(const TcParams p) {
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) TC_TRACE(0, 0, 5);          // all roles done
-    if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) p.trace[kTraceTile + 4 * blockIdx.x + 2] = gtimer();
+    if (TC_TRACE_ON && p.trace && threadIdx.x == 0 && blockIdx.x < 1024) p.trace[kTraceTile + 4 * blockIdx.x + 2] = gtimer();
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -797,9 +809,11 @@ cudaError_t launch_pass_tc(const TcParams &p, cudaStream_t s) {
         const size_t sm = (size_t)p.smem_bytes;                                                              \
         cudaError_t e = p.g1f16 ? (p.check   ? pdl_launch(pass_tc_kernel<V, true, TC_CHECK>, g, b, sm, s, p)  \
                                    : p.yflag ? pdl_launch(pass_tc_kernel<V, true, TC_P2PY>, g, b, sm, s, p)   \
+                                   : p.adapt ? pdl_launch(pass_tc_kernel<V, true, TC_ADAPT>, g, b, sm, s, p)  \
                                              : pdl_launch(pass_tc_kernel<V, true, TC_PLAIN>, g, b, sm, s, p)) \
                                 : (p.check   ? pdl_launch(pass_tc_kernel<V, false, TC_CHECK>, g, b, sm, s, p) \
                                    : p.yflag ? pdl_launch(pass_tc_kernel<V, false, TC_P2PY>, g, b, sm, s, p)  \
+                                   : p.adapt ? pdl_launch(pass_tc_kernel<V, false, TC_ADAPT>, g, b, sm, s, p) \
                                              : pdl_launch(pass_tc_kernel<V, false, TC_PLAIN>, g, b, sm, s, p)); \
         if (e != cudaSuccess) return e;                                                                      \
     } break;
@@ -821,6 +835,8 @@ cudaError_t pass_tc_prepare(int NK, int smem_bytes) {
         if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, true, TC_P2PY>, A, smem_bytes);    \
         if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, false, TC_CHECK>, A, smem_bytes);  \
         if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, false, TC_P2PY>, A, smem_bytes);   \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, true, TC_ADAPT>, A, smem_bytes);   \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(pass_tc_kernel<V, false, TC_ADAPT>, A, smem_bytes);  \
         return e;                                                                                            \
     }
         CR_TC_NK_LIST(CR_CASE)
