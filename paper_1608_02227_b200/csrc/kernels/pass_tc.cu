@@ -49,6 +49,7 @@ struct __align__(8) TcBarriers {
     uint64_t d1_full[2], d1_empty[2], at_full[2], at_empty[2];
     uint64_t d2_full, d2_empty, xi_full;
     uint32_t tmem_base;
+    uint32_t nzAT[2][4];         // per A-operand buffer, per epilogue warp: its 32 rows of Theta^k not all zero
     // CR_TC_CHECK tags: the tile index u (or run index) a slot / buffer holds, written by its
     // producer before the release (arrive) its consumer acquires (wait), checked after the wait
     int tagT[kTcMaxStages], tagX1[kTcMaxStages], tagX2[kTcMaxStages], tagAT[2], tagXi;
@@ -428,14 +429,20 @@ pass_tc_kernel(const TcParams p) {
                 // K-step jj (8 j) advances the start address by 2 lbo2 bytes
                 const uint64_t bh = smem_desc_u32(xh, lbo2, 128, 0), bl = smem_desc_u32(xh + g2_bytes, lbo2, 128, 0);
                 const uint32_t ws = window_start ? 1u : 0u;
+                // an all-zero Theta^k tile adds nothing to Theta X: its MMAs are skipped (exact), except
+                // at a window start, whose MMAs reset the accumulator (accumulate = 0)
+                const volatile uint32_t *nz = bar->nzAT[a];
+                const bool issue = window_start || ((nz[0] | nz[1] | nz[2] | nz[3]) != 0u);
+                if (issue) {
 #pragma unroll
-                for (int pass = 0; pass < 3; ++pass) {
-                    const uint64_t bd0 = pass == 1 ? bl : bh;
-                    const uint32_t a0 = tmu + c_at + (uint32_t)a * 64 + (pass == 2 ? 32u : 0u);
+                    for (int pass = 0; pass < 3; ++pass) {
+                        const uint64_t bd0 = pass == 1 ? bl : bh;
+                        const uint32_t a0 = tmu + c_at + (uint32_t)a * 64 + (pass == 2 ? 32u : 0u);
 #pragma unroll
-                    for (int jj = 0; jj < TBN / 8; ++jj)
-                        mma_tf32_ts_warp(tmu + c_d2, a0 + (uint32_t)jj * 8, bd0 + (uint64_t)(jj * 2 * lbo2 / 16), id2,
-                                         (pass | jj) != 0 ? 1u : (ws ^ 1u));
+                        for (int jj = 0; jj < TBN / 8; ++jj)
+                            mma_tf32_ts_warp(tmu + c_d2, a0 + (uint32_t)jj * 8, bd0 + (uint64_t)(jj * 2 * lbo2 / 16), id2,
+                                             (pass | jj) != 0 ? 1u : (ws ^ 1u));
+                    }
                 }
                 mma_commit_warp(&bar->at_empty[a]);
                 mma_commit_warp(&bar->g2empty[c.z]);
@@ -715,6 +722,11 @@ pass_tc_kernel(const TcParams p) {
             __syncwarp();
             if (tr) TC_TRACE(3 + wg, c.u, 4);
             tc_tag(p, if (q == 0 && lane == 0) bar->tagAT[b] = c.u);
+            {
+                // rows of Theta^k are >= 0, so a row is all zero iff its fp32 sum is 0
+                const uint32_t wnz = __any_sync(0xffffffffu, rtile != 0.f) ? 1u : 0u;
+                if (lane == 0) *reinterpret_cast<volatile uint32_t *>(&bar->nzAT[b][q]) = wnz;   // before the release below
+            }
             if (lane == 0) {
                 mbar_arrive(&bar->d1_empty[b]);
                 mbar_arrive(&bar->at_full[b]);
